@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the ProxyAttn hot path on B200: ms per attention layer at 128K tokens
+(Llama-3.1-8B attention shape) and speedup vs a dense kernel built in the same run
+(BASELINE.json "metric").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one whole pass of the hot path over one layer: proxyattn_estimate (A1-A6: pool,
+proxy lse, proxy max-pool, Alg. 1 budgets, Eq. 3 selection) + proxyattn_prefill (A7,
+tcgen05 block-sparse attention).  Inputs are resident in HBM; the L2 is flushed (a 256 MiB
+write, outside the timed events) before every timed step.  Each step is timed with CUDA
+events on the stream the kernels are launched on; the timed region is bracketed by a
+barrier + synchronize; the JSON value is the max over ranks.
+
+--impl reference runs the fp64 CPU oracle (oracle/, test infrastructure) on the host cores
+on a bounded sample of the same workload and extrapolates to ms per layer.
+
+N > 1 (torchrun): the layer's query heads are sharded by KV-head group across ranks
+(strong scaling).  With g = 1 (Llama) the single proxy group spans all ranks, so the
+pooled proxy sums are all-reduced (NCCL, the only exchange step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "ms per attention layer at 128K (Llama-3.1-8B shape) and speedup vs dense"
+WORKLOAD = dict(name="llama3.1-8b-attn-128k", n_q_heads=32, n_kv_heads=8, head_dim=128,
+                seq_len=131072, block_size=128, stride=4, n_groups=1, gamma=0.9,
+                min_budget_tokens=0, seed=0)
+L2_FLUSH_BYTES = 256 << 20
+KERNELS_PER_STEP = 8   # pool, proxy_lse, proxy_maxpool, budget_lse, budget_mass, finalize, select, attn
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "_source": "fallback (B200_PROFILING.md)"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.result = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = []
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                rows.append((float(f[0]), float(f[1]), f[3:7]))
+            except ValueError:
+                pass
+        if not rows:
+            return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
+        sm = [r[0] for r in rows]
+        self.result = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": rows[0][1],
+                       "samples": len(rows), "reasons": reasons}
+
+
+def build_config(pa, rank: int, ws: int, w=WORKLOAD):
+    Hq, Hkv, g = w["n_q_heads"], w["n_kv_heads"], w["n_groups"]
+    assert Hkv % ws == 0 or ws == 1, "shard count must divide the kv heads"
+    per = Hq // ws
+    b, e = (rank * per, (rank + 1) * per) if ws > 1 else (0, 0)
+    return pa.Config(Hq, Hkv, w["head_dim"], w["seq_len"], w["block_size"], w["stride"], g,
+                     w["gamma"], w["min_budget_tokens"], q_head_begin=b, q_head_end=e)
+
+
+def gen_inputs(w, device):
+    import workloads
+
+    return workloads.structured(w["n_q_heads"], w["n_kv_heads"], w["seq_len"], w["head_dim"],
+                                seed=w["seed"], device=device)
+
+
+# ------------------------------------------------------------------------ oracle --
+def oracle_sample(w, Q, K, V, cnt_full=None, budget_s=10.0):
+    """Time the fp64 CPU oracle on a bounded sample of the layer and extrapolate to a full
+    layer (ms).  Sample: proxy scores for a few block rows, Alg. 1 for one head, selection
+    on those rows, attention for a few (head, block-row) items."""
+    import oracle
+
+    oc = oracle.Cfg(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"],
+                    w["block_size"], w["stride"], w["n_groups"], w["gamma"],
+                    w["min_budget_tokens"], round_bf16=True)
+    M, bs, Ns = oc.M, oc.block_size // oc.stride, oc.Ns
+    Qf = Q.float().cpu().numpy()
+    Kf = K.float().cpu().numpy()
+    Vf = V.float().cpu().numpy()
+    t0 = time.perf_counter()
+    Pq, Pk, scale = oracle.pool(oc, Qf, Kf)
+    t_pool = time.perf_counter() - t0
+    rows = [M // 8, M // 2, M - 1]
+    t0 = time.perf_counter()
+    _, L = oracle.proxy_scores(oc, Pq, Pk, scale, rows=rows)
+    t_rows = time.perf_counter() - t0
+    logits_rows = sum(bs * (m * bs) + bs * (bs + 1) / 2 for m in rows)
+    logits_all = oc.n_groups * Ns * (Ns + 1) / 2
+    t_proxy = t_rows * logits_all / logits_rows
+    t0 = time.perf_counter()
+    ks, _, _, _ = oracle.budgets(oc, Qf, Kf, heads=[0])
+    t_budget = (time.perf_counter() - t0) * oc.n_q_heads
+    kst = np.full(oc.n_q_heads, max(int(ks[0]), 1), np.int32)
+    t0 = time.perf_counter()
+    cnt, idx, _ = oracle.select(oc, np.nan_to_num(L, nan=-np.inf), kst, rows=rows)
+    t_sel = (time.perf_counter() - t0) * M / len(rows)
+    items = np.array([[h, m] for h in (0, 17) for m in rows], np.int32).reshape(-1)
+    t0 = time.perf_counter()
+    oracle.attention(oc, Qf, Kf, Vf, cnt, idx, items=items)
+    t_att_s = time.perf_counter() - t0
+    sel_blocks = sum(int(cnt[h, m]) for h in (0, 17) for m in rows)
+    total_blocks = (int(cnt_full.sum()) if cnt_full is not None else
+                    sum(oracle.row_count(oc, int(kst[0]), m) for m in range(M)) * oc.n_q_heads)
+    t_att = t_att_s * total_blocks / max(sel_blocks, 1)
+    total = t_pool + t_proxy + t_budget + t_sel + t_att
+    sample = (f"pool full; proxy rows {rows} of {M} (x{logits_all / logits_rows:.0f} by logit "
+              f"count); Alg.1 head 0 (x{oc.n_q_heads}); select {len(rows)} rows; attention "
+              f"{len(items) // 2} (head,row) items (x{total_blocks / max(sel_blocks, 1):.0f} by "
+              f"selected blocks); extrapolated to one full layer")
+    return total * 1e3, sample, oracle.num_threads(), dict(
+        pool_s=t_pool, proxy_s=t_proxy, budget_s=t_budget, select_s=t_sel, attention_s=t_att)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    w = WORKLOAD
+    Q, K, V, meta = gen_inputs(w, "cpu")
+    vals = []
+    sample = cores = None
+    for i in range(args.warmup + args.steps):
+        ms, sample, cores, parts = oracle_sample(w, Q, K, V)
+        if i >= args.warmup:
+            vals.append(ms)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["name"], **{k: w[k] for k in w if k != "name"}},
+        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- ours --
+def run_ours(args):
+    import paper_2509_24745_b200 as pa
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = dict(WORKLOAD)
+    if args.seq_len:
+        w["seq_len"] = args.seq_len
+        w["name"] = f"llama3.1-8b-attn-{args.seq_len // 1024}k"
+    cfg = build_config(pa, rank, ws, w)
+    Q, K, V, meta = gen_inputs(w, dev)
+    hb, he = cfg.local_heads
+    r = cfg.r
+    Ql = Q[hb:he].contiguous()
+    Kl = K[hb // r:he // r].contiguous()
+    Vl = V[hb // r:he // r].contiguous()
+    M = cfg.M
+    Hl = cfg.Hl
+    wsp = pa.alloc_workspace(cfg, dev)
+    kstar = torch.empty(Hl, dtype=torch.int32, device=dev)
+    budget = torch.empty(Hl, dtype=torch.float32, device=dev)
+    cnt = torch.empty(Hl, M, dtype=torch.int32, device=dev)
+    idx = torch.empty(Hl, M, M, dtype=torch.int32, device=dev)
+    O = torch.empty_like(Ql)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    group_split = ws > 1 and cfg.n_groups < ws
+
+    def estimate():
+        if group_split:   # proxy group spans ranks: pool -> all-reduce -> scores
+            import torch.distributed as dist
+
+            qsum, ksum = pa.pool(cfg, Ql, Kl)
+            dist.all_reduce(qsum)
+            dist.all_reduce(ksum)
+            L = pa.proxy_scores(cfg, qsum, ksum, wsp)
+            pa._lib._check(pa.lib().proxyattn_budgets(
+                pa._lib._cfg_ref(cfg), pa._lib._ptr(Ql), pa._lib._ptr(Kl), pa._lib._ptr(wsp),
+                wsp.numel(), pa._lib._ptr(kstar), pa._lib._ptr(budget), pa._lib._stream(dev)))
+            pa._lib._check(pa.lib().proxyattn_select(
+                pa._lib._cfg_ref(cfg), pa._lib._ptr(L), pa._lib._ptr(kstar), pa._lib._ptr(cnt),
+                pa._lib._ptr(idx), pa._lib._stream(dev)))
+        else:
+            pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
+
+    def prefill():
+        pa.prefill(cfg, Ql, Kl, Vl, cnt, idx, O)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    st = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        flush.zero_()
+        estimate()
+        prefill()
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()                    # L2 flush, outside the events
+            ev[i][0].record(st)
+            estimate()
+            ev[i][1].record(st)
+            prefill()
+            ev[i][2].record(st)
+        barrier()
+    est_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    att_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    step_ms = [a + b for a, b in zip(est_ms, att_ms)]
+    total_ms = float(np.sum(step_ms))
+
+    # dense baseline (same run, same inputs), fewer iterations
+    dense_ms = []
+    Od = torch.empty_like(Ql)
+    for i in range(args.warmup + max(2, args.steps // 2)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        pa.dense_prefill(cfg, Ql, Kl, Vl, Od)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            dense_ms.append(e0.elapsed_time(e1))
+    dense = float(np.mean(dense_ms))
+
+    # max over ranks
+    vec = torch.tensor([total_ms / args.steps, float(np.mean(est_ms)), float(np.mean(att_ms)), dense],
+                       dtype=torch.float64, device=dev)
+    sel_blocks = float(cnt.sum().item())
+    blocks_t = torch.tensor([sel_blocks], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(blocks_t, op=dist.ReduceOp.SUM)
+    layer_ms, est_m, att_m, dense_m = vec.tolist()
+    total_blocks = blocks_t.item()
+
+    # e2e through the C-ABI host path (H2D of Q/K/V and D2H of O inside the timed region)
+    e2e = None
+    if ws == 1 and not args.no_e2e:
+        Qh = Q.cpu().pin_memory()
+        Kh = K.cpu().pin_memory()
+        Vh = V.cpu().pin_memory()
+        Oh = torch.empty_like(Qh).pin_memory()
+        ksh = torch.empty(cfg.n_q_heads, dtype=torch.int32).pin_memory()
+        del wsp
+        torch.cuda.empty_cache()
+        dws = torch.empty(pa.forward_host_workspace_bytes(cfg), dtype=torch.uint8, device=dev)
+        pa.forward_host(cfg, Qh, Kh, Vh, Oh, dws, ksh)
+        ts = []
+        for _ in range(max(2, args.steps // 2)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pa.forward_host(cfg, Qh, Kh, Vh, Oh, dws, ksh)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        h2d = (Qh.numel() + Kh.numel() + Vh.numel()) * 2
+        d2h = Oh.numel() * 2 + ksh.numel() * 4
+        e2e = {"value": float(np.mean(ts)), "unit": "ms", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+        del dws
+
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+
+    Mfull = M
+    dense_blocks = w["n_q_heads"] * Mfull * (Mfull + 1) / 2
+    sparsity = 1.0 - total_blocks / dense_blocks
+    b, d = w["block_size"], w["head_dim"]
+    flops_exec = 4.0 * b * b * d * total_blocks / ws      # per rank (attention kernel)
+    pk = peaks()
+    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    achieved = flops_exec / (att_m * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(w["name"])
+        except Exception:
+            traffic = None
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        ms, sample, cores, parts = oracle_sample(w, Q.cpu(), K.cpu(), V.cpu(), cnt.cpu().numpy())
+        cpu = {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample}
+    clocks = getattr(clk, "result", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []})
+    line = {
+        "metric": METRIC,
+        "value": layer_ms,
+        "unit": "ms",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": layer_ms,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (structured generator, SURVEY §8d; seed 0; inputs resident in HBM)",
+        "config": {"workload": w["name"], "heads": f"{w['n_q_heads']}/{w['n_kv_heads']}",
+                   "head_dim": d, "seq_len": w["seq_len"], "block": b, "stride": w["stride"],
+                   "proxy_groups": w["n_groups"], "gamma": w["gamma"],
+                   "min_budget_tokens": w["min_budget_tokens"],
+                   "parallelism": f"head-group x{ws}" if ws > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "speedup_vs_dense": dense_m / layer_ms,
+        "dense_ms": dense_m,
+        "estimate_ms": est_m,
+        "prefill_ms": att_m,
+        "sparsity": sparsity,
+        "tflops_exec": achieved,
+        "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (A7)", "achieved": achieved,
+                     "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
+                     "traffic": traffic,
+                     "peak_source": pk["_source"] + " bf16_tflops_sustained",
+                     "algorithmic": "4*b^2*d FLOP per executed (head,row,block) = 8.39 MFLOP"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq-len", type=int, default=0, help="override N (sweep)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

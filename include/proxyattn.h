@@ -1,0 +1,162 @@
+/*
+ * proxyattn.h — C-ABI of libproxyattn, the B200 (sm_100a) hot path of ProxyAttn
+ * (arXiv 2509.24745, "ProxyAttn: Guided Sparse Attention via Representative Heads").
+ *
+ * Citations: P:<line> = PAPER.md line (section / equation), S:<line> = SPEC.md line.
+ * Steps A1-A8 are SURVEY.md §8(a); readings Z1-Z23 are listed in DESIGN.md.
+ *
+ * Conventions (every entry point):
+ *  - All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors), contiguous,
+ *    16-byte aligned.  Layout is head-major: Q [Hl][N][d], K/V [Hkv_l][N][d], O [Hl][N][d],
+ *    where Hl = q_head_end - q_head_begin is the local query-head shard and Hkv_l = Hl / r
+ *    (r = Hq/Hkv) the kv heads it uses, starting at kv head q_head_begin / r.
+ *  - Element type: bf16 (__nv_bfloat16) by default; fp32 when PROXYATTN_FLAG_FP32_DEBUG.
+ *  - Per-head outputs (kstar, budget, block_cnt, block_idx) are indexed by local head.
+ *  - All work is enqueued on `stream` (a cudaStream_t, passed as void*); no call
+ *    synchronises the host except proxyattn_forward_host.
+ *  - The library allocates no device memory: scratch comes from the caller's workspace.
+ *  - Return codes: PROXYATTN_OK or one of the negative PROXYATTN_E_* codes; a
+ *    human-readable reason is available from proxyattn_last_error() (thread-local).
+ *    Validation errors are raised before anything is enqueued.
+ *  - Determinism: identical inputs give bit-identical outputs (no float atomics,
+ *    fixed reduction orders).
+ */
+#ifndef PROXYATTN_H
+#define PROXYATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- config -- */
+
+/* AttnConfig.  Invariants: Hq % Hkv == 0, Hkv % g == 0, b % s == 0,
+ * N % b == 0 (Z19), 0 < gamma <= 1, min_budget_tokens >= 0.
+ * bf16 build supports d == 128, b == 128; FP32_DEBUG supports d % 32 == 0, d <= 128,
+ * any b with b % s == 0 (SIMT kernels, for the 1e-4 parity contract). */
+typedef struct {
+    int32_t  n_q_heads;          /* Hq (global) */
+    int32_t  n_kv_heads;         /* Hkv (global) */
+    int32_t  head_dim;           /* d */
+    int64_t  seq_len;            /* N */
+    int32_t  block_size;         /* b (Z18) */
+    int32_t  stride;             /* s, strided q/k sampling */
+    int32_t  n_groups;           /* g, proxy heads */
+    float    gamma;              /* cumulative threshold of Alg. 1 */
+    int32_t  min_budget_tokens;  /* per-row floor ceil(tokens/b) blocks (Z13/Z14) */
+    uint32_t flags;              /* PROXYATTN_FLAG_* */
+    int32_t  q_head_begin;       /* local shard [begin, end) of query heads; end == 0 means all */
+    int32_t  q_head_end;
+} proxyattn_cfg;
+
+#define PROXYATTN_FLAG_FP32_DEBUG  0x1u  /* fp32 Q/K/V/O, SIMT FFMA kernels (1e-4 contract)   */
+#define PROXYATTN_FLAG_CHECK       0x2u  /* prefill validates block lists on the device (E_SHAPE) */
+
+#define PROXYATTN_OK               0
+#define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */
+#define PROXYATTN_E_UNSUPPORTED   -2  /* head_dim / block size not supported by this build        */
+#define PROXYATTN_E_SHAPE         -3  /* invalid block list (empty, unsorted, out of range, acausal) */
+#define PROXYATTN_E_WORKSPACE     -4  /* workspace missing or too small                             */
+#define PROXYATTN_E_CUDA          -5  /* CUDA launch / runtime failure                              */
+
+/* ------------------------------------------------------------- workspace -- */
+
+/* Bytes of device scratch proxyattn_estimate needs (pooled proxies, row log-sum-exps,
+ * the log-domain block map, budget partials).  Returns E_CONFIG on an invalid config. */
+int proxyattn_workspace_bytes(const proxyattn_cfg* cfg, size_t* out_bytes);
+
+/* ------------------------------------------------------- fused estimate -- */
+
+/* A1-A6: proxy pooling (Eq. 2), strided sampling, proxy block
+ * scores (Eq. 1), Alg. 1 budgets and Eq. 3 per-head top-k masks
+ * (P:308-320).  Inputs Q, K (local shard layout above).  Outputs, all device memory:
+ *   kstar     [Hl]        int32   K*_h, blocks needed by the last query block (1..M)
+ *   budget    [Hl]        float   b_h = K*_h / M
+ *   block_cnt [Hl][M]     int32   K_{h,m} = min(m+1, max(ceil(K*_h (m+1)/M), F, 1)) (Z12)
+ *   block_idx [Hl][M][M]  int32   row stride M; first block_cnt entries valid, ascending,
+ *                                 diagonal block m always included (Z15)
+ * Requires every proxy group touched by the shard to be fully inside it (else E_CONFIG;
+ * use the staged entries with an all-reduce of the pooled sums instead). */
+int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                       void* workspace, size_t workspace_bytes,
+                       int32_t* kstar, float* budget, int32_t* block_cnt, int32_t* block_idx,
+                       void* stream);
+
+/* ---------------------------------------------------------------- attention -- */
+
+/* A7: block-sparse causal attention.  For every local head
+ * h and query block m: O[h][t] = softmax over keys k in the listed blocks with k <= t of
+ * Q[h][t]·K[kv(h)][k]/sqrt(d), times V.  Accepts ANY valid lists (non-empty, ascending,
+ * in range, n <= m), so oracle masks can be injected.  With PROXYATTN_FLAG_CHECK the
+ * lists are validated on the device first and E_SHAPE is returned on a violation
+ * (this flag synchronises the stream). */
+int proxyattn_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
+                      const int32_t* block_cnt, const int32_t* block_idx, void* O,
+                      void* stream);
+
+/* A8: dense causal attention, the same engine with every causal block;
+ * the same-run baseline for "speedup vs dense". */
+int proxyattn_dense_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                            const void* V, void* O, void* stream);
+
+/* ---------------------------------------------------------- staged entries -- */
+
+/* A1 (Eq. 2 + stride): fp32 pooled SUMS over the shard's heads, qsum/ksum [g_l][N/s][d],
+ * g_l = proxy groups touched by the shard.  With g < #shards the sums are partial and the
+ * caller all-reduces them (the only cross-GPU step). */
+int proxyattn_pool(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                   float* qsum, float* ksum, void* stream);
+
+/* A2-A3 (Eq. 1): from complete fp32 pooled sums, rounds them to the proxy precision
+ * (bf16 RNE; fp32 in FP32_DEBUG), then writes the log-domain block map
+ * L [g_l][M][M] float, L[c][m][n] = max over sampled i in block m, j in block n, j <= i of
+ * z_ij - lse_i (Z6), -inf for n > m.  Uses the workspace of proxyattn_workspace_bytes. */
+int proxyattn_proxy_scores(const proxyattn_cfg* cfg, const float* qsum, const float* ksum,
+                           void* workspace, size_t workspace_bytes, float* L, void* stream);
+
+/* A4 (Alg. 1): per local head, kstar/budget from its own last-block queries (Z7-Z11). */
+int proxyattn_budgets(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                      void* workspace, size_t workspace_bytes,
+                      int32_t* kstar, float* budget, void* stream);
+
+/* A5-A6 (Eq. 3): per (local head, block row) top-K_{h,m} columns of the shared row of L,
+ * diagonal forced and counted, ties to the lower index (Z15, Z17), emitted ascending. */
+int proxyattn_select(const proxyattn_cfg* cfg, const float* L, const int32_t* kstar,
+                     int32_t* block_cnt, int32_t* block_idx, void* stream);
+
+/* -------------------------------------------------------------- host path -- */
+
+/* End-to-end call on HOST buffers (pinned or pageable): copies Q/K/V to the device
+ * workspace, runs estimate + prefill, copies O (and kstar when non-NULL) back, and
+ * synchronises `stream` before returning.  device_ws must hold
+ * proxyattn_forward_host_workspace_bytes(cfg) bytes. */
+int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out_bytes);
+int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const void* K_host,
+                           const void* V_host, void* O_host, int32_t* kstar_host,
+                           void* device_ws, size_t device_ws_bytes, void* stream);
+
+/* ----------------------------------------------------------------- misc -- */
+
+/* §3.1 cost model: g / (Hq * s^2). */
+double proxyattn_cost_ratio(const proxyattn_cfg* cfg);
+
+/* Thread-local message for the last non-zero return code. */
+const char* proxyattn_last_error(void);
+
+/* Library build id (compile flags / arch), for logs. */
+const char* proxyattn_build_info(void);
+
+/* Diagnostic: one 128x128x128 tcgen05 GEMM tile of each operand mode the attention
+ * kernel uses, on bf16 inputs A [128][128], B [128][128]:
+ *   C_ss [128][128] = A · B^T  (A, B K-major in shared memory, TMA SWIZZLE_128B)
+ *   C_ts [128][128] = A · B    (A staged in TMEM via tcgen05.st, B MN-major in shared memory)
+ * fp32 outputs.  Used by the GPU tests to pin the descriptor encodings. */
+int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROXYATTN_H */

@@ -1,0 +1,286 @@
+"""ctypes binding of libproxyattn (include/proxyattn.h) — argument marshalling only.
+
+Every compute step runs in the CUDA kernels behind the C-ABI; this module only turns
+torch tensors into device pointers and the current CUDA stream into a cudaStream_t.
+It fails loudly when the shared library is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, replace
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_PKG, "libproxyattn.so")
+
+FLAG_FP32_DEBUG = 0x1
+FLAG_CHECK = 0x2
+
+OK = 0
+E_CONFIG = -1
+E_UNSUPPORTED = -2
+E_SHAPE = -3
+E_WORKSPACE = -4
+E_CUDA = -5
+
+
+class ProxyAttnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"proxyattn error {code}: {msg}")
+        self.code = code
+
+
+class _CCfg(ctypes.Structure):
+    _fields_ = [
+        ("n_q_heads", ctypes.c_int32),
+        ("n_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("seq_len", ctypes.c_int64),
+        ("block_size", ctypes.c_int32),
+        ("stride", ctypes.c_int32),
+        ("n_groups", ctypes.c_int32),
+        ("gamma", ctypes.c_float),
+        ("min_budget_tokens", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+        ("q_head_begin", ctypes.c_int32),
+        ("q_head_end", ctypes.c_int32),
+    ]
+
+
+@dataclass(frozen=True)
+class Config:
+    """proxyattn_cfg (S:27-34 AttnConfig plus the build flags and the head shard)."""
+
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    seq_len: int
+    block_size: int = 128
+    stride: int = 4
+    n_groups: int = 1
+    gamma: float = 0.9
+    min_budget_tokens: int = 0
+    fp32_debug: bool = False
+    check: bool = False
+    q_head_begin: int = 0
+    q_head_end: int = 0
+
+    @property
+    def M(self) -> int:
+        return self.seq_len // self.block_size
+
+    @property
+    def r(self) -> int:
+        return self.n_q_heads // self.n_kv_heads
+
+    @property
+    def local_heads(self) -> tuple[int, int]:
+        return self.q_head_begin, (self.q_head_end or self.n_q_heads)
+
+    @property
+    def Hl(self) -> int:
+        b, e = self.local_heads
+        return e - b
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return torch.float32 if self.fp32_debug else torch.bfloat16
+
+    def replace(self, **kw) -> "Config":
+        return replace(self, **kw)
+
+    def c(self) -> _CCfg:
+        flags = (FLAG_FP32_DEBUG if self.fp32_debug else 0) | (FLAG_CHECK if self.check else 0)
+        return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
+                     self.block_size, self.stride, self.n_groups, float(self.gamma),
+                     self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end)
+
+
+_lib = None
+_P = ctypes.c_void_p
+_CP = ctypes.POINTER(_CCfg)
+
+_SIGS = {
+    "proxyattn_workspace_bytes": ([_CP, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "proxyattn_estimate": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_prefill": ([_CP, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_dense_prefill": ([_CP, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_pool": ([_CP, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_proxy_scores": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P], ctypes.c_int),
+    "proxyattn_budgets": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P, _P], ctypes.c_int),
+    "proxyattn_select": ([_CP, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_forward_host_workspace_bytes": ([_CP, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "proxyattn_forward_host": ([_CP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "proxyattn_cost_ratio": ([_CP], ctypes.c_double),
+    "proxyattn_last_error": ([], ctypes.c_char_p),
+    "proxyattn_build_info": ([], ctypes.c_char_p),
+    "proxyattn_debug_umma": ([_P, _P, _P, _P, _P], ctypes.c_int),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def lib() -> ctypes.CDLL:
+    """Load libproxyattn.so (built by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(
+                f"{SO_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(SO_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        raise ProxyAttnError(rc, lib().proxyattn_last_error().decode())
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _cfg_ref(cfg: Config):
+    return ctypes.byref(cfg.c())
+
+
+def workspace_bytes(cfg: Config) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().proxyattn_workspace_bytes(_cfg_ref(cfg), ctypes.byref(n)))
+    return n.value
+
+
+def alloc_workspace(cfg: Config, device) -> torch.Tensor:
+    return torch.empty(workspace_bytes(cfg), dtype=torch.uint8, device=device)
+
+
+def estimate(cfg: Config, Q: torch.Tensor, K: torch.Tensor, workspace: torch.Tensor | None = None,
+             out: tuple | None = None):
+    """proxyattn_estimate -> (kstar [Hl] i32, budget [Hl] f32, block_cnt [Hl][M] i32,
+    block_idx [Hl][M][M] i32)."""
+    dev = Q.device
+    if workspace is None:
+        workspace = alloc_workspace(cfg, dev)
+    if out is None:
+        Hl, M = cfg.Hl, cfg.M
+        out = (torch.empty(Hl, dtype=torch.int32, device=dev),
+               torch.empty(Hl, dtype=torch.float32, device=dev),
+               torch.empty(Hl, M, dtype=torch.int32, device=dev),
+               torch.empty(Hl, M, M, dtype=torch.int32, device=dev))
+    kstar, budget, cnt, idx = out
+    _check(lib().proxyattn_estimate(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(workspace),
+                                    workspace.numel(), _ptr(kstar), _ptr(budget), _ptr(cnt),
+                                    _ptr(idx), _stream(dev)))
+    return kstar, budget, cnt, idx
+
+
+def prefill(cfg: Config, Q, K, V, block_cnt, block_idx, O=None):
+    """proxyattn_prefill -> O [Hl][N][d]."""
+    if O is None:
+        O = torch.empty_like(Q)
+    _check(lib().proxyattn_prefill(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(block_cnt),
+                                   _ptr(block_idx), _ptr(O), _stream(Q.device)))
+    return O
+
+
+def dense_prefill(cfg: Config, Q, K, V, O=None):
+    """proxyattn_dense_prefill -> O [Hl][N][d]."""
+    if O is None:
+        O = torch.empty_like(Q)
+    _check(lib().proxyattn_dense_prefill(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                                         _stream(Q.device)))
+    return O
+
+
+def pool(cfg: Config, Q, K):
+    """proxyattn_pool -> fp32 (qsum, ksum) [g_l][N/s][d]."""
+    gl = _local_groups(cfg)
+    shape = (gl, cfg.seq_len // cfg.stride, cfg.head_dim)
+    qsum = torch.empty(shape, dtype=torch.float32, device=Q.device)
+    ksum = torch.empty_like(qsum)
+    _check(lib().proxyattn_pool(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(qsum), _ptr(ksum),
+                                _stream(Q.device)))
+    return qsum, ksum
+
+
+def proxy_scores(cfg: Config, qsum, ksum, workspace=None):
+    """proxyattn_proxy_scores -> L [g_l][M][M] fp32 (log domain, -inf above the diagonal)."""
+    if workspace is None:
+        workspace = alloc_workspace(cfg, qsum.device)
+    L = torch.empty(_local_groups(cfg), cfg.M, cfg.M, dtype=torch.float32, device=qsum.device)
+    _check(lib().proxyattn_proxy_scores(_cfg_ref(cfg), _ptr(qsum), _ptr(ksum), _ptr(workspace),
+                                        workspace.numel(), _ptr(L), _stream(qsum.device)))
+    return L
+
+
+def budgets(cfg: Config, Q, K, workspace=None):
+    """proxyattn_budgets -> (kstar [Hl] i32, budget [Hl] f32)."""
+    if workspace is None:
+        workspace = alloc_workspace(cfg, Q.device)
+    kstar = torch.empty(cfg.Hl, dtype=torch.int32, device=Q.device)
+    budget = torch.empty(cfg.Hl, dtype=torch.float32, device=Q.device)
+    _check(lib().proxyattn_budgets(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(workspace),
+                                   workspace.numel(), _ptr(kstar), _ptr(budget),
+                                   _stream(Q.device)))
+    return kstar, budget
+
+
+def select(cfg: Config, L, kstar):
+    """proxyattn_select -> (block_cnt [Hl][M], block_idx [Hl][M][M])."""
+    cnt = torch.empty(cfg.Hl, cfg.M, dtype=torch.int32, device=L.device)
+    idx = torch.empty(cfg.Hl, cfg.M, cfg.M, dtype=torch.int32, device=L.device)
+    _check(lib().proxyattn_select(_cfg_ref(cfg), _ptr(L), _ptr(kstar), _ptr(cnt), _ptr(idx),
+                                  _stream(L.device)))
+    return cnt, idx
+
+
+def forward_host_workspace_bytes(cfg: Config) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().proxyattn_forward_host_workspace_bytes(_cfg_ref(cfg), ctypes.byref(n)))
+    return n.value
+
+
+def forward_host(cfg: Config, Qh, Kh, Vh, Oh, device_ws, kstar_h=None):
+    """proxyattn_forward_host on host (CPU, ideally pinned) tensors; synchronises."""
+    _check(lib().proxyattn_forward_host(_cfg_ref(cfg), _ptr(Qh), _ptr(Kh), _ptr(Vh), _ptr(Oh),
+                                        _ptr(kstar_h), _ptr(device_ws), device_ws.numel(),
+                                        _stream(device_ws.device)))
+    return Oh
+
+
+def cost_ratio(cfg: Config) -> float:
+    return lib().proxyattn_cost_ratio(_cfg_ref(cfg))
+
+
+def build_info() -> str:
+    return lib().proxyattn_build_info().decode()
+
+
+def debug_umma(A: torch.Tensor, B: torch.Tensor):
+    """proxyattn_debug_umma -> (C_ss = A B^T, C_ts = A B), fp32 [128][128]."""
+    Css = torch.empty(128, 128, dtype=torch.float32, device=A.device)
+    Cts = torch.empty_like(Css)
+    _check(lib().proxyattn_debug_umma(_ptr(A), _ptr(B), _ptr(Css), _ptr(Cts), _stream(A.device)))
+    return Css, Cts
+
+
+def _local_groups(cfg: Config) -> int:
+    b, e = cfg.local_heads
+    gq = cfg.n_q_heads // cfg.n_groups
+    return (e - 1) // gq - b // gq + 1

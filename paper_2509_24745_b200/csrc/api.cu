@@ -1,0 +1,328 @@
+// api.cu — the extern "C" boundary of libproxyattn (include/proxyattn.h): validation,
+// workspace carve-up and kernel launches.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/proxyattn.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(PROXYATTN_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define PA_CUDA(expr, where)                      \
+    do {                                          \
+        cudaError_t _e = (expr);                  \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+// O1: validate the config and derive every size the kernels need.
+int derive(const proxyattn_cfg* c, pa::Dims& D) {
+    if (!c) return fail(PROXYATTN_E_CONFIG, "cfg is NULL");
+    if (c->n_q_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 || c->seq_len <= 0 ||
+        c->block_size <= 0 || c->stride <= 0 || c->n_groups <= 0)
+        return fail(PROXYATTN_E_CONFIG, "non-positive dimension");
+    if (c->n_q_heads % c->n_kv_heads)
+        return fail(PROXYATTN_E_CONFIG, "n_q_heads %% n_kv_heads != 0 (S:30)");
+    if (c->n_kv_heads % c->n_groups)
+        return fail(PROXYATTN_E_CONFIG, "n_kv_heads %% n_groups != 0 (S:31)");
+    if (c->block_size % c->stride)
+        return fail(PROXYATTN_E_CONFIG, "block_size %% stride != 0 (S:32)");
+    if (c->seq_len % c->block_size)
+        return fail(PROXYATTN_E_CONFIG, "seq_len %% block_size != 0 (Z19: padding not supported)");
+    if (!(c->gamma > 0.f && c->gamma <= 1.f))
+        return fail(PROXYATTN_E_CONFIG, "gamma must be in (0, 1] (S:33)");
+    if (c->min_budget_tokens < 0) return fail(PROXYATTN_E_CONFIG, "min_budget_tokens < 0");
+    D.fp32 = (c->flags & PROXYATTN_FLAG_FP32_DEBUG) != 0;
+    if (D.fp32) {
+        if (c->head_dim % 32 || c->head_dim > 128)
+            return fail(PROXYATTN_E_UNSUPPORTED, "FP32_DEBUG needs head_dim %% 32 == 0 and <= 128");
+    } else {
+        if (c->head_dim != 128) return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs head_dim == 128");
+        if (c->block_size != 128) return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs block_size == 128");
+    }
+    if (c->seq_len / c->block_size > (1 << 20)) return fail(PROXYATTN_E_UNSUPPORTED, "too many blocks");
+    D.Hq = c->n_q_heads;
+    D.Hkv = c->n_kv_heads;
+    D.d = c->head_dim;
+    D.b = c->block_size;
+    D.s = c->stride;
+    D.g = c->n_groups;
+    D.r = D.Hq / D.Hkv;
+    D.N = c->seq_len;
+    D.M = static_cast<int>(D.N / D.b);
+    D.Ns = D.N / D.s;
+    D.bs = D.b / D.s;
+    D.gamma = c->gamma;
+    D.flags = c->flags;
+    D.F = (c->min_budget_tokens + D.b - 1) / D.b;
+    D.gq = D.Hq / D.g;
+    D.gk = D.Hkv / D.g;
+    D.qb = c->q_head_begin;
+    D.qe = c->q_head_end == 0 ? D.Hq : c->q_head_end;
+    if (D.qb < 0 || D.qe > D.Hq || D.qb >= D.qe)
+        return fail(PROXYATTN_E_CONFIG, "bad shard [%d, %d)", D.qb, D.qe);
+    if (D.qb % D.r || D.qe % D.r)
+        return fail(PROXYATTN_E_CONFIG, "shard must align to kv heads (r = %d)", D.r);
+    D.Hl = D.qe - D.qb;
+    D.kvb = D.qb / D.r;
+    D.Hkvl = D.Hl / D.r;
+    D.gb = pa::group_of_q(D, D.qb);
+    D.gl = pa::group_of_q(D, D.qe - 1) - D.gb + 1;
+    return PROXYATTN_OK;
+}
+
+bool groups_complete(const pa::Dims& D) { return D.qb % D.gq == 0 && D.qe % D.gq == 0; }
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+template <typename T>
+T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+int run_proxy_from_pooled(const pa::Dims& D, void* Pq, void* Pk, void* ws, const pa::Workspace& W,
+                          float* L, cudaStream_t st) {
+    float* lse = at<float>(ws, W.lse);
+    if (pa::score_tc_supported(D)) {
+        PA_CUDA(pa::launch_proxy_tc(D, Pq, Pk, at<float>(ws, W.scratch), lse, L, st), "proxy_tc");
+        return PROXYATTN_OK;
+    }
+    PA_CUDA(pa::launch_proxy_lse(D, Pq, Pk, lse, st), "proxy_lse");
+    PA_CUDA(pa::launch_proxy_maxpool(D, Pq, Pk, lse, L, st), "proxy_maxpool");
+    return PROXYATTN_OK;
+}
+
+int run_budgets(const pa::Dims& D, const void* Q, const void* K, void* ws, const pa::Workspace& W,
+                int32_t* kstar, float* budget, cudaStream_t st) {
+    float* blse = at<float>(ws, W.blse);
+    float* bmass = at<float>(ws, W.bmass);
+    if (pa::score_tc_supported(D)) {
+        PA_CUDA(pa::launch_budget_tc(D, Q, K, at<float>(ws, W.scratch), bmass, st), "budget_tc");
+    } else {
+        PA_CUDA(pa::launch_budget_lse(D, Q, K, blse, st), "budget_lse");
+        PA_CUDA(pa::launch_budget_mass(D, Q, K, blse, bmass, st), "budget_mass");
+    }
+    PA_CUDA(pa::launch_budget_finalize(D, bmass, kstar, budget, st), "budget_finalize");
+    return PROXYATTN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int proxyattn_workspace_bytes(const proxyattn_cfg* cfg, size_t* out) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!out) return fail(PROXYATTN_E_CONFIG, "out is NULL");
+    *out = pa::workspace_layout(D).total;
+    return PROXYATTN_OK;
+}
+
+int proxyattn_pool(const proxyattn_cfg* cfg, const void* Q, const void* K, float* qsum,
+                   float* ksum, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!Q || !K || !qsum || !ksum) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    PA_CUDA(pa::launch_pool(D, Q, K, qsum, ksum, nullptr, nullptr, S(stream)), "pool");
+    return PROXYATTN_OK;
+}
+
+int proxyattn_proxy_scores(const proxyattn_cfg* cfg, const float* qsum, const float* ksum,
+                           void* ws, size_t ws_bytes, float* L, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    const pa::Workspace W = pa::workspace_layout(D);
+    if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
+    if (!qsum || !ksum || !L) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    void* Pq = at<char>(ws, W.pq);
+    void* Pk = at<char>(ws, W.pk);
+    PA_CUDA(pa::launch_round_proxies(D, qsum, ksum, Pq, Pk, S(stream)), "round_proxies");
+    return run_proxy_from_pooled(D, Pq, Pk, ws, W, L, S(stream));
+}
+
+int proxyattn_budgets(const proxyattn_cfg* cfg, const void* Q, const void* K, void* ws,
+                      size_t ws_bytes, int32_t* kstar, float* budget, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    const pa::Workspace W = pa::workspace_layout(D);
+    if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
+    if (!Q || !K || !kstar || !budget) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    return run_budgets(D, Q, K, ws, W, kstar, budget, S(stream));
+}
+
+int proxyattn_select(const proxyattn_cfg* cfg, const float* L, const int32_t* kstar,
+                     int32_t* block_cnt, int32_t* block_idx, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!L || !kstar || !block_cnt || !block_idx) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, S(stream)), "select");
+    return PROXYATTN_OK;
+}
+
+int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, void* ws,
+                       size_t ws_bytes, int32_t* kstar, float* budget, int32_t* block_cnt,
+                       int32_t* block_idx, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!groups_complete(D))
+        return fail(PROXYATTN_E_CONFIG,
+                    "shard [%d, %d) splits a proxy group of %d query heads: use proxyattn_pool + "
+                    "all-reduce + proxyattn_proxy_scores",
+                    D.qb, D.qe, D.gq);
+    const pa::Workspace W = pa::workspace_layout(D);
+    if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
+    if (!Q || !K || !kstar || !budget || !block_cnt || !block_idx)
+        return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    cudaStream_t st = S(stream);
+    void* Pq = at<char>(ws, W.pq);
+    void* Pk = at<char>(ws, W.pk);
+    float* L = at<float>(ws, W.L);
+    PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st), "pool");
+    rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st);
+    if (rc) return rc;
+    rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
+    if (rc) return rc;
+    PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, st), "select");
+    return PROXYATTN_OK;
+}
+
+static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
+                     const int32_t* block_cnt, const int32_t* block_idx, void* O, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!Q || !K || !V || !O) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    cudaStream_t st = S(stream);
+    if (block_cnt && (D.flags & PROXYATTN_FLAG_CHECK)) {
+        int* bad = nullptr;
+        PA_CUDA(cudaMallocAsync(&bad, sizeof(int), st), "check alloc");
+        PA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st), "check memset");
+        PA_CUDA(pa::launch_check_lists(D, block_cnt, block_idx, bad, st), "check_lists");
+        int hbad = 0;
+        PA_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "check copy");
+        PA_CUDA(cudaFreeAsync(bad, st), "check free");
+        PA_CUDA(cudaStreamSynchronize(st), "check sync");
+        if (hbad) return fail(PROXYATTN_E_SHAPE, "%d block rows violate the list contract (S:319)", hbad);
+    }
+    if (D.fp32) {
+        PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
+    } else {
+        PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
+    }
+    return PROXYATTN_OK;
+}
+
+int proxyattn_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
+                      const int32_t* block_cnt, const int32_t* block_idx, void* O, void* stream) {
+    if (!block_cnt || !block_idx) return fail(PROXYATTN_E_SHAPE, "NULL block lists");
+    return attention(cfg, Q, K, V, block_cnt, block_idx, O, stream);
+}
+
+int proxyattn_dense_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
+                            void* O, void* stream) {
+    return attention(cfg, Q, K, V, nullptr, nullptr, O, stream);
+}
+
+// Device workspace of the host path: Q, K, V, O, per-head outputs, then the estimate scratch.
+struct HostLayout {
+    size_t q, k, v, o, kstar, budget, cnt, idx, ws, total;
+};
+static HostLayout host_layout(const pa::Dims& D) {
+    HostLayout h{};
+    const size_t el = D.fp32 ? 4 : 2;
+    size_t off = 0;
+    h.q = off;      off = pa::align256(off + (size_t)D.Hl * D.N * D.d * el);
+    h.k = off;      off = pa::align256(off + (size_t)D.Hkvl * D.N * D.d * el);
+    h.v = off;      off = pa::align256(off + (size_t)D.Hkvl * D.N * D.d * el);
+    h.o = off;      off = pa::align256(off + (size_t)D.Hl * D.N * D.d * el);
+    h.kstar = off;  off = pa::align256(off + (size_t)D.Hl * 4);
+    h.budget = off; off = pa::align256(off + (size_t)D.Hl * 4);
+    h.cnt = off;    off = pa::align256(off + (size_t)D.Hl * D.M * 4);
+    h.idx = off;    off = pa::align256(off + (size_t)D.Hl * D.M * D.M * 4);
+    h.ws = off;     off = pa::align256(off + pa::workspace_layout(D).total);
+    h.total = off;
+    return h;
+}
+
+int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (!out) return fail(PROXYATTN_E_CONFIG, "out is NULL");
+    *out = host_layout(D).total;
+    return PROXYATTN_OK;
+}
+
+int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void* Kh, const void* Vh,
+                           void* Oh, int32_t* kstar_h, void* dws, size_t dws_bytes, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    const HostLayout H = host_layout(D);
+    if (!dws || dws_bytes < H.total) return fail(PROXYATTN_E_WORKSPACE, "device workspace needs %zu bytes", H.total);
+    if (!Qh || !Kh || !Vh || !Oh) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    cudaStream_t st = S(stream);
+    const size_t el = D.fp32 ? 4 : 2;
+    const size_t qb = (size_t)D.Hl * D.N * D.d * el, kb = (size_t)D.Hkvl * D.N * D.d * el;
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.q), Qh, qb, cudaMemcpyHostToDevice, st), "H2D Q");
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, st), "H2D K");
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, st), "H2D V");
+    rc = proxyattn_estimate(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws),
+                            dws_bytes - H.ws, at<int32_t>(dws, H.kstar), at<float>(dws, H.budget),
+                            at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), stream);
+    if (rc) return rc;
+    rc = proxyattn_prefill(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.v),
+                           at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), at<char>(dws, H.o), stream);
+    if (rc) return rc;
+    PA_CUDA(cudaMemcpyAsync(Oh, at<char>(dws, H.o), qb, cudaMemcpyDeviceToHost, st), "D2H O");
+    if (kstar_h)
+        PA_CUDA(cudaMemcpyAsync(kstar_h, at<char>(dws, H.kstar), (size_t)D.Hl * 4, cudaMemcpyDeviceToHost, st),
+                "D2H kstar");
+    PA_CUDA(cudaStreamSynchronize(st), "forward_host sync");
+    return PROXYATTN_OK;
+}
+
+double proxyattn_cost_ratio(const proxyattn_cfg* cfg) {
+    if (!cfg || cfg->n_q_heads <= 0 || cfg->stride <= 0) return 0.0;
+    return static_cast<double>(cfg->n_groups) /
+           (static_cast<double>(cfg->n_q_heads) * cfg->stride * cfg->stride);
+}
+
+const char* proxyattn_last_error(void) { return g_err.c_str(); }
+
+const char* proxyattn_build_info(void) {
+    return "libproxyattn sm_100a (tcgen05/TMEM/TMA attention; SIMT estimation v1)";
+}
+
+int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream) {
+    if (!A || !B || !C_ss || !C_ts) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    PA_CUDA(pa::launch_debug_umma(A, B, C_ss, C_ts, S(stream)), "debug_umma");
+    return PROXYATTN_OK;
+}
+
+}  // extern "C"

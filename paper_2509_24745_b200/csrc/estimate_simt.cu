@@ -1,0 +1,473 @@
+// estimate_simt.cu — A1 pooling, SIMT (FFMA) A2-A4 estimation kernels, A4 budget finalize
+// and A5-A6 selection.
+//
+// A1  Eq. 2, GQA alignment, stride
+// A2  Eq. 1 softmax normaliser over the sampled causal keys (Z4)
+// A3  Eq. 1 max-pool to (N/b)x(N/b), stored as log-probabilities (Z6)
+// A4  Alg. 1 with readings Z7-Z11
+// A5  Eq. 3 row counts (Z12-Z14), A6 Eq. 3 top-k (Z15, Z17)
+//
+// The SIMT estimation kernels (warp per logit row) serve the FP32_DEBUG build (1e-4
+// contract) and small configs; the bf16 build uses the tcgen05 kernels of
+// estimate_tc.cu for A2-A4 when the shapes allow.
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pa {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void load_row(const T* p, int lane, float (&x)[4], int dv) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = (j < dv) ? to_f32(p[lane * dv + j]) : 0.f;
+}
+
+// ------------------------------------------------------------------------ A1 --
+// One warp per (local group c, sampled row i).  Lane owns d/32 contiguous elements.
+template <typename T>
+__global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict__ K,
+                            float* __restrict__ qsum, float* __restrict__ ksum,
+                            T* __restrict__ Pq, T* __restrict__ Pk) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= static_cast<long long>(D.gl) * D.Ns) return;
+    const int c = static_cast<int>(w / D.Ns);
+    const long long i = w % D.Ns;
+    const long long p = i * D.s;  // first token of each stride window
+    const int grp = D.gb + c;
+    const int dv = D.d >> 5;
+    // query heads of the group inside the shard, and their kv heads (global ids)
+    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
+    const int k0 = max(grp * D.gk, D.kvb), k1 = min((grp + 1) * D.gk, D.kvb + D.Hkvl);
+    // fp64 accumulation: the sum of <= 64 bf16 (or fp32) values is then exact, so the proxy
+    // rounding below is one RNE of the exact sum, as in the oracle (precision contract c.3).
+    double aq[4] = {0., 0., 0., 0.}, ak[4] = {0., 0., 0., 0.};
+    for (int h = h0; h < h1; ++h) {  // fixed ascending order
+        float x[4];
+        load_row(Q + (static_cast<long long>(h - D.qb) * D.N + p) * D.d, lane, x, dv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) aq[j] += x[j];
+    }
+    for (int k = k0; k < k1; ++k) {
+        float x[4];
+        load_row(K + (static_cast<long long>(k - D.kvb) * D.N + p) * D.d, lane, x, dv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ak[j] += x[j];
+    }
+    const long long o = w * D.d + lane * dv;
+    for (int j = 0; j < dv; ++j) {
+        if (qsum) qsum[o + j] = static_cast<float>(aq[j]);
+        if (ksum) ksum[o + j] = static_cast<float>(ak[j]);
+        if (Pq) Pq[o + j] = from_f64<T>(aq[j]);
+        if (Pk) Pk[o + j] = from_f64<T>(ak[j]);
+    }
+}
+
+template <typename T>
+__global__ void round_kernel(long long n, const float* __restrict__ qs, const float* __restrict__ ks,
+                             T* __restrict__ Pq, T* __restrict__ Pk) {
+    long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) {
+        Pq[i] = from_f32<T>(qs[i]);
+        Pk[i] = from_f32<T>(ks[i]);
+    }
+}
+
+// ------------------------------------------------------------------------ A2 --
+// One warp per (c, sampled row i): lse_i = log sum_{j<=i} exp(z_ij).
+template <typename T>
+__global__ void proxy_lse_simt(Dims D, const T* __restrict__ Pq, const T* __restrict__ Pk,
+                               float scale, float* __restrict__ lse) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= static_cast<long long>(D.gl) * D.Ns) return;
+    const int c = static_cast<int>(w / D.Ns);
+    const long long i = w % D.Ns;
+    const int dv = D.d >> 5;
+    float q[4];
+    load_row(Pq + w * D.d, lane, q, dv);
+    const T* kb = Pk + static_cast<long long>(c) * D.Ns * D.d;
+    float mx = -INFINITY, sum = 0.f;
+    for (long long j = 0; j <= i; ++j) {
+        float k[4];
+        load_row(kb + j * D.d, lane, k, dv);
+        float part = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) part = fmaf(q[e], k[e], part);
+        const float z = warp_sum(part) * scale;
+        if (z > mx) {
+            sum = sum * expf(mx - z) + 1.f;
+            mx = z;
+        } else {
+            sum += expf(z - mx);
+        }
+    }
+    if (lane == 0) lse[w] = mx + logf(sum);
+}
+
+// ------------------------------------------------------------------------ A3 --
+// One warp per (c, m, n): L[c][m][n] = max_{i in m, j in n, j<=i} z_ij - lse_i; -inf for n > m.
+template <typename T>
+__global__ void proxy_maxpool_simt(Dims D, const T* __restrict__ Pq, const T* __restrict__ Pk,
+                                   float scale, const float* __restrict__ lse,
+                                   float* __restrict__ L) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
+    if (w >= cells) return;
+    const int c = static_cast<int>(w / (static_cast<long long>(D.M) * D.M));
+    const int m = static_cast<int>((w / D.M) % D.M);
+    const int n = static_cast<int>(w % D.M);
+    if (n > m) {
+        if (lane == 0) L[w] = -INFINITY;
+        return;
+    }
+    const int dv = D.d >> 5;
+    const T* qb = Pq + static_cast<long long>(c) * D.Ns * D.d;
+    const T* kb = Pk + static_cast<long long>(c) * D.Ns * D.d;
+    float best = -INFINITY;
+    for (int ii = 0; ii < D.bs; ++ii) {
+        const long long i = static_cast<long long>(m) * D.bs + ii;
+        float q[4];
+        load_row(qb + i * D.d, lane, q, dv);
+        const float li = lse[static_cast<long long>(c) * D.Ns + i];
+        for (int jj = 0; jj < D.bs; ++jj) {
+            const long long j = static_cast<long long>(n) * D.bs + jj;
+            if (j > i) break;
+            float k[4];
+            load_row(kb + j * D.d, lane, k, dv);
+            float part = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) part = fmaf(q[e], k[e], part);
+            best = fmaxf(best, warp_sum(part) * scale - li);
+        }
+    }
+    if (lane == 0) L[w] = best;
+}
+
+// ------------------------------------------------------------------------ A4 --
+// One warp per (local head, last-block row t): lse_t over keys k <= t (own head, full res).
+template <typename T>
+__global__ void budget_lse_simt(Dims D, const T* __restrict__ Q, const T* __restrict__ K,
+                                float* __restrict__ blse) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= static_cast<long long>(D.Hl) * D.b) return;
+    const int hl = static_cast<int>(w / D.b);
+    const long long t = D.N - D.b + (w % D.b);
+    const int dv = D.d >> 5;
+    const float sc = rsqrtf(static_cast<float>(D.d));
+    float q[4];
+    load_row(Q + (static_cast<long long>(hl) * D.N + t) * D.d, lane, q, dv);
+    const T* kb = K + static_cast<long long>(hl / D.r) * D.N * D.d;
+    float mx = -INFINITY, sum = 0.f;
+    for (long long k = 0; k <= t; ++k) {
+        float kv[4];
+        load_row(kb + k * D.d, lane, kv, dv);
+        float part = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) part = fmaf(q[e], kv[e], part);
+        const float z = warp_sum(part) * sc;
+        if (z > mx) {
+            sum = sum * expf(mx - z) + 1.f;
+            mx = z;
+        } else {
+            sum += expf(z - mx);
+        }
+    }
+    if (lane == 0) blse[w] = mx + logf(sum);
+}
+
+// One warp per (local head, key block n): a[n] = (1/b^2) sum_t sum_{k in n, k<=t} softmax.
+template <typename T>
+__global__ void budget_mass_simt(Dims D, const T* __restrict__ Q, const T* __restrict__ K,
+                                 const float* __restrict__ blse, float* __restrict__ bmass) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= static_cast<long long>(D.Hl) * D.M) return;
+    const int hl = static_cast<int>(w / D.M);
+    const int n = static_cast<int>(w % D.M);
+    const int dv = D.d >> 5;
+    const float sc = rsqrtf(static_cast<float>(D.d));
+    const T* kb = K + static_cast<long long>(hl / D.r) * D.N * D.d;
+    float acc = 0.f;
+    for (int tt = 0; tt < D.b; ++tt) {
+        const long long t = D.N - D.b + tt;
+        float q[4];
+        load_row(Q + (static_cast<long long>(hl) * D.N + t) * D.d, lane, q, dv);
+        const float lt = blse[static_cast<long long>(hl) * D.b + tt];
+        for (int kk = 0; kk < D.b; ++kk) {
+            const long long k = static_cast<long long>(n) * D.b + kk;
+            if (k > t) break;
+            float kv[4];
+            load_row(kb + k * D.d, lane, kv, dv);
+            float part = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) part = fmaf(q[e], kv[e], part);
+            acc += expf(warp_sum(part) * sc - lt);
+        }
+    }
+    if (lane == 0) bmass[w] = acc / (static_cast<float>(D.b) * D.b);
+}
+
+// Bitonic sort of (key, id) pairs in shared memory, order: key descending, id ascending.
+__device__ __forceinline__ bool before(float ka, int ia, float kb, int ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
+__device__ void bitonic_sort(float* key, int* id, int P) {
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool asc = ((lo & size) == 0);  // "asc" = keep `before` order
+                const bool sw = asc ? before(key[hi], id[hi], key[lo], id[lo])
+                                    : before(key[lo], id[lo], key[hi], id[hi]);
+                if (sw) {
+                    const float tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
+                    const int ti = id[lo]; id[lo] = id[hi]; id[hi] = ti;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__host__ __device__ __forceinline__ int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Alg. 1 lines 3-4: one CTA per local head.
+__global__ void budget_finalize_kernel(Dims D, const float* __restrict__ bmass,
+                                       int* __restrict__ kstar, float* __restrict__ budget) {
+    extern __shared__ unsigned char sm[];
+    const int P = next_pow2(D.M);
+    float* key = reinterpret_cast<float*>(sm);
+    int* id = reinterpret_cast<int*>(key + P);
+    const int hl = blockIdx.x;
+    for (int n = threadIdx.x; n < P; n += blockDim.x) {
+        key[n] = (n < D.M) ? bmass[static_cast<long long>(hl) * D.M + n] : -1.f;  // pads last
+        id[n] = n;
+    }
+    __syncthreads();
+    bitonic_sort(key, id, P);
+    if (threadIdx.x == 0) {
+        float T = 0.f;
+        for (int j = 0; j < D.M; ++j) T += key[j];  // summed in the sorted order (Z11)
+        int ks = D.M;
+        if (D.gamma < 1.f) {
+            float Pf = 0.f;
+            for (int k = 1; k <= D.M; ++k) {
+                Pf += key[k - 1] / T;
+                if (Pf >= D.gamma) {
+                    ks = k;
+                    break;
+                }
+            }
+        }
+        kstar[hl] = ks;
+        budget[hl] = static_cast<float>(ks) / D.M;
+    }
+}
+
+// ------------------------------------------------------------------- A5-A6 --
+// One CTA per (local group c, block row m).  Sorts columns 0..m-1 of the shared score row
+// by (L desc, index asc) once, then each head of the group keeps the first K_{h,m}-1 of
+// that order plus the diagonal, emitted ascending (nested prefixes).
+__global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __restrict__ kstar,
+                              int* __restrict__ block_cnt, int* __restrict__ block_idx) {
+    extern __shared__ unsigned char sm[];
+    const int c = blockIdx.x / D.M;
+    const int m = D.M - 1 - (blockIdx.x % D.M);  // long rows first
+    const int P = next_pow2(max(m, 1));
+    float* key = reinterpret_cast<float*>(sm);
+    int* id = reinterpret_cast<int*>(key + next_pow2(D.M));
+    int* rank = id + next_pow2(D.M);
+    __shared__ int warp_tot[32];
+    __shared__ int base_s;
+    const float* row = L + (static_cast<long long>(c) * D.M + m) * D.M;
+    for (int n = threadIdx.x; n < P; n += blockDim.x) {
+        key[n] = (n < m) ? row[n] : -INFINITY;
+        id[n] = (n < m) ? n : INT_MAX;
+    }
+    __syncthreads();
+    if (m > 1) bitonic_sort(key, id, P);
+    for (int p = threadIdx.x; p < m; p += blockDim.x) rank[id[p]] = p;
+    __syncthreads();
+
+    const int grp = D.gb + c;
+    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int h = h0; h < h1; ++h) {
+        const int hl = h - D.qb;
+        const int K = row_count(D, kstar[hl], m);
+        const int keep = K - 1;  // non-diagonal blocks kept (diagonal forced, Z15)
+        int* out = block_idx + (static_cast<long long>(hl) * D.M + m) * D.M;
+        if (threadIdx.x == 0) base_s = 0;
+        __syncthreads();
+        for (int base = 0; base <= m; base += blockDim.x) {
+            const int n = base + threadIdx.x;
+            const bool f = (n <= m) && (n == m || rank[n] < keep);
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) warp_tot[wid] = __popc(bal);
+            __syncthreads();
+            int off = base_s;
+            for (int w2 = 0; w2 < wid; ++w2) off += warp_tot[w2];
+            off += __popc(bal & ((1u << lane) - 1u));
+            if (f) out[off] = n;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int s = 0;
+                for (int w2 = 0; w2 < nw; ++w2) s += warp_tot[w2];
+                base_s += s;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) block_cnt[static_cast<long long>(hl) * D.M + m] = K;
+        __syncthreads();
+    }
+}
+
+// Device-side list validation (PROXYATTN_FLAG_CHECK): counts rows whose list is empty,
+// not strictly ascending, out of range, acausal or missing... (S:319 contract).
+__global__ void check_lists_kernel(Dims D, const int* __restrict__ cnt, const int* __restrict__ idx,
+                                   int* bad) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(D.Hl) * D.M) return;
+    const int m = static_cast<int>(i % D.M);
+    const int k = cnt[i];
+    bool ok = (k >= 1 && k <= m + 1);
+    const int* l = idx + i * D.M;
+    for (int u = 0; ok && u < k; ++u) {
+        const int n = l[u];
+        if (n < 0 || n > m || (u > 0 && n <= l[u - 1])) ok = false;
+    }
+    if (!ok) atomicAdd(bad, 1);
+}
+
+inline unsigned blocks_for(long long threads, int bs) {
+    return static_cast<unsigned>((threads + bs - 1) / bs);
+}
+
+}  // namespace
+
+cudaError_t launch_pool(const Dims& D, const void* Q, const void* K, float* qsum, float* ksum,
+                        void* Pq, void* Pk, cudaStream_t st) {
+    const long long thr = static_cast<long long>(D.gl) * D.Ns * 32;
+    if (D.fp32)
+        pool_kernel<float><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const float*>(Q), static_cast<const float*>(K), qsum, ksum,
+            static_cast<float*>(Pq), static_cast<float*>(Pk));
+    else
+        pool_kernel<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), qsum,
+            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_round_proxies(const Dims& D, const float* qsum, const float* ksum, void* Pq,
+                                 void* Pk, cudaStream_t st) {
+    const long long n = static_cast<long long>(D.gl) * D.Ns * D.d;
+    if (D.fp32)
+        round_kernel<float><<<blocks_for(n, 256), 256, 0, st>>>(n, qsum, ksum,
+                                                               static_cast<float*>(Pq),
+                                                               static_cast<float*>(Pk));
+    else
+        round_kernel<__nv_bfloat16><<<blocks_for(n, 256), 256, 0, st>>>(
+            n, qsum, ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));
+    return cudaGetLastError();
+}
+
+static float proxy_scale(const Dims& D) {
+    // Eq. 2 means folded into the logit scale: 1/(|Gq| |Gk| sqrt(d)) (Z2, Z5)
+    return 1.0f / (static_cast<float>(D.gq) * static_cast<float>(D.gk) *
+                   sqrtf(static_cast<float>(D.d)));
+}
+
+cudaError_t launch_proxy_lse(const Dims& D, const void* Pq, const void* Pk, float* lse,
+                             cudaStream_t st) {
+    const long long thr = static_cast<long long>(D.gl) * D.Ns * 32;
+    const float sc = proxy_scale(D);
+    if (D.fp32)
+        proxy_lse_simt<float><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const float*>(Pq), static_cast<const float*>(Pk), sc, lse);
+    else
+        proxy_lse_simt<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Pq), static_cast<const __nv_bfloat16*>(Pk), sc,
+            lse);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_proxy_maxpool(const Dims& D, const void* Pq, const void* Pk, const float* lse,
+                                 float* L, cudaStream_t st) {
+    const long long thr = static_cast<long long>(D.gl) * D.M * D.M * 32;
+    const float sc = proxy_scale(D);
+    if (D.fp32)
+        proxy_maxpool_simt<float><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const float*>(Pq), static_cast<const float*>(Pk), sc, lse, L);
+    else
+        proxy_maxpool_simt<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Pq), static_cast<const __nv_bfloat16*>(Pk), sc,
+            lse, L);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_budget_lse(const Dims& D, const void* Q, const void* K, float* blse,
+                              cudaStream_t st) {
+    const long long thr = static_cast<long long>(D.Hl) * D.b * 32;
+    if (D.fp32)
+        budget_lse_simt<float><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const float*>(Q), static_cast<const float*>(K), blse);
+    else
+        budget_lse_simt<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), blse);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_budget_mass(const Dims& D, const void* Q, const void* K, const float* blse,
+                               float* bmass, cudaStream_t st) {
+    const long long thr = static_cast<long long>(D.Hl) * D.M * 32;
+    if (D.fp32)
+        budget_mass_simt<float><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const float*>(Q), static_cast<const float*>(K), blse, bmass);
+    else
+        budget_mass_simt<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), blse,
+            bmass);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar, float* budget,
+                                   cudaStream_t st) {
+    const int P = next_pow2(D.M);
+    const size_t sm = static_cast<size_t>(P) * 8;
+    budget_finalize_kernel<<<D.Hl, 512, sm, st>>>(D, bmass, kstar, budget);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* block_cnt,
+                          int* block_idx, cudaStream_t st) {
+    const int P = next_pow2(D.M);
+    const size_t sm = static_cast<size_t>(P) * 4 * 3;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+    }
+    select_kernel<<<D.gl * D.M, 512, sm, st>>>(D, L, kstar, block_cnt, block_idx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_lists(const Dims& D, const int* block_cnt, const int* block_idx,
+                               int* bad_out, cudaStream_t st) {
+    const long long n = static_cast<long long>(D.Hl) * D.M;
+    check_lists_kernel<<<blocks_for(n, 256), 256, 0, st>>>(D, block_cnt, block_idx, bad_out);
+    return cudaGetLastError();
+}
+
+}  // namespace pa

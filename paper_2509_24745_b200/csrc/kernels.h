@@ -1,0 +1,52 @@
+// kernels.h — host-side launchers of the libproxyattn kernels (called by api.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace pa {
+
+// A1: pooled group sums at sampled positions.  qsum/ksum (fp32) and/or Pq/Pk (element type
+// of the build, bf16 RNE or fp32) — any of the four may be null.
+cudaError_t launch_pool(const Dims& D, const void* Q, const void* K, float* qsum, float* ksum,
+                        void* Pq, void* Pk, cudaStream_t st);
+// A1 (staged path): round complete fp32 sums to the proxy element type.
+cudaError_t launch_round_proxies(const Dims& D, const float* qsum, const float* ksum, void* Pq,
+                                 void* Pk, cudaStream_t st);
+// A2: lse[c][i] over sampled causal keys.  A3: log-domain block max map.
+cudaError_t launch_proxy_lse(const Dims& D, const void* Pq, const void* Pk, float* lse,
+                             cudaStream_t st);
+cudaError_t launch_proxy_maxpool(const Dims& D, const void* Pq, const void* Pk, const float* lse,
+                                 float* L, cudaStream_t st);
+// A4: Alg. 1 row lse of the last block, block masses, then sort + prefix -> kstar/budget.
+cudaError_t launch_budget_lse(const Dims& D, const void* Q, const void* K, float* blse,
+                              cudaStream_t st);
+cudaError_t launch_budget_mass(const Dims& D, const void* Q, const void* K, const float* blse,
+                               float* bmass, cudaStream_t st);
+cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar, float* budget,
+                                   cudaStream_t st);
+// A5-A6: per (group, row) ordering, per head compaction.
+cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* block_cnt,
+                          int* block_idx, cudaStream_t st);
+// A7/A8 fp32 debug (SIMT) attention; block lists null => dense.
+cudaError_t launch_attn_simt(const Dims& D, const void* Q, const void* K, const void* V,
+                             const int* block_cnt, const int* block_idx, void* O,
+                             cudaStream_t st);
+// A7/A8 bf16 tcgen05 attention; block lists null => dense.
+cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
+                           const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
+// tcgen05 estimation (bf16, d = b = 128, s = 4): A2+A3 and A4 (see score_tc.cu).
+bool score_tc_supported(const Dims& D);
+size_t score_tc_scratch_bytes(const Dims& D);
+cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float* scratch,
+                            float* lse_nat, float* L, cudaStream_t st);
+cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float* scratch,
+                             float* bmass, cudaStream_t st);
+// Device-side validation of block lists; *bad_out (device int) receives the violation count.
+cudaError_t launch_check_lists(const Dims& D, const int* block_cnt, const int* block_idx,
+                               int* bad_out, cudaStream_t st);
+// Diagnostic GEMM tile (see proxyattn_debug_umma).
+cudaError_t launch_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts,
+                              cudaStream_t st);
+
+}  // namespace pa

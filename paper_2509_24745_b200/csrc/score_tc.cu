@@ -1,0 +1,379 @@
+// score_tc.cu — tcgen05 score kernels of the estimation (bf16 build, b = 128, d = 128):
+//
+//   A2  proxy_lse     Eq. 1 softmax normaliser of the proxy logits over the sampled causal
+//                     keys (Z4): per (sampled row, key chunk) online (max, sum) in
+//                     log2 units, combined per row afterwards -> lse2[c][i].
+//   A3  proxy_maxpool Eq. 1 max-pool (Z6): L[c][m][n] = max over the 32 x 32
+//                     sampled window of z_ij - lse_i (b/s = 32 rows = one warp's TMEM lanes,
+//                     so the row-window max is a warp reduction).
+//   A4  budget        Alg. 1 line 1-2 (Z7, Z8): per head, last block's 128 queries
+//                     against every key block: per (row t, block n) max m_tn and
+//                     s_tn = sum_k exp2(x_tk - m_tn); combined + sorted afterwards.
+//
+// All three share one warp-specialised tile engine (192 threads):
+//   warp 0 TMA producer (A tile once, then 128-key B tiles into a 2-stage ring),
+//   warp 1 TMEM allocator + single-thread tcgen05.mma issuer (S = A B^T, K = d = 128,
+//          SS operands K-major SWIZZLE_128B, fp32 accumulators double-buffered in TMEM),
+//   warps 2-5 epilogue: thread = tile row (TMEM lane), tcgen05.ld 128 columns, mode math.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace pa {
+namespace {
+
+constexpr int kBox = 128 * 64 * 2;   // one [128 rows][64 bf16] SWIZZLE_128B box
+constexpr int kTile = 2 * kBox;      // 128 x 128 bf16
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr int kChunk = 16;           // key tiles per CTA (proxy) / per CTA (budget)
+
+enum Mode { kLse = 0, kMaxpool = 1, kBudget = 2 };
+
+struct __align__(8) SBars {
+    uint64_t a_full;
+    uint64_t b_full[kStages];
+    uint64_t b_empty[kStages];
+    uint64_t s_full[2];
+    uint64_t s_empty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kSmem = 1024 + kTile * (1 + kStages) + sizeof(SBars);
+
+struct ScoreParams {
+    int mode;
+    int Ns;          // proxy: sampled rows per group
+    int N, M;        // budget: tokens, blocks
+    int n_tr;        // proxy: tile rows per group (Ns / 128)
+    int n_chunks;    // chunks per tile row (proxy) / per head (budget)
+    int r;           // budget: GQA ratio (local head -> local kv head)
+    float sc2;       // logit scale in log2 units
+    float* part_m;   // LSE: [gl][Ns][n_chunks]; BUDGET: [Hl][M][128]
+    float* part_s;
+    const float* lse2;  // MAXPOOL: [gl][Ns] (log2 units)
+    float* L;           // MAXPOOL: [gl][M][M] (natural log)
+};
+
+__global__ void __launch_bounds__(kThreads, 2)
+score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                ScoreParams p) {
+    // ---------------------------------------------------------------- problem --
+    int a_row, b_row0, u_begin, u_end, diag_u, prob;  // prob: group (proxy) / local head
+    int tr = 0;                                        // proxy tile row
+    if (p.mode == kBudget) {
+        prob = blockIdx.x / p.n_chunks;
+        const int k = blockIdx.x % p.n_chunks;
+        u_begin = k * kChunk;
+        u_end = min(u_begin + kChunk, p.M);
+        a_row = prob * p.N + (p.N - 128);
+        b_row0 = (prob / p.r) * p.N;
+        diag_u = p.M - 1;
+    } else {
+        const int per_group = p.n_tr * p.n_chunks;
+        prob = blockIdx.x / per_group;
+        const int rem = blockIdx.x % per_group;
+        tr = p.n_tr - 1 - rem / p.n_chunks;        // long rows first
+        const int k = rem % p.n_chunks;
+        u_begin = k * kChunk;
+        if (u_begin > tr) return;                  // chunk beyond the causal diagonal
+        u_end = min(u_begin + kChunk, tr + 1);
+        a_row = prob * p.Ns + tr * 128;
+        b_row0 = prob * p.Ns;
+        diag_u = tr;
+    }
+    const int nt = u_end - u_begin;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kTile;
+    SBars* bars = reinterpret_cast<SBars*>(smem + kTile * (1 + kStages));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->a_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars->b_full[s], 1);
+            mbar_init(&bars->b_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->s_empty[s], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&bars->tmem_base, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = bars->tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmA);
+            tma_prefetch(&tmB);
+            mbar_expect_tx(&bars->a_full, kTile);
+            tma_load_2d(sA, &tmA, &bars->a_full, 0, a_row);
+            tma_load_2d(sA + kBox, &tmA, &bars->a_full, 64, a_row);
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % kStages;
+                if (j >= kStages) mbar_wait(&bars->b_empty[s], ((j / kStages) - 1) & 1);
+                const int brow = b_row0 + (u_begin + j) * 128;
+                mbar_expect_tx(&bars->b_full[s], kTile);
+                tma_load_2d(sB + s * kTile, &tmB, &bars->b_full[s], 0, brow);
+                tma_load_2d(sB + s * kTile + kBox, &tmB, &bars->b_full[s], 64, brow);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 0, 0);
+            const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sB);
+            mbar_wait(&bars->a_full, 0);
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % kStages;
+                mbar_wait(&bars->b_full[s], (j / kStages) & 1);
+                if (j >= 2) mbar_wait(&bars->s_empty[j & 1], ((j >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t tS = tbase + (j & 1) * 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                    umma_ss(tS, sdesc_sw128(a_addr + off, 16, 1024),
+                            sdesc_sw128(b_addr + s * kTile + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
+                }
+                tc_commit(&bars->b_empty[s]);
+                tc_commit(&bars->s_full[j & 1]);
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int rr = quarter * 32 + lane;                  // tile row
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        float m_run = -INFINITY, s_run = 0.f;
+        float lse_row = 0.f;
+        if (p.mode == kMaxpool) lse_row = p.lse2[static_cast<long long>(prob) * p.Ns + tr * 128 + rr];
+        for (int j = 0; j < nt; ++j) {
+            const int u = u_begin + j;
+            mbar_wait(&bars->s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t raw[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + (j & 1) * 128 + c * 32, raw[c]);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bars->s_empty[j & 1]);
+            const bool diag = (u == diag_u);
+            if (p.mode == kMaxpool) {
+                // window c covers sampled key columns [32c, 32c + 32) = block column 4u + c
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float w = -INFINITY;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int col = c * 32 + e;
+                        float x = __uint_as_float(raw[c][e]) * p.sc2 - lse_row;
+                        if (diag && col > rr) x = -INFINITY;
+                        w = fmaxf(w, x);
+                    }
+                    w = warp_max(w);
+                    if (lane == 0) {
+                        const int m = tr * 4 + quarter, n = u * 4 + c;
+                        p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                    }
+                }
+            } else {
+                float x[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int col = c * 32 + e;
+                        const float v = __uint_as_float(raw[c][e]) * p.sc2;
+                        x[col] = (diag && col > rr) ? -INFINITY : v;
+                    }
+                float tmax = x[0];
+#pragma unroll
+                for (int e = 1; e < 128; ++e) tmax = fmaxf(tmax, x[e]);
+                float acc = 0.f;
+                if (p.mode == kLse) {
+                    const float m_new = fmaxf(m_run, tmax);
+#pragma unroll
+                    for (int e = 0; e < 128; ++e) acc += ex2(x[e] - m_new);
+                    s_run = s_run * ex2(m_run - m_new) + acc;
+                    m_run = m_new;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 128; ++e) acc += ex2(x[e] - tmax);
+                    const long long o = (static_cast<long long>(prob) * p.M + u) * 128 + rr;
+                    p.part_m[o] = tmax;
+                    p.part_s[o] = acc;
+                }
+            }
+        }
+        if (p.mode == kLse) {
+            const int k = u_begin / kChunk;
+            const long long o =
+                (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.n_chunks + k;
+            p.part_m[o] = m_run;
+            p.part_s[o] = s_run;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tbase, 256);
+    }
+}
+
+// lse2[c][i] = m* + log2(sum_k s_k 2^(m_k - m*)) over the row's chunks (fixed order).
+__global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, const float* part_m,
+                                   const float* part_s, float* lse2, float* lse_nat) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int row_in_group = static_cast<int>(i % Ns);
+    const int tr = row_in_group / 128;
+    const int nk = (tr + kChunk) / kChunk;   // chunks that exist for this tile row
+    const float* pm = part_m + i * n_chunks;
+    const float* ps = part_s + i * n_chunks;
+    float mx = -INFINITY;
+    for (int k = 0; k < nk; ++k) mx = fmaxf(mx, pm[k]);
+    float s = 0.f;
+    for (int k = 0; k < nk; ++k) s += ps[k] * ex2(pm[k] - mx);
+    const float l2 = mx + __log2f(s);
+    lse2[i] = l2;
+    if (lse_nat) lse_nat[i] = l2 * kLn2;
+    (void)n_tr;
+}
+
+__global__ void fill_neg_inf_kernel(float* L, long long n) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) L[i] = -INFINITY;
+}
+
+// Alg. 1 lines 2-4 for one local head per CTA: combine per-(row, block) partials into the
+// row lse, block masses a[n] = (1/b^2) sum_t s_tn 2^(m_tn - lse_t), then sort + prefix.
+__global__ void budget_combine_kernel(int M, float gamma, const float* __restrict__ part_m,
+                                      const float* __restrict__ part_s, float* __restrict__ bmass) {
+    __shared__ float lse_s[128];
+    const int hl = blockIdx.x;
+    const float* pm = part_m + static_cast<long long>(hl) * M * 128;
+    const float* ps = part_s + static_cast<long long>(hl) * M * 128;
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+        float mx = -INFINITY;
+        for (int n = 0; n < M; ++n) mx = fmaxf(mx, pm[static_cast<long long>(n) * 128 + t]);
+        float s = 0.f;
+        for (int n = 0; n < M; ++n) {
+            const long long o = static_cast<long long>(n) * 128 + t;
+            s += ps[o] * ex2(pm[o] - mx);
+        }
+        lse_s[t] = mx + __log2f(s);
+    }
+    __syncthreads();
+    for (int n = threadIdx.x; n < M; n += blockDim.x) {
+        float a = 0.f;
+        for (int t = 0; t < 128; ++t) {
+            const long long o = static_cast<long long>(n) * 128 + t;
+            a += ps[o] * ex2(pm[o] - lse_s[t]);
+        }
+        bmass[static_cast<long long>(hl) * M + n] = a / (128.f * 128.f);
+    }
+    (void)gamma;
+}
+
+bool set_smem_attr() {
+    static bool done = false;
+    if (!done) {
+        if (cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmem)) != cudaSuccess)
+            return false;
+        done = true;
+    }
+    return true;
+}
+
+}  // namespace
+
+bool score_tc_supported(const Dims& D) {
+    return !D.fp32 && D.d == 128 && D.b == 128 && D.s == 4 && (D.Ns % 128) == 0;
+}
+
+size_t score_tc_scratch_bytes(const Dims& D) {
+    const int n_tr = static_cast<int>(D.Ns / 128);
+    const int n_chunks = (n_tr + kChunk - 1) / kChunk;
+    const size_t lse_parts = 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4;
+    const size_t bud_parts = 2ull * D.Hl * D.M * 128 * 4;
+    return lse_parts > bud_parts ? lse_parts : bud_parts;
+}
+
+// A2 + A3 on tcgen05.  scratch: score_tc_scratch_bytes(D); lse_nat (may be null) receives
+// the natural-log lse for inspection.
+cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float* scratch,
+                            float* lse_nat, float* L, cudaStream_t st) {
+    if (!set_smem_attr()) return cudaErrorInvalidValue;
+    CUtensorMap ma, mb;
+    const uint64_t rows = static_cast<uint64_t>(D.gl) * D.Ns;
+    if (!make_map_bf16_sw128(&ma, Pq, rows, 128, 128) || !make_map_bf16_sw128(&mb, Pk, rows, 128, 128))
+        return cudaErrorInvalidValue;
+    ScoreParams p{};
+    p.Ns = static_cast<int>(D.Ns);
+    p.M = D.M;
+    p.n_tr = static_cast<int>(D.Ns / 128);
+    p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
+    // Eq. 2 means + 1/sqrt(d) folded into the scale (Z2, Z5), in log2 units.
+    p.sc2 = kLog2e / (static_cast<float>(D.gq) * static_cast<float>(D.gk) * sqrtf(static_cast<float>(D.d)));
+    float* part_m = scratch;
+    float* part_s = part_m + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;
+    float* lse2 = part_s + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;
+    p.part_m = part_m;
+    p.part_s = part_s;
+    const unsigned grid = static_cast<unsigned>(D.gl) * p.n_tr * p.n_chunks;
+    p.mode = kLse;
+    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const long long rws = static_cast<long long>(D.gl) * D.Ns;
+    lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
+        static_cast<int>(rws), p.n_tr, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
+    fill_neg_inf_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(L, cells);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    p.mode = kMaxpool;
+    p.lse2 = lse2;
+    p.L = L;
+    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    return cudaGetLastError();
+}
+
+// A4 on tcgen05: per-(row, block) partials, then combine into block masses bmass[Hl][M].
+cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float* scratch,
+                             float* bmass, cudaStream_t st) {
+    if (!set_smem_attr()) return cudaErrorInvalidValue;
+    CUtensorMap ma, mb;
+    if (!make_map_bf16_sw128(&ma, Q, static_cast<uint64_t>(D.Hl) * D.N, 128, 128) ||
+        !make_map_bf16_sw128(&mb, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
+        return cudaErrorInvalidValue;
+    ScoreParams p{};
+    p.mode = kBudget;
+    p.N = static_cast<int>(D.N);
+    p.M = D.M;
+    p.r = D.r;
+    p.n_chunks = (D.M + kChunk - 1) / kChunk;
+    p.sc2 = kLog2e / sqrtf(static_cast<float>(D.d));
+    p.part_m = scratch;
+    p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
+    const unsigned grid = static_cast<unsigned>(D.Hl) * p.n_chunks;
+    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    budget_combine_kernel<<<D.Hl, 256, 0, st>>>(D.M, D.gamma, p.part_m, p.part_s, bmass);
+    return cudaGetLastError();
+}
+
+}  // namespace pa
