@@ -38,7 +38,7 @@ import torch  # noqa: E402
 METRIC = "ms per attention layer at 128K (Llama-3.1-8B shape) and speedup vs dense"
 WORKLOAD = dict(name="llama3.1-8b-attn-128k", n_q_heads=32, n_kv_heads=8, head_dim=128,
                 seq_len=131072, block_size=128, stride=4, n_groups=1, gamma=0.9,
-                min_budget_tokens=0, seed=0)
+                min_budget_tokens=0, seed=0, preset="llama-128k")
 L2_FLUSH_BYTES = 256 << 20
 KERNELS_PER_STEP = 8   # pool, proxy_lse, proxy_maxpool, budget_lse, budget_mass, finalize, select, attn
 
@@ -122,7 +122,8 @@ def gen_inputs(w, device):
     import workloads
 
     return workloads.structured(w["n_q_heads"], w["n_kv_heads"], w["seq_len"], w["head_dim"],
-                                seed=w["seed"], device=device)
+                                seed=w["seed"], params=workloads.PRESETS[w["preset"]],
+                                device=device)
 
 
 # ------------------------------------------------------------------------ oracle --

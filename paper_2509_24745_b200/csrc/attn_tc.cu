@@ -4,19 +4,29 @@
 // softmax(Q[h][t] K[kv(h)][k] / sqrt(d)) V[kv(h)][k],
 // FlashAttention-style online softmax, causal mask only inside the diagonal block.
 //
-// One CTA per (local head, query block row m); CTAs are ordered longest row first.
-// Warp roles (192 threads):
-//   warp 0      TMA producer: Q tile once, then K/V tiles of each selected block into a
-//               2-stage ring (128 x 128 bf16 tiles, two SWIZZLE_128B boxes each)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//               S_j = Q K_j^T (SS, K-major both)        -> TMEM S[j%2]  (128 cols fp32)
-//               O  += P_j V_j (A = P_j from TMEM, B = V_j MN-major) -> TMEM O (128 cols)
-//   warps 2-5   softmax: thread = query row (TMEM lane); tcgen05.ld S_j, scale, diagonal
-//               mask, online max with lazy rescale (threshold 2^8), exp2, P_j packed to
-//               bf16 and tcgen05.st over S_j's first 64 columns; O correction in TMEM when
-//               the running max moved; epilogue O / l -> bf16 -> global.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384) of a 512-column allocation.
+// GQA packing: one CTA serves TWO query heads of the same KV head (a "pair") at the same
+// query block row m.  Heads of one KV head always share a proxy group (groups are
+// KV-aligned), so their lists are prefixes of one order (nested); the CTA walks
+// the UNION of the two ascending lists and each K/V tile is loaded once for both heads,
+// halving L2->SM traffic.  Any lists are accepted (oracle injection): the union walk and
+// per-head flags are general.
+//
+// Warp roles (320 threads):
+//   warp 0      TMA producer: Q tiles of both heads, then K/V tiles of each union block
+//               into a 2-stage ring (128 x 128 bf16 tiles = two SWIZZLE_128B boxes)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, FA4-style order:
+//               S_s = Q_s K_u^T (SS)  and  O_s += P_s V_u (A = P_s from TMEM, B = V MN-major);
+//               S_s(u+1) is issued right after O_s += P_s(u) V(u) so each head's softmax
+//               overlaps the other head's MMAs
+//   warps 2-5   softmax of slot 0, warps 6-9 softmax of slot 1: thread = query row (TMEM
+//               lane); tcgen05.ld S, scale, diagonal mask, online max with lazy rescale
+//               (threshold 2^8), exp2, P packed to bf16 and tcgen05.st over S's first 64
+//               columns; O correction in TMEM when the max moved; epilogue O/l -> bf16.
+// TMEM (512 columns): S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512).
 #include <cuda_bf16.h>
+
+#include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -30,7 +40,7 @@ constexpr int kTileRows = 128;                   // b = 128 query rows / keys pe
 constexpr int kBox = kTileRows * 64 * 2;         // 16 KB: [128 rows][64 bf16] SW128 box
 constexpr int kTile = 2 * kBox;                  // 32 KB: a 128 x 128 bf16 tile
 constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;        // log2 units: P <= 2^8 before a rescale
 
 struct __align__(8) Bars {
@@ -39,36 +49,82 @@ struct __align__(8) Bars {
     uint64_t v_full[kStages];
     uint64_t kv_empty[kStages];
     uint64_t s_full[2];
-    uint64_t p_full;
-    uint64_t o_done;
+    uint64_t p_half[2][2];   // [slot][half]: P columns for keys [64 h, 64 h + 64) are in TMEM
+    uint64_t o_done[2];
     uint32_t tmem_base;
 };
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTile * (1 + 2 * kStages) + sizeof(Bars);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTile * (2 + 2 * kStages) + sizeof(Bars);
+
+// Ascending union of two ascending block lists (null list = dense 0..m).
+struct UnionWalk {
+    const int* a;
+    const int* b;
+    int na, nb, ia, ib;
+    __device__ __forceinline__ int at(const int* l, int i) const { return l ? __ldg(l + i) : i; }
+    // Returns false at the end; flags bit s = slot s selected the block.
+    __device__ __forceinline__ bool next(int& n, int& flags) {
+        const int va = ia < na ? at(a, ia) : INT_MAX;
+        const int vb = ib < nb ? at(b, ib) : INT_MAX;
+        if (va == INT_MAX && vb == INT_MAX) return false;
+        if (va < vb) {
+            n = va; flags = 1; ++ia;
+        } else if (vb < va) {
+            n = vb; flags = 2; ++ib;
+        } else {
+            n = va; flags = 3; ++ia; ++ib;
+        }
+        return true;
+    }
+};
 
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-               int Hl, int r, float scale_log2) {
+               int r, int Hl, int pair_mode, float scale_log2) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = smem + kTile;                   // kStages tiles
-    uint8_t* sV = smem + kTile * (1 + kStages);   // kStages tiles
-    Bars* bars = reinterpret_cast<Bars*>(smem + kTile * (1 + 2 * kStages));
+    uint8_t* sQ = smem;                           // 2 tiles (slot 0, slot 1)
+    uint8_t* sK = smem + 2 * kTile;               // kStages tiles
+    uint8_t* sV = smem + kTile * (2 + kStages);   // kStages tiles
+    Bars* bars = reinterpret_cast<Bars*>(smem + kTile * (2 + 2 * kStages));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int bid = blockIdx.x;
-    const int m = M - 1 - bid / Hl;               // longest rows first (LPT order)
-    const int hl = bid % Hl;
-    const int kvl = hl / r;
+    // Work item -> two slots (local head, block row) sharing one kv head.  Items are
+    // ordered kv-head major (so the ~148 resident CTAs stream one kv head's K/V through L2
+    // together), heaviest rows first within a kv head.
+    int hs0, hs1, ms0, ms1, nslots;
+    if (pair_mode == 0) {              // two heads of one kv head, same row
+        const int ppk = (r + 1) >> 1;
+        const int per_kv = ppk * M;
+        const int kvi = bid / per_kv, rem = bid % per_kv;
+        const int i0 = 2 * (rem % ppk);
+        ms0 = ms1 = M - 1 - rem / ppk;
+        hs0 = kvi * r + i0;
+        hs1 = hs0 + 1;
+        nslots = (i0 + 1 < r) ? 2 : 1;
+    } else {                           // one head, two adjacent rows
+        const int nrp = (M + 1) >> 1;
+        const int per_kv = r * nrp;
+        const int kvi = bid / per_kv, rem = bid % per_kv;
+        hs0 = hs1 = kvi * r + rem % r;
+        ms0 = M - 1 - 2 * (rem / r);
+        ms1 = ms0 - 1;
+        nslots = ms1 >= 0 ? 2 : 1;
+    }
+    (void)Hl;
+    const int kvl = hs0 / r;
     const bool dense = (block_cnt == nullptr);
-    const long long row = static_cast<long long>(hl) * M + m;
-    const int cnt = dense ? (m + 1) : block_cnt[row];
-    const int* list = dense ? nullptr : block_idx + row * M;
+    const long long row0 = static_cast<long long>(hs0) * M + ms0;
+    const long long row1 = static_cast<long long>(hs1) * M + ms1;
+    const int cnt0 = dense ? ms0 + 1 : block_cnt[row0];
+    const int cnt1 = nslots < 2 ? 0 : (dense ? ms1 + 1 : block_cnt[row1]);
+    const int* list0 = dense ? nullptr : block_idx + row0 * M;
+    const int* list1 = (dense || nslots < 2) ? nullptr : block_idx + row1 * M;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->q_full, 1);
@@ -77,10 +133,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mbar_init(&bars->v_full[s], 1);
             mbar_init(&bars->kv_empty[s], 1);
         }
-        mbar_init(&bars->s_full[0], 1);
-        mbar_init(&bars->s_full[1], 1);
-        mbar_init(&bars->p_full, 128);
-        mbar_init(&bars->o_done, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->p_half[s][0], 128);
+            mbar_init(&bars->p_half[s][1], 128);
+            mbar_init(&bars->o_done[s], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
@@ -95,23 +153,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             tma_prefetch(&tmQ);
             tma_prefetch(&tmK);
             tma_prefetch(&tmV);
-            const int qrow = hl * N + m * kTileRows;
-            mbar_expect_tx(&bars->q_full, kTile);
-            tma_load_2d(sQ, &tmQ, &bars->q_full, 0, qrow);
-            tma_load_2d(sQ + kBox, &tmQ, &bars->q_full, 64, qrow);
-            for (int j = 0; j < cnt; ++j) {
-                const int s = j % kStages;
-                if (j >= kStages) mbar_wait(&bars->kv_empty[s], ((j / kStages) - 1) & 1);
-                const int n = dense ? j : __ldg(list + j);
+            mbar_expect_tx(&bars->q_full, kTile * nslots);
+            for (int s = 0; s < nslots; ++s) {
+                const int qrow = (s ? hs1 : hs0) * N + (s ? ms1 : ms0) * kTileRows;
+                tma_load_2d(sQ + s * kTile, &tmQ, &bars->q_full, 0, qrow);
+                tma_load_2d(sQ + s * kTile + kBox, &tmQ, &bars->q_full, 64, qrow);
+            }
+            UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
+            int n, f;
+            for (int u = 0; it.next(n, f); ++u) {
+                const int st = u % kStages;
+                if (u >= kStages) mbar_wait(&bars->kv_empty[st], ((u / kStages) - 1) & 1);
                 const int krow = kvl * N + n * kTileRows;
-                uint8_t* k_dst = sK + s * kTile;
-                uint8_t* v_dst = sV + s * kTile;
-                mbar_expect_tx(&bars->k_full[s], kTile);
-                tma_load_2d(k_dst, &tmK, &bars->k_full[s], 0, krow);
-                tma_load_2d(k_dst + kBox, &tmK, &bars->k_full[s], 64, krow);
-                mbar_expect_tx(&bars->v_full[s], kTile);
-                tma_load_2d(v_dst, &tmV, &bars->v_full[s], 0, krow);
-                tma_load_2d(v_dst + kBox, &tmV, &bars->v_full[s], 64, krow);
+                uint8_t* k_dst = sK + st * kTile;
+                uint8_t* v_dst = sV + st * kTile;
+                mbar_expect_tx(&bars->k_full[st], kTile);
+                tma_load_2d(k_dst, &tmK, &bars->k_full[st], 0, krow);
+                tma_load_2d(k_dst + kBox, &tmK, &bars->k_full[st], 64, krow);
+                mbar_expect_tx(&bars->v_full[st], kTile);
+                tma_load_2d(v_dst, &tmV, &bars->v_full[st], 0, krow);
+                tma_load_2d(v_dst + kBox, &tmV, &bars->v_full[st], 64, krow);
             }
         }
     } else if (warp == 1) {
@@ -119,72 +180,110 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         if (lane == 0) {
             constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-            const uint32_t tO = tbase + 256;
             const uint32_t q_addr = smem_u32(sQ);
             const uint32_t k_addr = smem_u32(sK);
             const uint32_t v_addr = smem_u32(sV);
             mbar_wait(&bars->q_full, 0);
-            auto issue_s = [&](int j) {
-                const int s = j % kStages;
-                mbar_wait(&bars->k_full[s], (j / kStages) & 1);
+            auto issue_s = [&](int slot, int u) {  // S_slot = Q_slot K(u)^T
+                const int st = u % kStages;
+                mbar_wait(&bars->k_full[st], (u / kStages) & 1);
                 tc_fence_after();
-                const uint32_t tS = tbase + (j & 1) * 128;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {  // K = d = 128 in steps of 16
+                for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-                    const uint64_t a = sdesc_sw128(q_addr + off, 16, 1024);
-                    const uint64_t b = sdesc_sw128(k_addr + s * kTile + off, 16, 1024);
-                    umma_ss(tS, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+                    umma_ss(tbase + slot * 128, sdesc_sw128(q_addr + slot * kTile + off, 16, 1024),
+                            sdesc_sw128(k_addr + st * kTile + off, 16, 1024), idesc_qk,
+                            kk > 0 ? 1u : 0u);
                 }
-                tc_commit(&bars->s_full[j & 1]);
+                tc_commit(&bars->s_full[slot]);
             };
-            issue_s(0);
-            for (int j = 0; j < cnt; ++j) {
-                if (j + 1 < cnt) issue_s(j + 1);
-                const int s = j % kStages;
-                mbar_wait(&bars->p_full, j & 1);
-                mbar_wait(&bars->v_full[s], (j / kStages) & 1);
-                tc_fence_after();
-                const uint32_t tP = tbase + (j & 1) * 128;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys in steps of 16
-                    const uint64_t b = sdesc_sw128(v_addr + s * kTile + kk * 2048, kBox, 1024);
-                    umma_ts(tO, tP + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-                }
-                tc_commit(&bars->kv_empty[s]);
-                tc_commit(&bars->o_done);
+            UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
+            int n_cur, f_cur, n_nxt = 0, f_nxt = 0;
+            bool has = it.next(n_cur, f_cur);
+            int jn[2] = {0, 0};                     // PVs issued per slot (p_full parity)
+            if (has) {
+                if (f_cur & 1) issue_s(0, 0);
+                if (f_cur & 2) issue_s(1, 0);
             }
+            for (int u = 0; has; ++u) {
+                const bool has_nxt = it.next(n_nxt, f_nxt);
+                const int st = u % kStages;
+                mbar_wait(&bars->v_full[st], (u / kStages) & 1);
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot) {
+                    if (!(f_cur & (1 << slot))) continue;
+                    const uint32_t tP = tbase + slot * 128;
+                    const uint32_t tO = tbase + 256 + slot * 128;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {   // PV over keys [64 half, 64 half + 64)
+                        mbar_wait(&bars->p_half[slot][half], jn[slot] & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {  // K steps of 16 keys
+                            const int kk = half * 4 + k4;
+                            const uint64_t b = sdesc_sw128(v_addr + st * kTile + kk * 2048, kBox, 1024);
+                            umma_ts(tO, tP + kk * 8, b, idesc_pv, (jn[slot] > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc_commit(&bars->o_done[slot]);
+                    ++jn[slot];
+                    if (has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                }
+                tc_commit(&bars->kv_empty[st]);
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot)
+                    if (!(f_cur & (1 << slot)) && has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                n_cur = n_nxt;
+                f_cur = f_nxt;
+                has = has_nxt;
+            }
+            (void)n_cur;
         }
     } else {
         // ------------------------------------------------------------- softmax --
+        const int slot = (warp - 2) >> 2;
         const int quarter = warp & 3;                   // TMEM lane quarter of this warp
         const int rr = quarter * 32 + lane;             // query row within the block
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t tS = tbase + lane_off + slot * 128;
+        const uint32_t tO = tbase + lane_off + 256 + slot * 128;
+        const int my_cnt = slot ? cnt1 : cnt0;
+        const int* my_list = slot ? list1 : list0;
+        const int m = slot ? ms1 : ms0;
+        const int my_h = slot ? hs1 : hs0;
         float m_used = -INFINITY;                       // running max (log2 units)
         float l = 0.f;                                  // running denominator
-        for (int j = 0; j < cnt; ++j) {
-            const int n = dense ? j : __ldg(list + j);
-            mbar_wait(&bars->s_full[j & 1], (j >> 1) & 1);
+        int n_next = (my_cnt > 0) ? (my_list ? __ldg(my_list) : 0) : 0;
+        for (int j = 0; j < my_cnt; ++j) {
+            const int n = n_next;
+            if (j + 1 < my_cnt) n_next = my_list ? __ldg(my_list + j + 1) : j + 1;  // prefetch
+            mbar_wait(&bars->s_full[slot], j & 1);
             tc_fence_after();
-            const uint32_t tS = tbase + lane_off + (j & 1) * 128;
             uint32_t raw[4][32];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, raw[c]);
             tmem_ld_wait();
-            float x[128];
+            if (n == m) {  // diagonal block: key index > row index is masked (causal)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c * 32 + e > rr) raw[c][e] = 0xff800000u;  // -inf
+            }
+            // row max of the raw logits, 8 independent chains (scale > 0 commutes with max)
+            float mx[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx[k] = __uint_as_float(raw[k >> 1][(k & 1) * 16]);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) x[c * 32 + e] = __uint_as_float(raw[c][e]) * scale_log2;
-            if (n == m) {  // diagonal block: key index > row index is masked (causal)
-#pragma unroll
-                for (int e = 0; e < 128; ++e)
-                    if (e > rr) x[e] = -INFINITY;
-            }
-            float rmax = x[0];
-#pragma unroll
-            for (int e = 1; e < 128; ++e) rmax = fmaxf(rmax, x[e]);
-            const float m_new = fmaxf(m_used, rmax);
+                for (int e = 0; e < 32; ++e) {
+                    const int k = c * 2 + (e >> 4);
+                    mx[k] = fmaxf(mx[k], __uint_as_float(raw[c][e]));
+                }
+            const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            const float m_new = fmaxf(m_used, rmax * scale_log2);
             const bool need = (m_new > m_used + kRescaleThreshold);
             const bool any = __any_sync(0xffffffffu, need);
             float factor = 1.f;
@@ -193,151 +292,84 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 m_used = m_new;
                 l *= factor;
             }
-            uint32_t pk[2][32];
+            const float neg_m = -m_used;
+            float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const float p0 = ex2(x[2 * c] - m_used);
-                const float p1 = ex2(x[2 * c + 1] - m_used);
-                l += p0 + p1;
-                pk[c >> 5][c & 31] = pack_bf16(p0, p1);
-            }
-            tmem_st32(tS, pk[0]);
-            tmem_st32(tS + 32, pk[1]);
-            if (j > 0) {
-                mbar_wait(&bars->o_done, (j - 1) & 1);  // PV_{j-1} finished writing O
-                tc_fence_after();
-                if (any) {
-                    const uint32_t tO = tbase + lane_off + 256;
+            for (int half = 0; half < 2; ++half) {
+                uint32_t pk[32];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32(tO + c * 32, o);
-                        tmem_ld_wait();
+                for (int c = 0; c < 32; ++c) {
+                    const int e0 = half * 64 + 2 * c;  // key column
+                    const float p0 = ex2(fmaf(__uint_as_float(raw[e0 >> 5][e0 & 31]), scale_log2, neg_m));
+                    const float p1 = ex2(fmaf(__uint_as_float(raw[(e0 + 1) >> 5][(e0 + 1) & 31]), scale_log2, neg_m));
+                    ls[c & 7] += p0 + p1;
+                    pk[c] = pack_bf16(p0, p1);
+                }
+                tmem_st32(tS + half * 32, pk);
+                if (half == 0 && j > 0) {
+                    mbar_wait(&bars->o_done[slot], (j - 1) & 1);  // PV_{j-1} finished writing O
+                    tc_fence_after();
+                    if (any) {
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
-                        tmem_st32(tO + c * 32, o);
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
+                            tmem_st32(tO + c * 32, o);
+                        }
                     }
                 }
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&bars->p_half[slot][half]);
             }
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&bars->p_full);
+            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
         }
         // ----------------------------------------------------------- epilogue --
-        mbar_wait(&bars->o_done, (cnt - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / l;
-        const uint32_t tO = tbase + lane_off + 256;
-        uint4* dst = reinterpret_cast<uint4*>(
-            O + (static_cast<long long>(hl) * N + static_cast<long long>(m) * kTileRows + rr) * 128);
+        if (my_cnt > 0) {
+            mbar_wait(&bars->o_done[slot], (my_cnt - 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / l;
+            uint4* dst = reinterpret_cast<uint4*>(
+                O + (static_cast<long long>(my_h) * N + static_cast<long long>(m) * kTileRows + rr) *
+                        128);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
-            uint32_t pkd[16];
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_ld_wait();
+                uint32_t pkd[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-                pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+                for (int e = 0; e < 16; ++e)
+                    pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
-                dst[c * 4 + v] = make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+                for (int v = 0; v < 4; ++v)
+                    dst[c * 4 + v] = make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
+        __syncwarp();
         tc_fence_after();
         tmem_dealloc(tbase, 512);
     }
 }
 
-// ------------------------------------------------------------ diagnostic GEMM --
-__global__ void __launch_bounds__(128, 1)
-debug_umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const __nv_bfloat16* __restrict__ A, float* __restrict__ Css,
-                  float* __restrict__ Cts) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + kTile;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kTile);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_init(&bar[2], 128);
-        fence_barrier_init();
+// Slot pairing: 0 = two heads of one kv head at the same row, 1 = one head at two adjacent
+// rows (default; adjacent rows' lists overlap strongly, independent of per-head budgets).
+// PROXYATTN_PAIR_MODE overrides it (for measurements).
+int attn_pair_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("PROXYATTN_PAIR_MODE");
+        mode = (e && e[0] == '0') ? 0 : 1;
     }
-    if (warp == 0) tmem_alloc(tslot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tbase = *tslot;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    // A (row-major [128][128]) into TMEM columns [256, 320) as packed bf16 pairs.
-    {
-        const int rr = warp * 32 + lane;
-        uint32_t pk[2][32];
-        const uint32_t* arow = reinterpret_cast<const uint32_t*>(A + rr * 128);
-#pragma unroll
-        for (int c = 0; c < 64; ++c) pk[c >> 5][c & 31] = arow[c];
-        tmem_st32(tbase + lane_off + 256, pk[0]);
-        tmem_st32(tbase + lane_off + 256 + 32, pk[1]);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&bar[2]);
-    }
-    if (threadIdx.x == 0) {
-        mbar_expect_tx(&bar[0], 2 * kTile);
-        tma_load_2d(sA, &tmA, &bar[0], 0, 0);
-        tma_load_2d(sA + kBox, &tmA, &bar[0], 64, 0);
-        tma_load_2d(sB, &tmB, &bar[0], 0, 0);
-        tma_load_2d(sB + kBox, &tmB, &bar[0], 64, 0);
-        mbar_wait(&bar[0], 0);
-        mbar_wait(&bar[2], 0);
-        tc_fence_after();
-        const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sB);
-        constexpr uint32_t idesc_ss = idesc_bf16_f32(128, 128, 0, 0);
-        constexpr uint32_t idesc_ts = idesc_bf16_f32(128, 128, 0, 1);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-            umma_ss(tbase, sdesc_sw128(a_addr + off, 16, 1024), sdesc_sw128(b_addr + off, 16, 1024),
-                    idesc_ss, kk > 0);
-        }
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            umma_ts(tbase + 128, tbase + 256 + kk * 8, sdesc_sw128(b_addr + kk * 2048, kBox, 1024),
-                    idesc_ts, kk > 0);
-        }
-        tc_commit(&bar[1]);
-    }
-    __syncwarp();
-    mbar_wait(&bar[1], 0);
-    tc_fence_after();
-    const int rr = warp * 32 + lane;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tbase + lane_off + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) Css[rr * 128 + c * 32 + e] = __uint_as_float(v[e]);
-        tmem_ld32(tbase + lane_off + 128 + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) Cts[rr * 128 + c * 32 + e] = __uint_as_float(v[e]);
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tbase, 512);
-    }
+    return mode;
 }
 
 }  // namespace
@@ -357,23 +389,13 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
         attr_set = true;
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
-    const unsigned grid = static_cast<unsigned>(D.Hl) * static_cast<unsigned>(D.M);
+    const int mode = attn_pair_mode();
+    const unsigned grid = mode == 0
+        ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(D.M)
+        : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((D.M + 1) / 2);
     attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
-        D.M, D.Hl, D.r, scale_log2);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts,
-                              cudaStream_t st) {
-    CUtensorMap ma, mb;
-    if (!make_map_bf16_sw128(&ma, A, 128, 128, 128) || !make_map_bf16_sw128(&mb, B, 128, 128, 128))
-        return cudaErrorInvalidValue;
-    const size_t sm = 1024 + 2 * kTile + 64;
-    cudaError_t e = cudaFuncSetAttribute(debug_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
-    debug_umma_kernel<<<1, 128, sm, st>>>(ma, mb, static_cast<const __nv_bfloat16*>(A), C_ss, C_ts);
+        D.M, D.r, D.Hl, mode, scale_log2);
     return cudaGetLastError();
 }
 
