@@ -78,6 +78,7 @@ struct UnionWalk {
     }
 };
 
+template <int kEmu>   // of every 4 key-column pairs, kEmu use the FMA-pipe exp2 (ex2_poly2)
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
@@ -292,17 +293,28 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 m_used = m_new;
                 l *= factor;
             }
-            const float neg_m = -m_used;
-            float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+            const uint64_t nm2 = f2_pack(-m_used, -m_used);
+            uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};   // packed partial row sums
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t pk[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
-                    const int e0 = half * 64 + 2 * c;  // key column
-                    const float p0 = ex2(fmaf(__uint_as_float(raw[e0 >> 5][e0 & 31]), scale_log2, neg_m));
-                    const float p1 = ex2(fmaf(__uint_as_float(raw[(e0 + 1) >> 5][(e0 + 1) & 31]), scale_log2, neg_m));
-                    ls[c & 7] += p0 + p1;
+                    const int e0 = half * 64 + 2 * c;  // key column of the pair
+                    const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
+                                                       __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
+                                               sc2, nm2);
+                    float p0, p1;
+                    if ((c & 3) < kEmu) {
+                        ex2_poly2(x2, p0, p1);
+                    } else {
+                        float x0, x1;
+                        f2_unpack(x2, x0, x1);
+                        p0 = ex2(x0);
+                        p1 = ex2(x1);
+                    }
+                    ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
                     pk[c] = pack_bf16(p0, p1);
                 }
                 tmem_st32(tS + half * 32, pk);
@@ -326,7 +338,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tc_fence_before();
                 mbar_arrive(&bars->p_half[slot][half]);
             }
-            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+            {
+                const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
+                float a, b;
+                f2_unpack(t, a, b);
+                l += a + b;
+            }
         }
         // ----------------------------------------------------------- epilogue --
         if (my_cnt > 0) {
@@ -372,6 +389,17 @@ int attn_pair_mode() {
     return mode;
 }
 
+// Fraction (x/4) of the softmax exponentials computed on the FMA pipe instead of MUFU
+// (FA4-style balance of the two pipes).  PROXYATTN_EXP_EMU=0..3 overrides the default.
+int attn_exp_emu() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PROXYATTN_EXP_EMU");
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+    }
+    return v;
+}
+
 }  // namespace
 
 cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
@@ -381,19 +409,22 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
         !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
         !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
         return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int emu = attn_exp_emu();
+    auto kern = emu == 0 ? attn_tc_kernel<0> : emu == 1 ? attn_tc_kernel<1> : emu == 2 ? attn_tc_kernel<2>
+              : attn_tc_kernel<3>;
+    static bool attr_set[4] = {false, false, false, false};
+    if (!attr_set[emu]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kSmemBytes));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[emu] = true;
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
     const int mode = attn_pair_mode();
     const unsigned grid = mode == 0
         ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(D.M)
         : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((D.M + 1) / 2);
-    attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(
+    kern<<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
         D.M, D.r, D.Hl, mode, scale_log2);
     return cudaGetLastError();

@@ -192,6 +192,58 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^x on the FMA/ALU pipes (no MUFU): Cody-Waite split x = j + f, j = rint(x), f in
+// [-0.5, 0.5], 2^f by a minimax cubic (max rel. error 7.5e-5, below bf16's 2^-9), then
+// j added to the exponent field.  x is clamped at -125 (result ~2^-125 there, incl. -inf).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.f);  // keeps exponent(p) + j >= 1 (p in [0.707, 1.414])
+    const float magic = 12582912.f;  // 1.5 * 2^23: x + magic holds rint(x) in its low bits
+    const float t = x + magic;
+    const float f = x - (t - magic);
+    const float p = fmaf(fmaf(fmaf(0.05517132207751274f, f, 0.24261054396629333f), f,
+                              0.6932609677314758f), f, 0.9999281167984009f);
+    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
+}
+
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// ex2_poly on a packed pair: 6 FMA-pipe instructions (3 FADD2/FFMA2 + 3 FFMA2 Horner)
+// plus 2 clamps and 2 exponent adds on the ALU pipe.
+__device__ __forceinline__ void ex2_poly2(uint64_t x2, float& r0, float& r1) {
+    float a, b;
+    f2_unpack(x2, a, b);
+    x2 = f2_pack(fmaxf(a, -125.f), fmaxf(b, -125.f));
+    const uint64_t t2 = f2_add(x2, f2_pack(12582912.f, 12582912.f));
+    const uint64_t j2 = f2_add(t2, f2_pack(-12582912.f, -12582912.f));
+    const uint64_t f2 = f2_fma(j2, f2_pack(-1.f, -1.f), x2);
+    uint64_t p2 = f2_fma(f2_pack(0.05517132207751274f, 0.05517132207751274f), f2,
+                         f2_pack(0.24261054396629333f, 0.24261054396629333f));
+    p2 = f2_fma(p2, f2, f2_pack(0.6932609677314758f, 0.6932609677314758f));
+    p2 = f2_fma(p2, f2, f2_pack(0.9999281167984009f, 0.9999281167984009f));
+    float p0, p1, t0, t1;
+    f2_unpack(p2, p0, p1);
+    f2_unpack(t2, t0, t1);
+    r0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+    r1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
