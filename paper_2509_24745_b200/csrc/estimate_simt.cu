@@ -66,6 +66,71 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
     }
 }
 
+// bf16 build: 16-byte loads (8 elements per thread, d/8 threads per sampled row), heads
+// summed in ascending order in fp64 (exact), 4 rows in flight per thread.
+__global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
+                                 const __nv_bfloat16* __restrict__ K, float* __restrict__ qsum,
+                                 float* __restrict__ ksum, __nv_bfloat16* __restrict__ Pq,
+                                 __nv_bfloat16* __restrict__ Pk) {
+    const int tpr = D.d >> 3;
+    const long long gt = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long row = gt / tpr;
+    const int part = static_cast<int>(gt % tpr);
+    if (row >= static_cast<long long>(D.gl) * D.Ns) return;
+    const int c = static_cast<int>(row / D.Ns);
+    const long long i = row % D.Ns;
+    const long long p = i * D.s;
+    const int grp = D.gb + c;
+    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
+    const int k0 = max(grp * D.gk, D.kvb), k1 = min((grp + 1) * D.gk, D.kvb + D.Hkvl);
+    auto accumulate = [&](const __nv_bfloat16* base, int a, int b, int head0, double (&acc)[8]) {
+        for (int h = a; h < b; h += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (h + k < b)
+                    v[k] = __ldg(reinterpret_cast<const uint4*>(
+                        base + (static_cast<long long>(h + k - head0) * D.N + p) * D.d + part * 8));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (h + k >= b) break;
+                const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(e[q]);
+                    acc[2 * q] += f.x;
+                    acc[2 * q + 1] += f.y;
+                }
+            }
+        }
+    };
+    double aq[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ak[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    accumulate(Q, h0, h1, D.qb, aq);
+    accumulate(K, k0, k1, D.kvb, ak);
+    const long long o = row * D.d + part * 8;
+    if (qsum) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            qsum[o + q] = static_cast<float>(aq[q]);
+            ksum[o + q] = static_cast<float>(ak[q]);
+        }
+    }
+    if (Pq) {
+        uint4 oq, ok;
+        uint32_t* wq = reinterpret_cast<uint32_t*>(&oq);
+        uint32_t* wk = reinterpret_cast<uint32_t*>(&ok);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162 bq(__double2bfloat16(aq[2 * q]), __double2bfloat16(aq[2 * q + 1]));
+            const __nv_bfloat162 bk(__double2bfloat16(ak[2 * q]), __double2bfloat16(ak[2 * q + 1]));
+            wq[q] = *reinterpret_cast<const uint32_t*>(&bq);
+            wk[q] = *reinterpret_cast<const uint32_t*>(&bk);
+        }
+        *reinterpret_cast<uint4*>(Pq + o) = oq;
+        *reinterpret_cast<uint4*>(Pk + o) = ok;
+    }
+}
+
 template <typename T>
 __global__ void round_kernel(long long n, const float* __restrict__ qs, const float* __restrict__ ks,
                              T* __restrict__ Pq, T* __restrict__ Pk) {
@@ -256,20 +321,50 @@ __global__ void budget_finalize_kernel(Dims D, const float* __restrict__ bmass,
     }
     __syncthreads();
     bitonic_sort(key, id, P);
-    if (threadIdx.x == 0) {
-        float T = 0.f;
-        for (int j = 0; j < D.M; ++j) T += key[j];  // summed in the sorted order (Z11)
-        int ks = D.M;
-        if (D.gamma < 1.f) {
-            float Pf = 0.f;
-            for (int k = 1; k <= D.M; ++k) {
-                Pf += key[k - 1] / T;
-                if (Pf >= D.gamma) {
-                    ks = k;
-                    break;
-                }
+    // Alg. 1 lines 3-4 in parallel: contiguous chunks of the descending order per thread,
+    // a deterministic block scan of the chunk sums (T = total), then the first prefix
+    // k with P(k) >= gamma * T (a min-reduction over the threads' candidates).
+    __shared__ float warp_sums[32];
+    __shared__ int kmin;
+    const int nthr = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (D.M + nthr - 1) / nthr;
+    const int j0 = min(tid * per, D.M), j1 = min(j0 + per, D.M);
+    float local = 0.f;
+    for (int j = j0; j < j1; ++j) local += key[j];
+    float incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    if (tid == 0) kmin = D.M;
+    __syncthreads();
+    if (wid == 0) {
+        float w = lane < (nthr >> 5) ? warp_sums[lane] : 0.f;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += v;
+        }
+        warp_sums[lane] = w;  // inclusive warp prefix
+    }
+    __syncthreads();
+    const float T = warp_sums[(nthr >> 5) - 1];
+    float run = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0.f);  // exclusive prefix
+    if (D.gamma < 1.f) {
+        const float target = D.gamma * T;
+        for (int j = j0; j < j1; ++j) {
+            run += key[j];
+            if (run >= target) {
+                atomicMin(&kmin, j + 1);  // integer min: order-independent
+                break;
             }
         }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int ks = D.gamma < 1.f ? kmin : D.M;
         kstar[hl] = ks;
         budget[hl] = static_cast<float>(ks) / D.M;
     }
@@ -288,8 +383,6 @@ __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __
     float* key = reinterpret_cast<float*>(sm);
     int* id = reinterpret_cast<int*>(key + next_pow2(D.M));
     int* rank = id + next_pow2(D.M);
-    __shared__ int warp_tot[32];
-    __shared__ int base_s;
     const float* row = L + (static_cast<long long>(c) * D.M + m) * D.M;
     for (int n = threadIdx.x; n < P; n += blockDim.x) {
         key[n] = (n < m) ? row[n] : -INFINITY;
@@ -303,33 +396,21 @@ __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __
     const int grp = D.gb + c;
     const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int h = h0; h < h1; ++h) {
+    // One warp per head: ballot compaction of {n <= m : n == m or rank[n] < K - 1}.
+    for (int h = h0 + wid; h < h1; h += nw) {
         const int hl = h - D.qb;
         const int K = row_count(D, kstar[hl], m);
         const int keep = K - 1;  // non-diagonal blocks kept (diagonal forced, Z15)
         int* out = block_idx + (static_cast<long long>(hl) * D.M + m) * D.M;
-        if (threadIdx.x == 0) base_s = 0;
-        __syncthreads();
-        for (int base = 0; base <= m; base += blockDim.x) {
-            const int n = base + threadIdx.x;
+        int base = 0;
+        for (int n0 = 0; n0 <= m; n0 += 32) {
+            const int n = n0 + lane;
             const bool f = (n <= m) && (n == m || rank[n] < keep);
             const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (lane == 0) warp_tot[wid] = __popc(bal);
-            __syncthreads();
-            int off = base_s;
-            for (int w2 = 0; w2 < wid; ++w2) off += warp_tot[w2];
-            off += __popc(bal & ((1u << lane) - 1u));
-            if (f) out[off] = n;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int s = 0;
-                for (int w2 = 0; w2 < nw; ++w2) s += warp_tot[w2];
-                base_s += s;
-            }
-            __syncthreads();
+            if (f) out[base + __popc(bal & ((1u << lane) - 1u))] = n;
+            base += __popc(bal);
         }
-        if (threadIdx.x == 0) block_cnt[static_cast<long long>(hl) * D.M + m] = K;
-        __syncthreads();
+        if (lane == 0) block_cnt[static_cast<long long>(hl) * D.M + m] = K;
     }
 }
 
@@ -363,7 +444,12 @@ cudaError_t launch_pool(const Dims& D, const void* Q, const void* K, float* qsum
         pool_kernel<float><<<blocks_for(thr, 256), 256, 0, st>>>(
             D, static_cast<const float*>(Q), static_cast<const float*>(K), qsum, ksum,
             static_cast<float*>(Pq), static_cast<float*>(Pk));
-    else
+    else if (D.d % 8 == 0 && (qsum == nullptr) == (ksum == nullptr) && (Pq == nullptr) == (Pk == nullptr)) {
+        const long long t2 = static_cast<long long>(D.gl) * D.Ns * (D.d / 8);
+        pool_bf16_kernel<<<blocks_for(t2, 256), 256, 0, st>>>(
+            D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), qsum,
+            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));
+    } else
         pool_kernel<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
             D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), qsum,
             ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));

@@ -17,6 +17,8 @@
 //   warps 2-5 epilogue: thread = tile row (TMEM lane), tcgen05.ld 128 columns, mode math.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -57,6 +59,7 @@ struct ScoreParams {
     float* L;           // MAXPOOL: [gl][M][M] (natural log)
 };
 
+template <int kEmu>   // of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4)
 __global__ void __launch_bounds__(kThreads, 2)
 score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 ScoreParams p) {
@@ -171,14 +174,15 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 // window c covers sampled key columns [32c, 32c + 32) = block column 4u + c
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    float w = -INFINITY;
+                    // max of the raw logits first (the scale is positive), 4 chains
+                    float w4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const int col = c * 32 + e;
-                        float x = __uint_as_float(raw[c][e]) * p.sc2 - lse_row;
-                        if (diag && col > rr) x = -INFINITY;
-                        w = fmaxf(w, x);
+                        const float x = (diag && col > rr) ? -INFINITY : __uint_as_float(raw[c][e]);
+                        w4[e & 3] = fmaxf(w4[e & 3], x);
                     }
+                    float w = fmaxf(fmaxf(w4[0], w4[1]), fmaxf(w4[2], w4[3])) * p.sc2 - lse_row;
                     w = warp_max(w);
                     if (lane == 0) {
                         const int m = tr * 4 + quarter, n = u * 4 + c;
@@ -186,28 +190,52 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                 }
             } else {
-                float x[128];
+                // raw logits; causal mask inside the diagonal tile; 8 independent max chains
+                if (diag) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > rr) raw[c][e] = 0xff800000u;  // -inf
+                }
+                float mx[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mx[k] = __uint_as_float(raw[k >> 1][(k & 1) * 16]);
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int col = c * 32 + e;
-                        const float v = __uint_as_float(raw[c][e]) * p.sc2;
-                        x[col] = (diag && col > rr) ? -INFINITY : v;
+                    for (int e = 0; e < 32; ++e)
+                        mx[c * 2 + (e >> 4)] = fmaxf(mx[c * 2 + (e >> 4)], __uint_as_float(raw[c][e]));
+                const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.sc2;
+                const float ref = (p.mode == kLse) ? fmaxf(m_run, tmax) : tmax;
+                const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
+                const uint64_t nref = f2_pack(-ref, -ref);
+                uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const int e0 = 2 * c;
+                    const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
+                                                       __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
+                                               sc2, nref);
+                    float e0v, e1v;
+                    if ((c & 3) < kEmu) {
+                        ex2_poly2_d4(x2, e0v, e1v);
+                    } else {
+                        float x0, x1;
+                        f2_unpack(x2, x0, x1);
+                        e0v = ex2(x0);
+                        e1v = ex2(x1);
                     }
-                float tmax = x[0];
-#pragma unroll
-                for (int e = 1; e < 128; ++e) tmax = fmaxf(tmax, x[e]);
-                float acc = 0.f;
+                    acc2[c & 3] = f2_add(acc2[c & 3], f2_pack(e0v, e1v));
+                }
+                float a0, a1;
+                f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
+                const float acc = a0 + a1;
                 if (p.mode == kLse) {
-                    const float m_new = fmaxf(m_run, tmax);
-#pragma unroll
-                    for (int e = 0; e < 128; ++e) acc += ex2(x[e] - m_new);
-                    s_run = s_run * ex2(m_run - m_new) + acc;
-                    m_run = m_new;
+                    s_run = s_run * ex2(m_run - ref) + acc;
+                    m_run = ref;
                 } else {
-#pragma unroll
-                    for (int e = 0; e < 128; ++e) acc += ex2(x[e] - tmax);
                     const long long o = (static_cast<long long>(prob) * p.M + u) * 128 + rr;
                     p.part_m[o] = tmax;
                     p.part_s[o] = acc;
@@ -256,40 +284,80 @@ __global__ void fill_neg_inf_kernel(float* L, long long n) {
     if (i < n) L[i] = -INFINITY;
 }
 
-// Alg. 1 lines 2-4 for one local head per CTA: combine per-(row, block) partials into the
-// row lse, block masses a[n] = (1/b^2) sum_t s_tn 2^(m_tn - lse_t), then sort + prefix.
-__global__ void budget_combine_kernel(int M, float gamma, const float* __restrict__ part_m,
-                                      const float* __restrict__ part_s, float* __restrict__ bmass) {
-    __shared__ float lse_s[128];
+// Alg. 1 lines 1-2 for one local head per CTA (1024 threads): combine the per-(row, block)
+// partials [u][t] into the row lse (8 chunk partials per row, merged in a fixed order),
+// then block masses a[u] = (1/b^2) sum_t s_tu 2^(m_tu - lse_t), one warp per block.
+__global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float* __restrict__ part_m,
+                                                              const float* __restrict__ part_s,
+                                                              float* __restrict__ bmass) {
+    __shared__ float cm[8][128], cs[8][128], lse_s[128];
     const int hl = blockIdx.x;
     const float* pm = part_m + static_cast<long long>(hl) * M * 128;
     const float* ps = part_s + static_cast<long long>(hl) * M * 128;
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
-        float mx = -INFINITY;
-        for (int n = 0; n < M; ++n) mx = fmaxf(mx, pm[static_cast<long long>(n) * 128 + t]);
-        float s = 0.f;
-        for (int n = 0; n < M; ++n) {
-            const long long o = static_cast<long long>(n) * 128 + t;
-            s += ps[o] * ex2(pm[o] - mx);
+    const int t = threadIdx.x & 127, c = threadIdx.x >> 7;
+    const int per = (M + 7) / 8;
+    const int u0 = c * per, u1 = min(u0 + per, M);
+    float m = -INFINITY, sum = 0.f;
+#pragma unroll 4
+    for (int u = u0; u < u1; ++u) {
+        const float mu = __ldg(pm + static_cast<long long>(u) * 128 + t);
+        const float su = __ldg(ps + static_cast<long long>(u) * 128 + t);
+        if (mu > m) {
+            sum = sum * ex2(m - mu) + su;
+            m = mu;
+        } else {
+            sum += su * ex2(mu - m);
         }
-        lse_s[t] = mx + __log2f(s);
+    }
+    cm[c][t] = m;
+    cs[c][t] = sum;
+    __syncthreads();
+    if (c == 0) {
+        float mx = -INFINITY;
+        for (int k = 0; k < 8; ++k) mx = fmaxf(mx, cm[k][t]);
+        float s2 = 0.f;
+        for (int k = 0; k < 8; ++k) s2 += cs[k][t] * ex2(cm[k][t] - mx);
+        lse_s[t] = mx + __log2f(s2);
     }
     __syncthreads();
-    for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float l4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) l4[k] = lse_s[lane + 32 * k];
+    for (int u = w; u < M; u += 32) {
+        const float* pmu = pm + static_cast<long long>(u) * 128;
+        const float* psu = ps + static_cast<long long>(u) * 128;
         float a = 0.f;
-        for (int t = 0; t < 128; ++t) {
-            const long long o = static_cast<long long>(n) * 128 + t;
-            a += ps[o] * ex2(pm[o] - lse_s[t]);
-        }
-        bmass[static_cast<long long>(hl) * M + n] = a / (128.f * 128.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a += __ldg(psu + lane + 32 * k) * ex2(__ldg(pmu + lane + 32 * k) - l4[k]);
+        a = warp_sum(a);
+        if (lane == 0) bmass[static_cast<long long>(hl) * M + u] = a / (128.f * 128.f);
     }
-    (void)gamma;
+}
+
+// Exp2 split between MUFU and the FMA pipe in the score epilogues (x/4 of the column
+// pairs on the FMA pipe); PROXYATTN_SCORE_EMU=0..3 overrides the default.
+int score_emu() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PROXYATTN_SCORE_EMU");
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+    }
+    return v;
+}
+
+using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
+
+ScoreKernel score_kernel() {
+    const int e = score_emu();
+    return e == 0 ? score_tc_kernel<0> : e == 1 ? score_tc_kernel<1> : e == 2 ? score_tc_kernel<2>
+                                                                      : score_tc_kernel<3>;
 }
 
 bool set_smem_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(score_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmem)) != cudaSuccess)
             return false;
         done = true;
@@ -334,7 +402,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.part_s = part_s;
     const unsigned grid = static_cast<unsigned>(D.gl) * p.n_tr * p.n_chunks;
     p.mode = kLse;
-    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const long long rws = static_cast<long long>(D.gl) * D.Ns;
@@ -347,7 +415,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.mode = kMaxpool;
     p.lse2 = lse2;
     p.L = L;
-    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     return cudaGetLastError();
 }
 
@@ -369,10 +437,10 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
     p.part_m = scratch;
     p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
     const unsigned grid = static_cast<unsigned>(D.Hl) * p.n_chunks;
-    score_tc_kernel<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    budget_combine_kernel<<<D.Hl, 256, 0, st>>>(D.M, D.gamma, p.part_m, p.part_s, bmass);
+    budget_combine_kernel<<<D.Hl, 1024, 0, st>>>(D.M, p.part_m, p.part_s, bmass);
     return cudaGetLastError();
 }
 

@@ -244,6 +244,27 @@ __device__ __forceinline__ void ex2_poly2(uint64_t x2, float& r0, float& r1) {
     r1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
 
+// Degree-4 variant (max rel. error 2.7e-6) for the estimation's log-sum-exps, where the
+// result feeds the 1e-4 gate on L rather than a bf16 operand.
+__device__ __forceinline__ void ex2_poly2_d4(uint64_t x2, float& r0, float& r1) {
+    float a, b;
+    f2_unpack(x2, a, b);
+    x2 = f2_pack(fmaxf(a, -125.f), fmaxf(b, -125.f));
+    const uint64_t t2 = f2_add(x2, f2_pack(12582912.f, 12582912.f));
+    const uint64_t j2 = f2_add(t2, f2_pack(-12582912.f, -12582912.f));
+    const uint64_t f2 = f2_fma(j2, f2_pack(-1.f, -1.f), x2);
+    uint64_t p2 = f2_fma(f2_pack(0.009570080786943436f, 0.009570080786943436f), f2,
+                         f2_pack(0.05591782182455063f, 0.05591782182455063f));
+    p2 = f2_fma(p2, f2, f2_pack(0.240247443318367f, 0.240247443318367f));
+    p2 = f2_fma(p2, f2, f2_pack(0.6931217908859253f, 0.6931217908859253f));
+    p2 = f2_fma(p2, f2, f2_pack(0.9999992847442627f, 0.9999992847442627f));
+    float p0, p1, t0, t1;
+    f2_unpack(p2, p0, p1);
+    f2_unpack(t2, t0, t1);
+    r0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+    r1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
