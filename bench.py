@@ -39,6 +39,14 @@ METRIC = "ms per attention layer at 128K (Llama-3.1-8B shape) and speedup vs den
 WORKLOAD = dict(name="llama3.1-8b-attn-128k", n_q_heads=32, n_kv_heads=8, head_dim=128,
                 seq_len=131072, block_size=128, stride=4, n_groups=1, gamma=0.9,
                 min_budget_tokens=0, seed=0, preset="llama-128k")
+WORKLOADS = {
+    "llama3.1-8b-attn-128k": WORKLOAD,
+    # BASELINE.json configs[3]: Qwen2.5-7B attention shape, 64K, g = 4, min budget 2048
+    "qwen2.5-7b-attn-64k": dict(name="qwen2.5-7b-attn-64k", n_q_heads=28, n_kv_heads=4,
+                                head_dim=128, seq_len=65536, block_size=128, stride=4,
+                                n_groups=4, gamma=0.9, min_budget_tokens=2048, seed=0,
+                                preset="qwen-64k"),
+}
 L2_FLUSH_BYTES = 256 << 20
 KERNELS_PER_STEP = 8   # pool, proxy_lse, proxy_maxpool, budget_lse, budget_mass, finalize, select, attn
 
@@ -110,12 +118,12 @@ class ClockSampler:
 
 
 def build_config(pa, rank: int, ws: int, w=WORKLOAD):
-    Hq, Hkv, g = w["n_q_heads"], w["n_kv_heads"], w["n_groups"]
-    assert Hkv % ws == 0 or ws == 1, "shard count must divide the kv heads"
-    per = Hq // ws
-    b, e = (rank * per, (rank + 1) * per) if ws > 1 else (0, 0)
-    return pa.Config(Hq, Hkv, w["head_dim"], w["seq_len"], w["block_size"], w["stride"], g,
-                     w["gamma"], w["min_budget_tokens"], q_head_begin=b, q_head_end=e)
+    from paper_2509_24745_b200 import shard
+
+    cfg = pa.Config(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"],
+                    w["block_size"], w["stride"], w["n_groups"], w["gamma"],
+                    w["min_budget_tokens"])
+    return shard.shard_config(cfg, ws, rank)
 
 
 def gen_inputs(w, device):
@@ -127,10 +135,12 @@ def gen_inputs(w, device):
 
 
 # ------------------------------------------------------------------------ oracle --
-def oracle_sample(w, Q, K, V, cnt_full=None, budget_s=10.0):
-    """Time the fp64 CPU oracle on a bounded sample of the layer and extrapolate to a full
-    layer (ms).  Sample: proxy scores for a few block rows, Alg. 1 for one head, selection
-    on those rows, attention for a few (head, block-row) items."""
+def oracle_sample(w, Q, K, V):
+    """Time the fp64 CPU oracle (as it stands) on a bounded sample of one layer and
+    extrapolate to the full layer (ms).  Sample: pooling (full), Alg. 1 budgets of every
+    head (full), proxy scores + selection of 3 block rows (scaled by logit / row count),
+    block-sparse attention of 4 (head, row) items of the two densest heads (scaled by the
+    layer's selected-block count under the oracle's own budgets)."""
     import oracle
 
     oc = oracle.Cfg(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"],
@@ -140,45 +150,45 @@ def oracle_sample(w, Q, K, V, cnt_full=None, budget_s=10.0):
     Qf = Q.float().cpu().numpy()
     Kf = K.float().cpu().numpy()
     Vf = V.float().cpu().numpy()
+    t = {}
     t0 = time.perf_counter()
     Pq, Pk, scale = oracle.pool(oc, Qf, Kf)
-    t_pool = time.perf_counter() - t0
+    t["pool_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    kst, _, _, _ = oracle.budgets(oc, Qf, Kf)
+    t["budget_s"] = time.perf_counter() - t0
     rows = [M // 8, M // 2, M - 1]
     t0 = time.perf_counter()
     _, L = oracle.proxy_scores(oc, Pq, Pk, scale, rows=rows)
     t_rows = time.perf_counter() - t0
     logits_rows = sum(bs * (m * bs) + bs * (bs + 1) / 2 for m in rows)
     logits_all = oc.n_groups * Ns * (Ns + 1) / 2
-    t_proxy = t_rows * logits_all / logits_rows
-    t0 = time.perf_counter()
-    ks, _, _, _ = oracle.budgets(oc, Qf, Kf, heads=[0])
-    t_budget = (time.perf_counter() - t0) * oc.n_q_heads
-    kst = np.full(oc.n_q_heads, max(int(ks[0]), 1), np.int32)
+    t["proxy_s"] = t_rows * logits_all / logits_rows
     t0 = time.perf_counter()
     cnt, idx, _ = oracle.select(oc, np.nan_to_num(L, nan=-np.inf), kst, rows=rows)
-    t_sel = (time.perf_counter() - t0) * M / len(rows)
-    items = np.array([[h, m] for h in (0, 17) for m in rows], np.int32).reshape(-1)
+    t["select_s"] = (time.perf_counter() - t0) * M / len(rows)
+    dense_heads = [int(h) for h in np.argsort(-kst, kind="stable")[:2]]
+    items = [(h, m) for h in dense_heads for m in (M // 2, M - 1)]
     t0 = time.perf_counter()
     oracle.attention(oc, Qf, Kf, Vf, cnt, idx, items=items)
     t_att_s = time.perf_counter() - t0
-    sel_blocks = sum(int(cnt[h, m]) for h in (0, 17) for m in rows)
-    total_blocks = (int(cnt_full.sum()) if cnt_full is not None else
-                    sum(oracle.row_count(oc, int(kst[0]), m) for m in range(M)) * oc.n_q_heads)
-    t_att = t_att_s * total_blocks / max(sel_blocks, 1)
-    total = t_pool + t_proxy + t_budget + t_sel + t_att
-    sample = (f"pool full; proxy rows {rows} of {M} (x{logits_all / logits_rows:.0f} by logit "
-              f"count); Alg.1 head 0 (x{oc.n_q_heads}); select {len(rows)} rows; attention "
-              f"{len(items) // 2} (head,row) items (x{total_blocks / max(sel_blocks, 1):.0f} by "
-              f"selected blocks); extrapolated to one full layer")
-    return total * 1e3, sample, oracle.num_threads(), dict(
-        pool_s=t_pool, proxy_s=t_proxy, budget_s=t_budget, select_s=t_sel, attention_s=t_att)
+    sel_blocks = sum(int(cnt[h, m]) for h, m in items)
+    total_blocks = sum(oracle.row_count(oc, int(k), m) for k in kst for m in range(M))
+    t["attention_s"] = t_att_s * total_blocks / max(sel_blocks, 1)
+    total = sum(t.values())
+    sample = (f"pool and Alg. 1 of all {oc.n_q_heads} heads in full; proxy scores of block "
+              f"rows {rows} of {M} (x{logits_all / logits_rows:.0f} by logit count) and their "
+              f"selection (x{M / len(rows):.0f}); attention of {len(items)} (head,row) items of "
+              f"the densest heads, {sel_blocks} blocks (x{total_blocks / max(sel_blocks, 1):.0f} "
+              f"to the layer's {total_blocks} selected blocks); extrapolated to one layer")
+    return total * 1e3, sample, oracle.num_threads(), t
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    w = WORKLOAD
+    w = dict(WORKLOADS[args.workload])
     Q, K, V, meta = gen_inputs(w, "cpu")
     vals = []
     sample = cores = None
@@ -212,10 +222,10 @@ def run_ours(args):
         dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    w = dict(WORKLOAD)
+    w = dict(WORKLOADS[args.workload])
     if args.seq_len:
         w["seq_len"] = args.seq_len
-        w["name"] = f"llama3.1-8b-attn-{args.seq_len // 1024}k"
+        w["name"] = w["name"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
     cfg = build_config(pa, rank, ws, w)
     Q, K, V, meta = gen_inputs(w, dev)
     hb, he = cfg.local_heads
@@ -232,24 +242,11 @@ def run_ours(args):
     idx = torch.empty(Hl, M, M, dtype=torch.int32, device=dev)
     O = torch.empty_like(Ql)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    group_split = ws > 1 and cfg.n_groups < ws
+    from paper_2509_24745_b200 import shard
 
     def estimate():
-        if group_split:   # proxy group spans ranks: pool -> all-reduce -> scores
-            import torch.distributed as dist
-
-            qsum, ksum = pa.pool(cfg, Ql, Kl)
-            dist.all_reduce(qsum)
-            dist.all_reduce(ksum)
-            L = pa.proxy_scores(cfg, qsum, ksum, wsp)
-            pa._lib._check(pa.lib().proxyattn_budgets(
-                pa._lib._cfg_ref(cfg), pa._lib._ptr(Ql), pa._lib._ptr(Kl), pa._lib._ptr(wsp),
-                wsp.numel(), pa._lib._ptr(kstar), pa._lib._ptr(budget), pa._lib._stream(dev)))
-            pa._lib._check(pa.lib().proxyattn_select(
-                pa._lib._cfg_ref(cfg), pa._lib._ptr(L), pa._lib._ptr(kstar), pa._lib._ptr(cnt),
-                pa._lib._ptr(idx), pa._lib._stream(dev)))
-        else:
-            pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
+        # g < #ranks: pool -> NCCL all-reduce of the pooled sums -> scores
+        shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=(kstar, budget, cnt, idx))
 
     def prefill():
         pa.prefill(cfg, Ql, Kl, Vl, cnt, idx, O)
@@ -303,13 +300,16 @@ def run_ours(args):
                        dtype=torch.float64, device=dev)
     sel_blocks = float(cnt.sum().item())
     blocks_t = torch.tensor([sel_blocks], dtype=torch.float64, device=dev)
+    per_rank_blocks = [sel_blocks]
     if ws > 1:
         import torch.distributed as dist
 
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-        dist.all_reduce(blocks_t, op=dist.ReduceOp.SUM)
+        parts = [torch.empty_like(blocks_t) for _ in range(ws)]
+        dist.all_gather(parts, blocks_t)
+        per_rank_blocks = [float(p.item()) for p in parts]
     layer_ms, est_m, att_m, dense_m = vec.tolist()
-    total_blocks = blocks_t.item()
+    total_blocks = float(sum(per_rank_blocks))
 
     # e2e through the C-ABI host path (H2D of Q/K/V and D2H of O inside the timed region)
     e2e = None
@@ -346,20 +346,21 @@ def run_ours(args):
     dense_blocks = w["n_q_heads"] * Mfull * (Mfull + 1) / 2
     sparsity = 1.0 - total_blocks / dense_blocks
     b, d = w["block_size"], w["head_dim"]
-    flops_exec = 4.0 * b * b * d * total_blocks / ws      # per rank (attention kernel)
+    flops_exec = 4.0 * b * b * d * max(per_rank_blocks)    # the slowest rank's attention
     pk = peaks()
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops_exec / (att_m * 1e-3) / 1e12
+    kname = "attn_tc4_kernel" if os.environ.get("PROXYATTN_ATTN", "3").startswith("4") else "attn_tc_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(w["name"])
+        try:   # dram read + write bytes per launch from the committed ncu --set full capture
+            traffic = json.load(open(tp)).get(w["name"], {}).get(kname)
         except Exception:
             traffic = None
     cpu = None
     if ws == 1 and not args.no_cpu:
-        ms, sample, cores, parts = oracle_sample(w, Q.cpu(), K.cpu(), V.cpu(), cnt.cpu().numpy())
+        ms, sample, cores, parts = oracle_sample(w, Q.cpu(), K.cpu(), V.cpu())
         cpu = {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample}
     clocks = getattr(clk, "result", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []})
     line = {
@@ -376,6 +377,7 @@ def run_ours(args):
         "dtype": "bf16",
         "data": "synthetic (structured generator, SURVEY §8d; seed 0; inputs resident in HBM)",
         "config": {"workload": w["name"], "heads": f"{w['n_q_heads']}/{w['n_kv_heads']}",
+                   "preset": w["preset"],
                    "head_dim": d, "seq_len": w["seq_len"], "block": b, "stride": w["stride"],
                    "proxy_groups": w["n_groups"], "gamma": w["gamma"],
                    "min_budget_tokens": w["min_budget_tokens"],
@@ -387,11 +389,12 @@ def run_ours(args):
         "prefill_ms": att_m,
         "sparsity": sparsity,
         "tflops_exec": achieved,
-        "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (A7)", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": f"{kname} (A7)", "achieved": achieved,
                      "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
                      "traffic": traffic,
                      "peak_source": pk["_source"] + " bf16_tflops_sustained",
                      "algorithmic": "4*b^2*d FLOP per executed (head,row,block) = 8.39 MFLOP"},
+        "work_share": [x / total_blocks for x in per_rank_blocks],
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": KERNELS_PER_STEP * args.steps,
@@ -411,6 +414,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq-len", type=int, default=0, help="override N (sweep)")
+    ap.add_argument("--workload", default="llama3.1-8b-attn-128k", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()

@@ -143,6 +143,13 @@ def _i32(a) -> np.ndarray | None:
     return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
 
 
+def _items(items) -> np.ndarray | None:
+    """(head, block row) pairs as an [n][2] int32 array (accepts flat or paired input)."""
+    if items is None:
+        return None
+    return np.ascontiguousarray(np.asarray(items, dtype=np.int32).reshape(-1, 2))
+
+
 def validate(cfg: Cfg) -> bool:
     c = cfg.c()
     return lib().oracle_validate(ctypes.byref(c)) == 0
@@ -239,7 +246,7 @@ def attention(cfg: Cfg, Q, K, V, block_cnt, block_idx, items=None):
     Q, K, V = _f32(Q), _f32(K), _f32(V)
     cnt = _i32(block_cnt)
     idx = _i32(block_idx)
-    it = _i32(items)
+    it = _items(items)
     O = np.full((cfg.n_q_heads, cfg.seq_len, cfg.head_dim), np.nan)
     lib().oracle_attention(ctypes.byref(c), _ptr(Q), _ptr(K), _ptr(V), _ptr(cnt), _ptr(idx),
                            _ptr(it), 0 if it is None else len(it), _ptr(O))
@@ -250,7 +257,7 @@ def dense(cfg: Cfg, Q, K, V, items=None):
     """Dense causal attention = O10 with every causal block."""
     c = _check(cfg)
     Q, K, V = _f32(Q), _f32(K), _f32(V)
-    it = _i32(items)
+    it = _items(items)
     O = np.full((cfg.n_q_heads, cfg.seq_len, cfg.head_dim), np.nan)
     lib().oracle_dense(ctypes.byref(c), _ptr(Q), _ptr(K), _ptr(V), _ptr(it),
                        0 if it is None else len(it), _ptr(O))

@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/proxyattn.h"
@@ -89,6 +90,24 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     D.gl = pa::group_of_q(D, D.qe - 1) - D.gb + 1;
     return PROXYATTN_OK;
 }
+
+}  // namespace
+
+namespace pa {
+// A7 kernel variant: 3 = attn_tc (two query-row slots per CTA sharing K/V tiles; default,
+// measured fastest), 4 = attn_tc4 (double-buffered S, column-split softmax).
+// PROXYATTN_ATTN=3|4 overrides the default.
+int attn_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PROXYATTN_ATTN");
+        v = (e && e[0] == '4') ? 4 : 3;
+    }
+    return v;
+}
+}  // namespace pa
+
+namespace {
 
 bool groups_complete(const pa::Dims& D) { return D.qb % D.gq == 0 && D.qe % D.gq == 0; }
 
@@ -232,7 +251,10 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32) {
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
-        PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
+        if (pa::attn_variant() == 4)
+            PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
+        else
+            PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
     }
     return PROXYATTN_OK;
 }

@@ -1,0 +1,108 @@
+"""Multi-GPU orchestration of one ProxyAttn layer: query heads sharded by KV-head group
+(SURVEY.md §8(e)), one process per GPU, torch.distributed (NCCL) for the plumbing.
+
+* Each rank holds a contiguous, KV-aligned shard of query heads [b, e) and the KV heads
+  they use; everything after pooling (budgets, selection, attention) is per head and local.
+* When every proxy group touched by a shard lies inside it (g >= #ranks, e.g. Qwen g=4 on
+  <= 4 GPUs) there is NO cross-GPU traffic.
+* When a proxy group spans ranks (Llama g=1), Eq. 2's pooled sums are the one exchange
+  step: fp32 partial sums of the local heads are all-reduced (sum), then each rank rounds
+  them and computes the group's block scores itself (replicated, ~0.3 ms at 128K).
+* all_gather of O is for verification only (not part of the timed step).
+
+The ops are the C-ABI calls of paper_2509_24745_b200 by default; tests inject other ops
+with the same signatures to check the orchestration on CPU with the gloo backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+
+
+def head_shard(n_q_heads: int, n_kv_heads: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard of query heads aligned to KV heads, as balanced as KV heads allow."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    if n_kv_heads % world:
+        raise ValueError(f"{n_kv_heads} kv heads cannot be split evenly over {world} ranks")
+    r = n_q_heads // n_kv_heads
+    per_kv = n_kv_heads // world
+    return rank * per_kv * r, (rank + 1) * per_kv * r
+
+
+def shard_config(cfg, world: int, rank: int):
+    if world == 1:
+        return cfg.replace(q_head_begin=0, q_head_end=0)
+    b, e = head_shard(cfg.n_q_heads, cfg.n_kv_heads, world, rank)
+    return cfg.replace(q_head_begin=b, q_head_end=e)
+
+
+def group_spans_ranks(cfg, world: int) -> bool:
+    """True when a proxy group (Hq/g query heads) is split across ranks."""
+    if world == 1:
+        return False
+    b, e = head_shard(cfg.n_q_heads, cfg.n_kv_heads, world, 0)
+    return (e - b) % (cfg.n_q_heads // cfg.n_groups) != 0
+
+
+@dataclass
+class Ops:
+    """The hot-path calls (C-ABI by default); signatures follow paper_2509_24745_b200."""
+
+    estimate: Callable
+    pool: Callable
+    proxy_scores: Callable
+    budgets: Callable
+    select: Callable
+
+
+def default_ops() -> Ops:
+    from . import _lib
+
+    return Ops(_lib.estimate, _lib.pool, _lib.proxy_scores, _lib.budgets, _lib.select)
+
+
+def estimate_sharded(cfg, Q_local, K_local, world: int, workspace=None, ops: Optional[Ops] = None,
+                     all_reduce: Optional[Callable] = None, out=None):
+    """A1-A6 for the local shard `cfg` (q_head_begin/end set).  Returns
+    (kstar, budget, block_cnt, block_idx) for the local heads."""
+    ops = ops or default_ops()
+    if not group_spans_ranks(cfg, world):
+        return ops.estimate(cfg, Q_local, K_local, workspace, out)
+    if all_reduce is None:
+        import torch.distributed as dist
+
+        all_reduce = dist.all_reduce
+    qsum, ksum = ops.pool(cfg, Q_local, K_local)          # fp32 partial sums, local heads
+    all_reduce(qsum)                                      # the single exchange
+    all_reduce(ksum)
+    L = ops.proxy_scores(cfg, qsum, ksum, workspace)      # replicated per rank
+    kstar, budget = ops.budgets(cfg, Q_local, K_local, workspace)
+    cnt, idx = ops.select(cfg, L, kstar)
+    if out is not None:
+        for dst, src in zip(out, (kstar, budget, cnt, idx)):
+            dst.copy_(src)
+        return out
+    return kstar, budget, cnt, idx
+
+
+def gather_heads(t_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """all_gather of a head-major local tensor into the full head dimension (verification)."""
+    import torch.distributed as dist
+
+    parts = [torch.empty_like(t_local) for _ in range(world)]
+    dist.all_gather(parts, t_local.contiguous(), group=group)
+    return torch.cat(parts, dim=0)
+
+
+def work_share(block_cnt_full: torch.Tensor, n_kv_heads: int, world: int) -> list[float]:
+    """Executed (head, row, block) units per rank under head sharding, as fractions."""
+    H = block_cnt_full.shape[0]
+    tot = float(block_cnt_full.sum())
+    out = []
+    for r in range(world):
+        b, e = head_shard(H, n_kv_heads, world, r)
+        out.append(float(block_cnt_full[b:e].sum()) / tot)
+    return out

@@ -1,0 +1,120 @@
+"""Full-size parity on the bench configuration (128K tokens, Llama-3.1-8B attention shape,
+the same launch configuration bench.py times), checked against the oracle on SAMPLED
+outputs the oracle can compute one by one: L rows, Alg. 1 budgets of sampled heads,
+selected blocks on sampled rows (margin-gated), and O on sampled (head, row)
+items with the GPU mask injected.  Plus properties that hold at any size."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2509_24745_b200 as pa
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 1e-4
+
+
+@pytest.fixture(scope="module")
+def layer():
+    dev = torch.device("cuda:0")
+    N = 131072
+    cfg = pa.Config(32, 8, 128, N, 128, 4, 1, 0.9, 0)
+    Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=workloads.PRESETS["llama-128k"],
+                                      device=dev)
+    kstar, budget, cnt, idx = pa.estimate(cfg, Q, K)
+    O = pa.prefill(cfg, Q, K, V, cnt, idx)
+    qsum, ksum = pa.pool(cfg, Q, K)
+    L = pa.proxy_scores(cfg, qsum, ksum)
+    torch.cuda.synchronize()
+    oc = oracle.Cfg(32, 8, 128, N, 128, 4, 1, 0.9, 0, round_bf16=True)
+    host = dict(Q=Q.float().cpu().numpy(), K=K.float().cpu().numpy(), V=V.float().cpu().numpy())
+    return dict(cfg=cfg, oc=oc, kstar=kstar.cpu().numpy(), budget=budget.cpu().numpy(),
+                cnt=cnt.cpu().numpy(), idx=idx, O=O, L=L.cpu().numpy(), **host)
+
+
+def test_fullsize_properties(layer):
+    cfg, cnt, ks = layer["cfg"], layer["cnt"], layer["kstar"]
+    M = cfg.M
+    assert np.all((ks >= 1) & (ks <= M))
+    np.testing.assert_allclose(layer["budget"], ks / M, rtol=1e-6)
+    # A5 closed form (Z12) on every (head, row)
+    m = np.arange(M)[None, :]
+    K = np.minimum(m + 1, np.maximum((ks[:, None].astype(np.int64) * (m + 1) + M - 1) // M, 1))
+    assert np.array_equal(cnt, K)
+    # lists: ascending, causal, diagonal last, nested across heads of the group by budget
+    idx = layer["idx"]
+    for h in (0, 7, 19, 31):
+        for mm in (0, 1, M // 3, M - 1):
+            lst = idx[h, mm, :cnt[h, mm]].cpu().numpy()
+            assert lst[-1] == mm and np.all(np.diff(lst) > 0) and lst[0] >= 0
+    L = layer["L"][0]
+    assert np.all(np.isneginf(L[np.triu_indices(M, 1)]))
+    assert np.all(np.isfinite(L[np.tril_indices(M)]))
+    assert np.all(L[np.tril_indices(M)] <= 1e-6)            # log-probabilities
+    assert torch.isfinite(layer["O"]).all()
+
+
+def test_fullsize_sampled_parity(layer):
+    cfg, oc = layer["cfg"], layer["oc"]
+    M = cfg.M
+    rows = [0, 1, M // 4, M // 2, 3 * M // 4, M - 1]
+    Pq, Pk, scale = oracle.pool(oc, layer["Q"], layer["K"])
+    _, Lref = oracle.proxy_scores(oc, Pq, Pk, scale, rows=rows)
+    for m in rows:
+        ref = Lref[0, m, :m + 1]
+        got = layer["L"][0, m, :m + 1].astype(np.float64)
+        assert np.max(np.abs(got - ref)) <= 1e-4, m
+    # budgets of sampled heads (margin-gated)
+    heads = [0, 5, 17, 30]
+    ks_ref, _, bmg, _ = oracle.budgets(oc, layer["Q"], layer["K"], heads=heads)
+    for h in heads:
+        if bmg[h] > MARGIN:
+            assert layer["kstar"][h] == ks_ref[h], (h, layer["kstar"][h], ks_ref[h])
+        else:
+            assert abs(int(layer["kstar"][h]) - int(ks_ref[h])) <= 1
+    # selection on sampled rows from the oracle's L with the GPU budgets injected
+    Lfull = np.full((1, M, M), -np.inf)
+    Lfull[0, rows] = Lref[0, rows]
+    ocnt, oidx, cmg = oracle.select(oc, Lfull, layer["kstar"], rows=rows)
+    checked = 0
+    idx = layer["idx"]
+    for h in range(cfg.n_q_heads):
+        for m in rows:
+            assert layer["cnt"][h, m] == ocnt[h, m]
+            if cmg[h, m] > MARGIN:
+                c = ocnt[h, m]
+                assert np.array_equal(idx[h, m, :c].cpu().numpy(), oidx[h, m, :c]), (h, m)
+                checked += 1
+    assert checked >= 0.9 * cfg.n_q_heads * len(rows)
+    # O on sampled (head, row) items with the GPU mask injected
+    items = [(0, M - 1), (17, M - 1), (5, M // 2), (30, 1), (11, 0), (24, 3 * M // 4)]
+    cnt_h = layer["cnt"]
+    idx_h = np.zeros((cfg.n_q_heads, M, M), np.int32)
+    for h, m in items:
+        idx_h[h, m, :cnt_h[h, m]] = idx[h, m, :cnt_h[h, m]].cpu().numpy()
+    Oref = oracle.attention(oc, layer["Q"], layer["K"], layer["V"], cnt_h, idx_h,
+                            items=np.array(items, np.int32).reshape(-1))
+    O = layer["O"]
+    for h, m in items:
+        got = O[h, m * 128:(m + 1) * 128].float().cpu().numpy()
+        err = np.abs(got - Oref[h, m * 128:(m + 1) * 128])
+        assert err.max() <= 2e-2 and err.mean() <= 2e-3, (h, m, err.max(), err.mean())
+
+
+def test_fullsize_dense_sampled(layer):
+    cfg, oc = layer["cfg"], layer["oc"]
+    dev = torch.device("cuda:0")
+    M = cfg.M
+    Q = torch.from_numpy(layer["Q"]).to(dev).bfloat16()
+    K = torch.from_numpy(layer["K"]).to(dev).bfloat16()
+    V = torch.from_numpy(layer["V"]).to(dev).bfloat16()
+    Od = pa.dense_prefill(cfg, Q, K, V)
+    items = [(3, M - 1), (20, M // 3)]
+    Oref = oracle.dense(oc, layer["Q"], layer["K"], layer["V"],
+                        items=np.array(items, np.int32).reshape(-1))
+    for h, m in items:
+        got = Od[h, m * 128:(m + 1) * 128].float().cpu().numpy()
+        err = np.abs(got - Oref[h, m * 128:(m + 1) * 128])
+        assert err.max() <= 2e-2 and err.mean() <= 2e-3, (h, m, err.max(), err.mean())

@@ -488,6 +488,21 @@ def test_block_reduce_sum_example():
     assert mass[0, 0] * 4 == pytest.approx(GOLD["block_reduce_sum"]["value"], abs=1e-15)
 
 
+def test_item_subsets_match_full_rows():
+    cfg = oracle.Cfg(4, 2, 16, 512, 64, 4, 1, 0.8)
+    Q, K, V = rand_qkv(cfg, 21)
+    est = oracle.pipeline(cfg, Q, K, V)
+    items = [(3, 7), (0, 0), (2, 4)]
+    Os = oracle.attention(cfg, Q, K, V, est["block_cnt"], est["block_idx"], items=items)
+    Od = oracle.dense(cfg, Q, K, V, items=np.array(items).reshape(-1))
+    Of = oracle.dense(cfg, Q, K, V)
+    b = cfg.block_size
+    for h, m in items:
+        assert np.array_equal(Os[h, m * b:(m + 1) * b], est["O"][h, m * b:(m + 1) * b])
+        assert np.array_equal(Od[h, m * b:(m + 1) * b], Of[h, m * b:(m + 1) * b])
+    assert np.isnan(Os[1]).all()                      # rows not listed are not written
+
+
 def test_determinism():
     cfg = CFG_A.replace(seq_len=512)
     Q, K, V = rand_qkv(cfg, 20)
