@@ -156,6 +156,11 @@ const char* proxyattn_build_info(void);
  * fp32 outputs.  Used by the GPU tests to pin the descriptor encodings. */
 int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream);
 
+/* Diagnostic: copies the per-event clock64 timeline recorded for one CTA of the last
+ * attention launch when the process runs with PROXYATTN_TRACE=<cta index> (n entries of
+ * [2 sides][256 iterations][2 slots][8 events]).  E_CONFIG when tracing is off. */
+int proxyattn_debug_trace(long long* host_out, size_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,7 @@ _SIGS = {
     "proxyattn_last_error": ([], ctypes.c_char_p),
     "proxyattn_build_info": ([], ctypes.c_char_p),
     "proxyattn_debug_umma": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_debug_trace": ([_P, ctypes.c_size_t], ctypes.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -101,7 +101,7 @@ int attn_variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("PROXYATTN_ATTN");
-        v = (e && e[0] == '4') ? 4 : 3;
+        v = (e && e[0] == '4') ? 4 : (e && e[0] == '5') ? 5 : 3;
     }
     return v;
 }
@@ -253,6 +253,8 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     } else {
         if (pa::attn_variant() == 4)
             PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
+        else if (pa::attn_variant() == 5)
+            PA_CUDA(pa::launch_attn_tc5(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc5");
         else
             PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
     }
@@ -339,6 +341,13 @@ const char* proxyattn_last_error(void) { return g_err.c_str(); }
 
 const char* proxyattn_build_info(void) {
     return "libproxyattn sm_100a (tcgen05/TMEM/TMA attention; SIMT estimation v1)";
+}
+
+int proxyattn_debug_trace(long long* host_out, size_t n) {
+    long long* d = pa::attn_trace_ptr();
+    if (!d || !host_out) return fail(PROXYATTN_E_CONFIG, "no trace (set PROXYATTN_TRACE=<cta>)");
+    PA_CUDA(cudaMemcpy(host_out, d, n * sizeof(long long), cudaMemcpyDeviceToHost), "trace copy");
+    return PROXYATTN_OK;
 }
 
 int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream) {

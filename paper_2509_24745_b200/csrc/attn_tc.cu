@@ -12,8 +12,9 @@
 // per-head flags are general.
 //
 // Warp roles (320 threads):
-//   warp 0      TMA producer: Q tiles of both heads, then K/V tiles of each union block
-//               into a 2-stage ring (128 x 128 bf16 tiles = two SWIZZLE_128B boxes)
+//   warp 0      TMA producer: Q tiles of both slots, then the K tiles (3-stage ring, two
+//               union blocks ahead) and V tiles (2-stage ring) of each union block
+//               (128 x 128 bf16 tiles = two SWIZZLE_128B boxes)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, FA4-style order:
 //               S_s = Q_s K_u^T (SS)  and  O_s += P_s V_u (A = P_s from TMEM, B = V MN-major);
 //               S_s(u+1) is issued right after O_s += P_s(u) V(u) so each head's softmax
@@ -39,22 +40,24 @@ namespace {
 constexpr int kTileRows = 128;                   // b = 128 query rows / keys per tile
 constexpr int kBox = kTileRows * 64 * 2;         // 16 KB: [128 rows][64 bf16] SW128 box
 constexpr int kTile = 2 * kBox;                  // 32 KB: a 128 x 128 bf16 tile
-constexpr int kStages = 2;
+constexpr int kKStages = 3;   // K tiles are fetched two union blocks ahead (S runs ahead of PV)
+constexpr int kVStages = 2;
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;        // log2 units: P <= 2^8 before a rescale
 
 struct __align__(8) Bars {
     uint64_t q_full;
-    uint64_t k_full[kStages];
-    uint64_t v_full[kStages];
-    uint64_t kv_empty[kStages];
+    uint64_t k_full[kKStages];
+    uint64_t k_empty[kKStages];
+    uint64_t v_full[kVStages];
+    uint64_t v_empty[kVStages];
     uint64_t s_full[2];
     uint64_t p_half[2][2];   // [slot][half]: P columns for keys [64 h, 64 h + 64) are in TMEM
     uint64_t o_done[2];
     uint32_t tmem_base;
 };
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTile * (2 + 2 * kStages) + sizeof(Bars);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTile * (2 + kKStages + kVStages) + sizeof(Bars);
 
 // Ascending union of two ascending block lists (null list = dense 0..m).
 struct UnionWalk {
@@ -83,14 +86,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-               int r, int Hl, int pair_mode, float scale_log2) {
+               int r, int Hl, int pair_mode, float scale_log2, long long* trace, int trace_bid) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sQ = smem;                           // 2 tiles (slot 0, slot 1)
-    uint8_t* sK = smem + 2 * kTile;               // kStages tiles
-    uint8_t* sV = smem + kTile * (2 + kStages);   // kStages tiles
-    Bars* bars = reinterpret_cast<Bars*>(smem + kTile * (2 + 2 * kStages));
+    uint8_t* sK = smem + 2 * kTile;                // kKStages tiles
+    uint8_t* sV = smem + kTile * (2 + kKStages);   // kVStages tiles
+    Bars* bars = reinterpret_cast<Bars*>(smem + kTile * (2 + kKStages + kVStages));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -129,10 +132,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->q_full, 1);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kKStages; ++s) {
             mbar_init(&bars->k_full[s], 1);
+            mbar_init(&bars->k_empty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
             mbar_init(&bars->v_full[s], 1);
-            mbar_init(&bars->kv_empty[s], 1);
+            mbar_init(&bars->v_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars->s_full[s], 1);
@@ -160,43 +166,60 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tma_load_2d(sQ + s * kTile, &tmQ, &bars->q_full, 0, qrow);
                 tma_load_2d(sQ + s * kTile + kBox, &tmQ, &bars->q_full, 64, qrow);
             }
-            UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
-            int n, f;
-            for (int u = 0; it.next(n, f); ++u) {
-                const int st = u % kStages;
-                if (u >= kStages) mbar_wait(&bars->kv_empty[st], ((u / kStages) - 1) & 1);
-                const int krow = kvl * N + n * kTileRows;
-                uint8_t* k_dst = sK + st * kTile;
-                uint8_t* v_dst = sV + st * kTile;
+            // Two cursors over the union: K tiles run two blocks ahead of V tiles.
+            UnionWalk itk{list0, list1, cnt0, cnt1, 0, 0};
+            UnionWalk itv{list0, list1, cnt0, cnt1, 0, 0};
+            int uk = 0, nk, fk, nv, fv;
+            auto load_k = [&]() -> bool {
+                if (!itk.next(nk, fk)) return false;
+                const int st = uk % kKStages;
+                if (uk >= kKStages) mbar_wait(&bars->k_empty[st], ((uk / kKStages) - 1) & 1);
+                const int krow = kvl * N + nk * kTileRows;
                 mbar_expect_tx(&bars->k_full[st], kTile);
-                tma_load_2d(k_dst, &tmK, &bars->k_full[st], 0, krow);
-                tma_load_2d(k_dst + kBox, &tmK, &bars->k_full[st], 64, krow);
+                tma_load_2d(sK + st * kTile, &tmK, &bars->k_full[st], 0, krow);
+                tma_load_2d(sK + st * kTile + kBox, &tmK, &bars->k_full[st], 64, krow);
+                ++uk;
+                return true;
+            };
+            load_k();
+            load_k();
+            for (int u = 0; itv.next(nv, fv); ++u) {
+                load_k();                                  // block u + 2
+                const int st = u % kVStages;
+                if (u >= kVStages) mbar_wait(&bars->v_empty[st], ((u / kVStages) - 1) & 1);
+                const int vrow = kvl * N + nv * kTileRows;
                 mbar_expect_tx(&bars->v_full[st], kTile);
-                tma_load_2d(v_dst, &tmV, &bars->v_full[st], 0, krow);
-                tma_load_2d(v_dst + kBox, &tmV, &bars->v_full[st], 64, krow);
+                tma_load_2d(sV + st * kTile, &tmV, &bars->v_full[st], 0, vrow);
+                tma_load_2d(sV + st * kTile + kBox, &tmV, &bars->v_full[st], 64, vrow);
             }
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------- MMA issuer --
-        if (lane == 0) {
+        // The whole warp runs this (warp-uniform) loop so every descriptor lives in the
+        // uniform datapath; only tcgen05.mma / tcgen05.commit are issued by the elected lane.
+        {
             constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-            const uint32_t q_addr = smem_u32(sQ);
-            const uint32_t k_addr = smem_u32(sK);
-            const uint32_t v_addr = smem_u32(sV);
+            // descriptor bases; K-steps advance the 14-bit start-address field (16-B units)
+            const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+            const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+            const uint64_t dv = sdesc_sw128(smem_u32(sV), kBox, 1024);
+            const bool leader = elect_one();
             mbar_wait(&bars->q_full, 0);
             auto issue_s = [&](int slot, int u) {  // S_slot = Q_slot K(u)^T
-                const int st = u % kStages;
-                mbar_wait(&bars->k_full[st], (u / kStages) & 1);
+                const int st = u % kKStages;
+                mbar_wait(&bars->k_full[st], (u / kKStages) & 1);
                 tc_fence_after();
+                if (leader) {
+                    const uint64_t a0 = dq + (slot * kTile >> 4), b0 = dk + (st * kTile >> 4);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-                    umma_ss(tbase + slot * 128, sdesc_sw128(q_addr + slot * kTile + off, 16, 1024),
-                            sdesc_sw128(k_addr + st * kTile + off, 16, 1024), idesc_qk,
-                            kk > 0 ? 1u : 0u);
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
+                        umma_ss(tbase + slot * 128, a0 + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
+                    }
+                    tc_commit(&bars->s_full[slot]);
                 }
-                tc_commit(&bars->s_full[slot]);
+                __syncwarp();
             };
             UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
             int n_cur, f_cur, n_nxt = 0, f_nxt = 0;
@@ -205,35 +228,52 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (has) {
                 if (f_cur & 1) issue_s(0, 0);
                 if (f_cur & 2) issue_s(1, 0);
+                if (leader) tc_commit(&bars->k_empty[0]);   // K(0) consumed by every S using it
+                __syncwarp();
             }
             for (int u = 0; has; ++u) {
                 const bool has_nxt = it.next(n_nxt, f_nxt);
-                const int st = u % kStages;
-                mbar_wait(&bars->v_full[st], (u / kStages) & 1);
+                const int st = u % kVStages;
+                mbar_wait(&bars->v_full[st], (u / kVStages) & 1);
 #pragma unroll
                 for (int slot = 0; slot < 2; ++slot) {
                     if (!(f_cur & (1 << slot))) continue;
                     const uint32_t tP = tbase + slot * 128;
                     const uint32_t tO = tbase + 256 + slot * 128;
+                    long long* tr = (trace && blockIdx.x == trace_bid && u < 256 && leader)
+                                        ? trace + (u * 2 + slot) * 8 : nullptr;
+                    if (tr) tr[0] = clock64();                 // MMA: start waiting for P
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {   // PV over keys [64 half, 64 half + 64)
                         mbar_wait(&bars->p_half[slot][half], jn[slot] & 1);
+                        if (tr) tr[1 + half] = clock64();      // MMA: P half ready
                         tc_fence_after();
+                        if (leader) {
+                            const uint64_t b0 = dv + (st * kTile >> 4);
 #pragma unroll
-                        for (int k4 = 0; k4 < 4; ++k4) {  // K steps of 16 keys
-                            const int kk = half * 4 + k4;
-                            const uint64_t b = sdesc_sw128(v_addr + st * kTile + kk * 2048, kBox, 1024);
-                            umma_ts(tO, tP + kk * 8, b, idesc_pv, (jn[slot] > 0 || kk > 0) ? 1u : 0u);
+                            for (int k4 = 0; k4 < 4; ++k4) {  // K steps of 16 keys
+                                const int kk = half * 4 + k4;
+                                umma_ts(tO, tP + kk * 8, b0 + (kk * 2048 >> 4), idesc_pv,
+                                        (jn[slot] > 0 || kk > 0) ? 1u : 0u);
+                            }
                         }
+                        __syncwarp();
                     }
-                    tc_commit(&bars->o_done[slot]);
+                    if (leader) tc_commit(&bars->o_done[slot]);
+                    __syncwarp();
                     ++jn[slot];
                     if (has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                    if (tr) tr[3] = clock64();                 // MMA: PV + next S issued
                 }
-                tc_commit(&bars->kv_empty[st]);
+                if (leader) tc_commit(&bars->v_empty[st]);
+                __syncwarp();
 #pragma unroll
                 for (int slot = 0; slot < 2; ++slot)
                     if (!(f_cur & (1 << slot)) && has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                if (has_nxt) {
+                    if (leader) tc_commit(&bars->k_empty[(u + 1) % kKStages]);   // K(u+1) consumed
+                    __syncwarp();
+                }
                 n_cur = n_nxt;
                 f_cur = f_nxt;
                 has = has_nxt;
@@ -258,8 +298,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         for (int j = 0; j < my_cnt; ++j) {
             const int n = n_next;
             if (j + 1 < my_cnt) n_next = my_list ? __ldg(my_list + j + 1) : j + 1;  // prefetch
+            long long* tr = (trace && blockIdx.x == trace_bid && lane == 0 && quarter == 2 && j < 256)
+                                ? trace + 256 * 16 + (j * 2 + slot) * 8 : nullptr;
+            if (tr) tr[0] = clock64();                         // SM: start waiting for S
             mbar_wait(&bars->s_full[slot], j & 1);
             tc_fence_after();
+            if (tr) tr[1] = clock64();                         // SM: S ready
             uint32_t raw[4][32];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, raw[c]);
@@ -284,6 +328,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 }
             const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            if (tr) tr[2] = clock64();                         // SM: S loaded + row max
             const float m_new = fmaxf(m_used, rmax * scale_log2);
             const bool need = (m_new > m_used + kRescaleThreshold);
             const bool any = __any_sync(0xffffffffu, need);
@@ -337,6 +382,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&bars->p_half[slot][half]);
+                if (tr) tr[3 + half] = clock64();              // SM: P half released
             }
             {
                 const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
@@ -380,6 +426,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 // Slot pairing: 0 = two heads of one kv head at the same row, 1 = one head at two adjacent
 // rows (default; adjacent rows' lists overlap strongly, independent of per-head budgets).
 // PROXYATTN_PAIR_MODE overrides it (for measurements).
+constexpr size_t kTraceBytes = 2 * 256 * 2 * 8 * sizeof(long long);
+
 int attn_pair_mode() {
     static int mode = -1;
     if (mode < 0) {
@@ -401,6 +449,11 @@ int attn_exp_emu() {
 }
 
 }  // namespace
+
+long long*& attn_trace_ptr() {
+    static long long* p = nullptr;
+    return p;
+}
 
 cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
@@ -424,9 +477,20 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
     const unsigned grid = mode == 0
         ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(D.M)
         : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((D.M + 1) / 2);
+    // PROXYATTN_TRACE=<cta>: per-event clock64 timeline of one CTA (diagnostics only), read
+    // back with proxyattn_debug_trace().
+    static long long* trace = nullptr;
+    static int trace_bid = -1;
+    if (trace_bid < 0) {
+        const char* e = getenv("PROXYATTN_TRACE");
+        trace_bid = e ? atoi(e) : 1 << 30;
+        if (e && cudaMalloc(&trace, kTraceBytes) != cudaSuccess) trace = nullptr;
+    }
+    if (trace) cudaMemsetAsync(trace, 0, kTraceBytes, st);
+    attn_trace_ptr() = trace;
     kern<<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
-        D.M, D.r, D.Hl, mode, scale_log2);
+        D.M, D.r, D.Hl, mode, scale_log2, trace, trace_bid);
     return cudaGetLastError();
 }
 

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-                int r, float scale_log2) {
+                int r, float scale_log2, long long* trace, int trace_bid) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -175,8 +175,11 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const uint32_t tP = tbase + (j & 1) * 128;
                 mbar_wait(&bars->v_full[st], (j / kVStages) & 1);
 #pragma unroll
+                long long* tr = (trace && blockIdx.x == trace_bid && j < 256) ? trace + (j * 2) * 8 : nullptr;
+                if (tr) tr[0] = clock64();
                 for (int c = 0; c < 2; ++c) {   // keys [64c, 64c + 64): P at S cols [64c, 64c+32)
                     mbar_wait(&bars->p_half[c], j & 1);
+                    if (tr) tr[1 + c] = clock64();
                     tc_fence_after();
 #pragma unroll
                     for (int k4 = 0; k4 < 4; ++k4) {
@@ -188,6 +191,7 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 tc_commit(&bars->v_empty[st]);
                 tc_commit(&bars->o_done);
                 if (j + 2 < cnt) issue_s(j + 2);   // overwrites S_{j&1} = P_j: after PV_j (in order)
+                if (tr) tr[3] = clock64();
             }
         }
     } else {
@@ -203,8 +207,12 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         for (int j = 0; j < cnt; ++j) {
             const int n = n_next;
             if (j + 1 < cnt) n_next = list ? __ldg(list + j + 1) : j + 1;
+            long long* tr = (trace && blockIdx.x == trace_bid && lane == 0 && q4 == 2 && j < 256)
+                                ? trace + 256 * 16 + (j * 2 + ch) * 8 : nullptr;
+            if (tr) tr[0] = clock64();
             mbar_wait(&bars->s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
+            if (tr) tr[1] = clock64();
             const uint32_t tS = tbase + lane_off + (j & 1) * 128 + ch * 64;
             uint32_t raw[2][32];
             tmem_ld32(tS, raw[0]);
@@ -227,8 +235,10 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     mx[c * 2 + (e >> 4)] = fmaxf(mx[c * 2 + (e >> 4)], __uint_as_float(raw[c][e]));
             const float pmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
             // exchange the partial max with the other column half of the same rows
+            if (tr) tr[2] = clock64();
             bars->red[j & 1][ch][rr] = pmax;
             named_bar(1 + q4, 64);
+            if (tr) tr[3] = clock64();
             const float rmax = fmaxf(pmax, bars->red[j & 1][ch ^ 1][rr]);
             const float m_new = fmaxf(m_used, rmax * scale_log2);
             const bool need = (m_new > m_used + kRescaleThreshold);
@@ -261,6 +271,7 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
                 pk[c] = pack_bf16(p0, p1);
             }
+            if (tr) tr[4] = clock64();
             tmem_st32(tS, pk);                           // P for this half's 64 keys
             {
                 const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
@@ -287,6 +298,7 @@ attn_tc4_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&bars->p_half[ch]);
+            if (tr) tr[5] = clock64();
         }
         // ----------------------------------------------------------- epilogue --
         if (cnt > 0) {
@@ -352,8 +364,20 @@ cudaError_t launch_attn_tc4(const Dims& D, const void* Q, const void* K, const v
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
     const unsigned grid = static_cast<unsigned>(D.Hl) * static_cast<unsigned>(D.M);
+    static long long* trace = nullptr;
+    static int trace_bid = -1;
+    if (trace_bid < 0) {
+        const char* e = getenv("PROXYATTN_TRACE");
+        trace_bid = e ? atoi(e) : 1 << 30;
+        if (e && cudaMalloc(&trace, 2 * 256 * 2 * 8 * sizeof(long long)) != cudaSuccess) trace = nullptr;
+    }
+    if (trace) {
+        cudaMemsetAsync(trace, 0, 2 * 256 * 2 * 8 * sizeof(long long), st);
+        attn_trace_ptr() = trace;
+    }
     kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt,
-                                             block_idx, static_cast<int>(D.N), D.M, D.r, scale_log2);
+                                             block_idx, static_cast<int>(D.N), D.M, D.r, scale_log2,
+                                             trace, trace_bid);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,424 @@
+// attn_tc5.cu — bf16 block-sparse causal prefill attention on tcgen05 (A7 / A8), variant v5:
+// the two-slot K/V-sharing structure of attn_tc.cu (one head x two adjacent query block rows
+// per CTA, union walk of the two ascending lists, each K/V tile loaded once for both rows)
+// with a COLUMN-SPLIT softmax: each (slot, TMEM lane quarter) is served by two warps that
+// own key columns [0,64) and [64,128) of the tile, exchange their partial row max through
+// shared memory and release their P halves to the PV MMA independently — halving the exp
+// latency on each slot's S -> softmax -> PV chain.
+//
+// Warp roles (640 threads = 5 warpgroups):
+//   WG0: warp 0 TMA producer, warp 1 TMEM allocator + single-thread tcgen05.mma issuer,
+//        warps 2-3 idle; the warpgroup drops to 64 registers (setmaxnreg.dec)
+//   WG1..4: softmax of (slot 0, cols 0-63), (slot 0, 64-127), (slot 1, 0-63), (slot 1,
+//        64-127); 104 registers each (setmaxnreg.inc; 4x128x64 + 16x32x104 = the 61440 launched)
+// TMEM (512 columns): S_0 [0,128) S_1 [128,256) O_0 [256,384) O_1 [384,512); P of column
+// half c lives in S columns [64c, 64c + 32).
+#include <cuda_bf16.h>
+
+#include <climits>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace pa {
+namespace {
+
+constexpr int kTileRows = 128;                   // b = 128 query rows / keys per tile
+constexpr int kBox = kTileRows * 64 * 2;         // 16 KB: [128 rows][64 bf16] SW128 box
+constexpr int kTile = 2 * kBox;                  // 32 KB: a 128 x 128 bf16 tile
+constexpr int kStages = 2;
+constexpr int kThreads = 640;
+constexpr float kRescaleThreshold = 8.0f;        // log2 units: P <= 2^8 before a rescale
+
+struct __align__(8) Bars {
+    uint64_t q_full;
+    uint64_t k_full[kStages];
+    uint64_t v_full[kStages];
+    uint64_t kv_empty[kStages];
+    uint64_t s_full[2];
+    uint64_t p_half[2][2];   // [slot][half]: P columns for keys [64 h, 64 h + 64) are in TMEM
+    uint64_t o_done[2];
+    uint32_t tmem_base;
+    float red[2][2][2][128]; // [j & 1][slot][column half][row]: partial row max exchange
+    float red_l[2][2][128];  // [slot][column half][row]: partial row sums (epilogue)
+};
+
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTile * (2 + 2 * kStages) + sizeof(Bars);
+
+// Ascending union of two ascending block lists (null list = dense 0..m).
+struct UnionWalk {
+    const int* a;
+    const int* b;
+    int na, nb, ia, ib;
+    __device__ __forceinline__ int at(const int* l, int i) const { return l ? __ldg(l + i) : i; }
+    // Returns false at the end; flags bit s = slot s selected the block.
+    __device__ __forceinline__ bool next(int& n, int& flags) {
+        const int va = ia < na ? at(a, ia) : INT_MAX;
+        const int vb = ib < nb ? at(b, ib) : INT_MAX;
+        if (va == INT_MAX && vb == INT_MAX) return false;
+        if (va < vb) {
+            n = va; flags = 1; ++ia;
+        } else if (vb < va) {
+            n = vb; flags = 2; ++ib;
+        } else {
+            n = va; flags = 3; ++ia; ++ib;
+        }
+        return true;
+    }
+};
+
+template <int kEmu>   // of every 4 key-column pairs, kEmu use the FMA-pipe exp2 (ex2_poly2)
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc5_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
+               const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
+               int r, int Hl, int pair_mode, float scale_log2, long long* trace, int trace_bid) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sQ = smem;                           // 2 tiles (slot 0, slot 1)
+    uint8_t* sK = smem + 2 * kTile;               // kStages tiles
+    uint8_t* sV = smem + kTile * (2 + kStages);   // kStages tiles
+    Bars* bars = reinterpret_cast<Bars*>(smem + kTile * (2 + 2 * kStages));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int bid = blockIdx.x;
+    // Work item -> two slots (local head, block row) sharing one kv head.  Items are
+    // ordered kv-head major (so the ~148 resident CTAs stream one kv head's K/V through L2
+    // together), heaviest rows first within a kv head.
+    int hs0, hs1, ms0, ms1, nslots;
+    if (pair_mode == 0) {              // two heads of one kv head, same row
+        const int ppk = (r + 1) >> 1;
+        const int per_kv = ppk * M;
+        const int kvi = bid / per_kv, rem = bid % per_kv;
+        const int i0 = 2 * (rem % ppk);
+        ms0 = ms1 = M - 1 - rem / ppk;
+        hs0 = kvi * r + i0;
+        hs1 = hs0 + 1;
+        nslots = (i0 + 1 < r) ? 2 : 1;
+    } else {                           // one head, two adjacent rows
+        const int nrp = (M + 1) >> 1;
+        const int per_kv = r * nrp;
+        const int kvi = bid / per_kv, rem = bid % per_kv;
+        hs0 = hs1 = kvi * r + rem % r;
+        ms0 = M - 1 - 2 * (rem / r);
+        ms1 = ms0 - 1;
+        nslots = ms1 >= 0 ? 2 : 1;
+    }
+    (void)Hl;
+    const int kvl = hs0 / r;
+    const bool dense = (block_cnt == nullptr);
+    const long long row0 = static_cast<long long>(hs0) * M + ms0;
+    const long long row1 = static_cast<long long>(hs1) * M + ms1;
+    const int cnt0 = dense ? ms0 + 1 : block_cnt[row0];
+    const int cnt1 = nslots < 2 ? 0 : (dense ? ms1 + 1 : block_cnt[row1]);
+    const int* list0 = dense ? nullptr : block_idx + row0 * M;
+    const int* list1 = (dense || nslots < 2) ? nullptr : block_idx + row1 * M;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars->k_full[s], 1);
+            mbar_init(&bars->v_full[s], 1);
+            mbar_init(&bars->kv_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->p_half[s][0], 128);
+            mbar_init(&bars->p_half[s][1], 128);
+            mbar_init(&bars->o_done[s], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = bars->tmem_base;
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer --
+        if (lane == 0) {
+            tma_prefetch(&tmQ);
+            tma_prefetch(&tmK);
+            tma_prefetch(&tmV);
+            mbar_expect_tx(&bars->q_full, kTile * nslots);
+            for (int s = 0; s < nslots; ++s) {
+                const int qrow = (s ? hs1 : hs0) * N + (s ? ms1 : ms0) * kTileRows;
+                tma_load_2d(sQ + s * kTile, &tmQ, &bars->q_full, 0, qrow);
+                tma_load_2d(sQ + s * kTile + kBox, &tmQ, &bars->q_full, 64, qrow);
+            }
+            UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
+            int n, f;
+            for (int u = 0; it.next(n, f); ++u) {
+                const int st = u % kStages;
+                if (u >= kStages) mbar_wait(&bars->kv_empty[st], ((u / kStages) - 1) & 1);
+                const int krow = kvl * N + n * kTileRows;
+                uint8_t* k_dst = sK + st * kTile;
+                uint8_t* v_dst = sV + st * kTile;
+                mbar_expect_tx(&bars->k_full[st], kTile);
+                tma_load_2d(k_dst, &tmK, &bars->k_full[st], 0, krow);
+                tma_load_2d(k_dst + kBox, &tmK, &bars->k_full[st], 64, krow);
+                mbar_expect_tx(&bars->v_full[st], kTile);
+                tma_load_2d(v_dst, &tmV, &bars->v_full[st], 0, krow);
+                tma_load_2d(v_dst + kBox, &tmV, &bars->v_full[st], 64, krow);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA issuer --
+        if (lane == 0) {
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+            const uint32_t q_addr = smem_u32(sQ);
+            const uint32_t k_addr = smem_u32(sK);
+            const uint32_t v_addr = smem_u32(sV);
+            mbar_wait(&bars->q_full, 0);
+            auto issue_s = [&](int slot, int u) {  // S_slot = Q_slot K(u)^T
+                const int st = u % kStages;
+                mbar_wait(&bars->k_full[st], (u / kStages) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                    umma_ss(tbase + slot * 128, sdesc_sw128(q_addr + slot * kTile + off, 16, 1024),
+                            sdesc_sw128(k_addr + st * kTile + off, 16, 1024), idesc_qk,
+                            kk > 0 ? 1u : 0u);
+                }
+                tc_commit(&bars->s_full[slot]);
+            };
+            UnionWalk it{list0, list1, cnt0, cnt1, 0, 0};
+            int n_cur, f_cur, n_nxt = 0, f_nxt = 0;
+            bool has = it.next(n_cur, f_cur);
+            int jn[2] = {0, 0};                     // PVs issued per slot (p_full parity)
+            if (has) {
+                if (f_cur & 1) issue_s(0, 0);
+                if (f_cur & 2) issue_s(1, 0);
+            }
+            for (int u = 0; has; ++u) {
+                const bool has_nxt = it.next(n_nxt, f_nxt);
+                const int st = u % kStages;
+                mbar_wait(&bars->v_full[st], (u / kStages) & 1);
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot) {
+                    if (!(f_cur & (1 << slot))) continue;
+                    const uint32_t tP = tbase + slot * 128;
+                    const uint32_t tO = tbase + 256 + slot * 128;
+                    long long* tr = (trace && blockIdx.x == trace_bid && u < 256) ? trace + (u * 2 + slot) * 8 : nullptr;
+                    if (tr) tr[0] = clock64();
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {   // PV over keys [64 half, 64 half + 64)
+                        mbar_wait(&bars->p_half[slot][half], jn[slot] & 1);
+                        if (tr) tr[1 + half] = clock64();
+                        tc_fence_after();
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {  // K steps of 16 keys
+                            const int kk = half * 4 + k4;
+                            const uint64_t b = sdesc_sw128(v_addr + st * kTile + kk * 2048, kBox, 1024);
+                            umma_ts(tO, tP + half * 64 + k4 * 8, b, idesc_pv, (jn[slot] > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc_commit(&bars->o_done[slot]);
+                    ++jn[slot];
+                    if (has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                    if (tr) tr[3] = clock64();
+                }
+                tc_commit(&bars->kv_empty[st]);
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot)
+                    if (!(f_cur & (1 << slot)) && has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
+                n_cur = n_nxt;
+                f_cur = f_nxt;
+                has = has_nxt;
+            }
+            (void)n_cur;
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------- softmax --
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        const int grp = (warp - 4) >> 2;               // 0..3
+        const int slot = grp >> 1;
+        const int ch = grp & 1;                         // column half
+        const int quarter = warp & 3;                   // TMEM lane quarter of this warp
+        const int rr = quarter * 32 + lane;             // query row within the block
+        const int bar_id = 1 + slot * 4 + quarter;      // the two column halves of these rows
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t tS = tbase + lane_off + slot * 128 + ch * 64;
+        const uint32_t tO = tbase + lane_off + 256 + slot * 128 + ch * 64;
+        const int my_cnt = slot ? cnt1 : cnt0;
+        const int* my_list = slot ? list1 : list0;
+        const int m = slot ? ms1 : ms0;
+        const int my_h = slot ? hs1 : hs0;
+        float m_used = -INFINITY;                       // running max (log2 units)
+        float l = 0.f;                                  // partial denominator (own columns)
+        int n_next = (my_cnt > 0) ? (my_list ? __ldg(my_list) : 0) : 0;
+        for (int j = 0; j < my_cnt; ++j) {
+            const int n = n_next;
+            if (j + 1 < my_cnt) n_next = my_list ? __ldg(my_list + j + 1) : j + 1;  // prefetch
+            long long* tr = (trace && blockIdx.x == trace_bid && lane == 0 && quarter == 2 && ch == 0 && j < 256)
+                                ? trace + 256 * 16 + (j * 2 + slot) * 8 : nullptr;
+            if (tr) tr[0] = clock64();
+            mbar_wait(&bars->s_full[slot], j & 1);
+            tc_fence_after();
+            if (tr) tr[1] = clock64();
+            uint32_t raw[2][32];
+            tmem_ld32(tS, raw[0]);
+            tmem_ld32(tS + 32, raw[1]);
+            tmem_ld_wait();
+            if (n == m) {  // diagonal block: key index > row index is masked (causal)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (ch * 64 + c * 32 + e > rr) raw[c][e] = 0xff800000u;  // -inf
+            }
+            float mx[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mx[k] = __uint_as_float(raw[k >> 1][(k & 1) * 16]);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    mx[c * 2 + (e >> 4)] = fmaxf(mx[c * 2 + (e >> 4)], __uint_as_float(raw[c][e]));
+            const float pmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+            bars->red[j & 1][slot][ch][rr] = pmax;       // exchange with the other column half
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            const float rmax = fmaxf(pmax, bars->red[j & 1][slot][ch ^ 1][rr]);
+            if (tr) tr[2] = clock64();
+            const float m_new = fmaxf(m_used, rmax * scale_log2);
+            const bool need = (m_new > m_used + kRescaleThreshold);
+            const bool any = __any_sync(0xffffffffu, need);   // same rows in both halves
+            float factor = 1.f;
+            if (any) {
+                factor = ex2(m_used - m_new);  // 0 on the first block (m_used = -inf)
+                m_used = m_new;
+                l *= factor;
+            }
+            const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+            const uint64_t nm2 = f2_pack(-m_used, -m_used);
+            uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int e0 = 2 * c;
+                const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
+                                                   __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
+                                           sc2, nm2);
+                float p0, p1;
+                if ((c & 3) < kEmu) {
+                    ex2_poly2(x2, p0, p1);
+                } else {
+                    float x0, x1;
+                    f2_unpack(x2, x0, x1);
+                    p0 = ex2(x0);
+                    p1 = ex2(x1);
+                }
+                ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
+                pk[c] = pack_bf16(p0, p1);
+            }
+            tmem_st32(tS, pk);                           // P of this half's 64 keys
+            {
+                const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
+                float a, b;
+                f2_unpack(t, a, b);
+                l += a + b;
+            }
+            if (j > 0) {
+                mbar_wait(&bars->o_done[slot], (j - 1) & 1);  // PV_{j-1} finished writing O
+                tc_fence_after();
+                if (any) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&bars->p_half[slot][ch]);
+            if (tr) { tr[3] = clock64(); tr[4] = tr[3]; }
+        }
+        // ----------------------------------------------------------- epilogue --
+        if (my_cnt > 0) {
+            bars->red_l[slot][ch][rr] = l;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            const float inv = 1.f / (l + bars->red_l[slot][ch ^ 1][rr]);
+            mbar_wait(&bars->o_done[slot], (my_cnt - 1) & 1);
+            tc_fence_after();
+            uint4* dst = reinterpret_cast<uint4*>(
+                O + (static_cast<long long>(my_h) * N + static_cast<long long>(m) * kTileRows + rr) * 128 +
+                ch * 64);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
+                tmem_ld_wait();
+                uint32_t pkd[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    dst[c * 4 + v] = make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tbase, 512);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_attn_tc5(const Dims& D, const void* Q, const void* K, const void* V,
+                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
+    CUtensorMap mq, mk, mv;
+    if (!make_map_bf16_sw128(&mq, Q, static_cast<uint64_t>(D.Hl) * D.N, 128, 128) ||
+        !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
+        !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
+        return cudaErrorInvalidValue;
+    const char* ev = getenv("PROXYATTN_EXP_EMU");
+    const int emu = (ev && ev[0] >= '0' && ev[0] <= '3') ? ev[0] - '0' : 0;
+    auto kern = emu == 0 ? attn_tc5_kernel<0> : emu == 1 ? attn_tc5_kernel<1>
+              : emu == 2 ? attn_tc5_kernel<2> : attn_tc5_kernel<3>;
+    static bool attr_set[4] = {false, false, false, false};
+    if (!attr_set[emu]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kSmemBytes));
+        if (e != cudaSuccess) return e;
+        attr_set[emu] = true;
+    }
+    const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
+    const unsigned grid = static_cast<unsigned>(D.Hl) * static_cast<unsigned>((D.M + 1) / 2);
+    static long long* trace = nullptr;
+    static int trace_bid = -1;
+    if (trace_bid < 0) {
+        const char* e = getenv("PROXYATTN_TRACE");
+        trace_bid = e ? atoi(e) : 1 << 30;
+        if (e && cudaMalloc(&trace, 2 * 256 * 2 * 8 * sizeof(long long)) != cudaSuccess) trace = nullptr;
+    }
+    if (trace) {
+        cudaMemsetAsync(trace, 0, 2 * 256 * 2 * 8 * sizeof(long long), st);
+        attn_trace_ptr() = trace;
+    }
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt,
+                                             block_idx, static_cast<int>(D.N), D.M, D.r, D.Hl, 1,
+                                             scale_log2, trace, trace_bid);
+    return cudaGetLastError();
+}
+
+}  // namespace pa
