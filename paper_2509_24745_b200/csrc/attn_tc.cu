@@ -362,9 +362,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
                     pk[c] = pack_bf16(p0, p1);
                 }
+                if (tr) tr[5 + half] = clock64();              // SM: exps of this half done
                 tmem_st32(tS + half * 32, pk);
                 if (half == 0 && j > 0) {
                     mbar_wait(&bars->o_done[slot], (j - 1) & 1);  // PV_{j-1} finished writing O
+                    if (tr) tr[7] = clock64();                 // SM: O ready for correction
                     tc_fence_after();
                     if (any) {
 #pragma unroll

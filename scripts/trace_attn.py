@@ -47,6 +47,7 @@ valid = ss[:, :, 0] > 0
 for s in range(2):
     v = ss[:, s][valid[:, s]]
     print(f"slot {s}: S-wait {d(v[:,1], v[:,0]):.0f}  load+max {d(v[:,2], v[:,1]):.0f}  half0 {d(v[:,3], v[:,2]):.0f}  half1 {d(v[:,4], v[:,3]):.0f}  iter {np.median(np.diff(v[:,1])):.0f}")
+    print(f"        exps0 {d(v[:,5], v[:,2]):.0f}  st0+odone {d(v[:,7], v[:,5]):.0f}  fence+arrive0 {d(v[:,3], v[:,7]):.0f}  exps1 {d(v[:,6], v[:,3]):.0f}  st1+arrive1 {d(v[:,4], v[:,6]):.0f}")
 mm = mma[40:200]
 for s in range(2):
     v = mm[:, s][mm[:, s, 0] > 0]
