@@ -226,6 +226,11 @@ def run_ours(args):
     if args.seq_len:
         w["seq_len"] = args.seq_len
         w["name"] = w["name"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
+        import workloads
+
+        cand = w["preset"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
+        if cand in workloads.PRESETS:      # per-length calibration to Table 8
+            w["preset"] = cand
     cfg = build_config(pa, rank, ws, w)
     Q, K, V, meta = gen_inputs(w, dev)
     hb, he = cfg.local_heads

@@ -50,10 +50,17 @@ typedef struct {
     uint32_t flags;              /* PROXYATTN_FLAG_* */
     int32_t  q_head_begin;       /* local shard [begin, end) of query heads; end == 0 means all */
     int32_t  q_head_end;
+    int32_t  static_kstar;       /* > 0: static top-K baseline (Fig. 6c): every head uses
+                                    K* = static_kstar instead of Alg. 1's dynamic budget; 0 = Alg. 1 */
 } proxyattn_cfg;
 
 #define PROXYATTN_FLAG_FP32_DEBUG  0x1u  /* fp32 Q/K/V/O, SIMT FFMA kernels (1e-4 contract)   */
 #define PROXYATTN_FLAG_CHECK       0x2u  /* prefill validates block lists on the device (E_SHAPE) */
+/* Method variants (readings Z1, Z12, Z16), off by default: */
+#define PROXYATTN_FLAG_FORCE_SINK  0x4u  /* block 0 always selected, counted toward K (Z16 alternative) */
+#define PROXYATTN_FLAG_CONSTANT_K  0x8u  /* Eq. 3 K = ceil(b_i M) on every row, capped at m+1 (Z12 alt.) */
+#define PROXYATTN_FLAG_DESIGNATED_HEAD 0x10u /* proxy = the group's first query / kv head instead of
+                                                the Eq. 2 mean ("a designated head"; Z1 alt.) */
 
 #define PROXYATTN_OK               0
 #define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */

@@ -48,6 +48,10 @@ class _CCfg(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("min_budget_tokens", ctypes.c_int32),
         ("round_bf16", ctypes.c_int32),
+        ("force_sink", ctypes.c_int32),
+        ("constant_k", ctypes.c_int32),
+        ("designated_head", ctypes.c_int32),
+        ("static_kstar", ctypes.c_int32),
     ]
 
 
@@ -65,6 +69,10 @@ class Cfg:
     gamma: float
     min_budget_tokens: int = 0
     round_bf16: bool = False
+    force_sink: bool = False        # method variants
+    constant_k: bool = False
+    designated_head: bool = False
+    static_kstar: int = 0
 
     @property
     def M(self) -> int:
@@ -77,7 +85,9 @@ class Cfg:
     def c(self) -> _CCfg:
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
-                     self.min_budget_tokens, int(bool(self.round_bf16)))
+                     self.min_budget_tokens, int(bool(self.round_bf16)), int(bool(self.force_sink)),
+                     int(bool(self.constant_k)), int(bool(self.designated_head)),
+                     int(self.static_kstar))
 
     def replace(self, **kw) -> "Cfg":
         d = dict(self.__dict__)

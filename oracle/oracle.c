@@ -81,18 +81,21 @@ void oracle_pool(const oracle_cfg* c, const float* Q, const float* K,
             if (oracle_group_of_q(c, h) != grp) continue;
             const float* q = Q + ((long)h * N + p) * d;
             for (int e = 0; e < d; ++e) pq[e] += (double)q[e];
+            if (c->designated_head) break;     /* the group's first query head only */
         }
         for (int kvh = 0; kvh < c->n_kv_heads; ++kvh) {
             if (group_of_kv(c, kvh) != grp) continue;
             const float* k = K + ((long)kvh * N + p) * d;
             for (int e = 0; e < d; ++e) pk[e] += (double)k[e];
+            if (c->designated_head) break;     /* ... and its first kv head */
         }
         if (c->round_bf16) {
             for (int e = 0; e < d; ++e) { pq[e] = oracle_rne_bf16(pq[e]); pk[e] = oracle_rne_bf16(pk[e]); }
         }
     }
     /* Eq. 2 means and Eq. 1's 1/sqrt(d_k): z = (qsum/|Gq|)·(ksum/|Gk|)/sqrt(d). */
-    if (scale_out) *scale_out = 1.0 / ((double)gq * (double)gk * sqrt((double)d));
+    if (scale_out) *scale_out = c->designated_head ? 1.0 / sqrt((double)d)
+                                                   : 1.0 / ((double)gq * (double)gk * sqrt((double)d));
 }
 
 /* ----------------------------------------------------------------- O4-O6 -- */
@@ -198,6 +201,13 @@ void oracle_budgets(const oracle_cfg* c, const float* Q, const float* K,
         for (int hi = 0; hi < nh; ++hi) {
             int h = heads ? heads[hi] : hi;
             int kvh = h / r;
+            if (c->static_kstar > 0) {          /* static top-K baseline: Alg. 1 not run */
+                int ks = c->static_kstar < M ? c->static_kstar : M;
+                kstar[h] = ks;
+                if (budget) budget[h] = (double)ks / M;
+                if (margin) margin[h] = INFINITY;
+                continue;
+            }
             for (int n = 0; n < M; ++n) a[n] = 0.0;
             /* Alg. 1 line 1: A^ = softmax(Q_last K^T / sqrt(d_k)), own head, full resolution,
              * causal inside the last block (Z7). */
@@ -234,7 +244,8 @@ int oracle_row_count(const oracle_cfg* c, int kstar, int m) {
     const long M = n_blocks(c);
     const long b = c->block_size;
     long F = (c->min_budget_tokens + b - 1) / b;                 /* ceil(tokens / b) */
-    long K = ((long)kstar * (m + 1) + M - 1) / M;                /* ceil(b_i (m+1)), Z12 */
+    long K = c->constant_k ? (long)kstar                          /* K = b_i M on every row */
+                           : ((long)kstar * (m + 1) + M - 1) / M;   /* ceil(b_i (m+1)), Z12 */
     if (K < F) K = F;
     if (K < 1) K = 1;
     if (K > m + 1) K = m + 1;                                    /* capped at the causal row */
@@ -261,6 +272,7 @@ void oracle_select(const oracle_cfg* c, const double* L, const int32_t* kstar,
             /* Eq. 3 TopK over the shared score row; the diagonal is forced first (Z15),
              * the other columns 0..m-1 ordered by (score desc, index asc) (Z17). */
             for (int n = 0; n < m; ++n) { s[n].v = Lrow[n]; s[n].n = n; }
+            if (c->force_sink && m > 0) s[0].v = INFINITY;   /* sink block first (forced, counted) */
             qsort(s, (size_t)m, sizeof(vi_pair), cmp_desc_then_index);
             for (int h = 0; h < c->n_q_heads; ++h) {
                 if (oracle_group_of_q(c, h) != grp) continue;

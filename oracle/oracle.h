@@ -34,6 +34,11 @@ typedef struct {
     double  gamma;              /* γ of Alg. 1 */
     int32_t min_budget_tokens;  /* P:466 / P:764 (reading Z13/Z14) */
     int32_t round_bf16;         /* 1: pooled proxies are rounded to bf16 (RNE), precision contract c.3 */
+    /* method variants (DESIGN.md readings; all 0 = the paper's method as read in Z1-Z23) */
+    int32_t force_sink;         /* block 0 always selected and counted (Z16 alternative) */
+    int32_t constant_k;         /* Eq. 3 K = K* on every row, capped at m+1 (Z12 alternative) */
+    int32_t designated_head;    /* proxy = the group's first q / kv head (Z1 alternative) */
+    int32_t static_kstar;       /* > 0: every head uses K* = static_kstar (Fig. 6c static top-K) */
 } oracle_cfg;
 
 /* O1: returns 0 when the config satisfies the DS-1 invariants, -1 otherwise. */

@@ -17,6 +17,9 @@ SO_PATH = os.path.join(_PKG, "libproxyattn.so")
 
 FLAG_FP32_DEBUG = 0x1
 FLAG_CHECK = 0x2
+FLAG_FORCE_SINK = 0x4
+FLAG_CONSTANT_K = 0x8
+FLAG_DESIGNATED_HEAD = 0x10
 
 OK = 0
 E_CONFIG = -1
@@ -46,6 +49,7 @@ class _CCfg(ctypes.Structure):
         ("flags", ctypes.c_uint32),
         ("q_head_begin", ctypes.c_int32),
         ("q_head_end", ctypes.c_int32),
+        ("static_kstar", ctypes.c_int32),
     ]
 
 
@@ -66,6 +70,10 @@ class Config:
     check: bool = False
     q_head_begin: int = 0
     q_head_end: int = 0
+    force_sink: bool = False        # method variants
+    constant_k: bool = False
+    designated_head: bool = False
+    static_kstar: int = 0
 
     @property
     def M(self) -> int:
@@ -92,10 +100,14 @@ class Config:
         return replace(self, **kw)
 
     def c(self) -> _CCfg:
-        flags = (FLAG_FP32_DEBUG if self.fp32_debug else 0) | (FLAG_CHECK if self.check else 0)
+        flags = ((FLAG_FP32_DEBUG if self.fp32_debug else 0) | (FLAG_CHECK if self.check else 0)
+                 | (FLAG_FORCE_SINK if self.force_sink else 0)
+                 | (FLAG_CONSTANT_K if self.constant_k else 0)
+                 | (FLAG_DESIGNATED_HEAD if self.designated_head else 0))
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
-                     self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end)
+                     self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,
+                     self.static_kstar)
 
 
 _lib = None

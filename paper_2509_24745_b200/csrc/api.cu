@@ -74,6 +74,8 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     D.bs = D.b / D.s;
     D.gamma = c->gamma;
     D.flags = c->flags;
+    if (c->static_kstar < 0) return fail(PROXYATTN_E_CONFIG, "static_kstar < 0");
+    D.static_kstar = c->static_kstar;
     D.F = (c->min_budget_tokens + D.b - 1) / D.b;
     D.gq = D.Hq / D.g;
     D.gk = D.Hkv / D.g;
@@ -134,6 +136,10 @@ int run_budgets(const pa::Dims& D, const void* Q, const void* K, void* ws, const
                 int32_t* kstar, float* budget, cudaStream_t st) {
     float* blse = at<float>(ws, W.blse);
     float* bmass = at<float>(ws, W.bmass);
+    if (D.static_kstar > 0) {   // static top-K baseline (Fig. 6c): Alg. 1 is not run
+        PA_CUDA(pa::launch_static_budget(D, kstar, budget, st), "static_budget");
+        return PROXYATTN_OK;
+    }
     if (pa::score_tc_supported(D)) {
         PA_CUDA(pa::launch_budget_tc(D, Q, K, at<float>(ws, W.scratch), bmass, st), "budget_tc");
     } else {

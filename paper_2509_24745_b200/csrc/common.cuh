@@ -26,7 +26,10 @@ struct Dims {
     float gamma;
     uint32_t flags;
     bool fp32;    // FP32_DEBUG
+    int static_kstar;   // > 0: static top-K baseline (Alg. 1 skipped)
 };
+
+__host__ __device__ __forceinline__ bool has_flag(const Dims& D, uint32_t f) { return (D.flags & f) != 0; }
 
 // Query-head h (global) -> proxy group (groups aligned with the keys, Z3).
 __host__ __device__ __forceinline__ int group_of_q(const Dims& D, int h) {
@@ -35,7 +38,9 @@ __host__ __device__ __forceinline__ int group_of_q(const Dims& D, int h) {
 
 // Eq. 3 row count under reading Z12: K_{h,m} = min(m+1, max(ceil(K* (m+1)/M), F, 1)).
 __host__ __device__ __forceinline__ int row_count(const Dims& D, int kstar, int m) {
-    long long k = ((long long)kstar * (m + 1) + D.M - 1) / D.M;
+    long long k = (D.flags & PROXYATTN_FLAG_CONSTANT_K)
+                      ? (long long)kstar                                  // Z12 alternative
+                      : ((long long)kstar * (m + 1) + D.M - 1) / D.M;
     if (k < D.F) k = D.F;
     if (k < 1) k = 1;
     if (k > m + 1) k = m + 1;

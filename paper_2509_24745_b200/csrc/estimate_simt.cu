@@ -39,9 +39,11 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
     const long long p = i * D.s;  // first token of each stride window
     const int grp = D.gb + c;
     const int dv = D.d >> 5;
-    // query heads of the group inside the shard, and their kv heads (global ids)
-    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
-    const int k0 = max(grp * D.gk, D.kvb), k1 = min((grp + 1) * D.gk, D.kvb + D.Hkvl);
+    // group's query heads / kv heads inside the shard (designated head: only the first)
+    const int gqe = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gq;
+    const int gke = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gk;
+    const int h0 = max(grp * D.gq, D.qb), h1 = min(grp * D.gq + gqe, D.qe);
+    const int k0 = max(grp * D.gk, D.kvb), k1 = min(grp * D.gk + gke, D.kvb + D.Hkvl);
     // fp64 accumulation: the sum of <= 64 bf16 (or fp32) values is then exact, so the proxy
     // rounding below is one RNE of the exact sum, as in the oracle (precision contract c.3).
     double aq[4] = {0., 0., 0., 0.}, ak[4] = {0., 0., 0., 0.};
@@ -81,8 +83,11 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
     const long long i = row % D.Ns;
     const long long p = i * D.s;
     const int grp = D.gb + c;
-    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
-    const int k0 = max(grp * D.gk, D.kvb), k1 = min((grp + 1) * D.gk, D.kvb + D.Hkvl);
+    // group's query heads / kv heads inside the shard (designated head: only the first)
+    const int gqe = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gq;
+    const int gke = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gk;
+    const int h0 = max(grp * D.gq, D.qb), h1 = min(grp * D.gq + gqe, D.qe);
+    const int k0 = max(grp * D.gk, D.kvb), k1 = min(grp * D.gk + gke, D.kvb + D.Hkvl);
     auto accumulate = [&](const __nv_bfloat16* base, int a, int b, int head0, double (&acc)[8]) {
         for (int h = a; h < b; h += 4) {
             uint4 v[4];
@@ -384,8 +389,9 @@ __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __
     int* id = reinterpret_cast<int*>(key + next_pow2(D.M));
     int* rank = id + next_pow2(D.M);
     const float* row = L + (static_cast<long long>(c) * D.M + m) * D.M;
+    const bool sink = has_flag(D, PROXYATTN_FLAG_FORCE_SINK);
     for (int n = threadIdx.x; n < P; n += blockDim.x) {
-        key[n] = (n < m) ? row[n] : -INFINITY;
+        key[n] = (n < m) ? ((sink && n == 0) ? INFINITY : row[n]) : -INFINITY;  // forced sink first
         id[n] = (n < m) ? n : INT_MAX;
     }
     __syncthreads();
@@ -470,9 +476,25 @@ cudaError_t launch_round_proxies(const Dims& D, const float* qsum, const float* 
 }
 
 static float proxy_scale(const Dims& D) {
-    // Eq. 2 means folded into the logit scale: 1/(|Gq| |Gk| sqrt(d)) (Z2, Z5)
+    // Eq. 2 means folded into the logit scale: 1/(|Gq| |Gk| sqrt(d)) (Z2, Z5); a designated
+    // head is used as is: 1/sqrt(d)
+    if (has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD)) return rsqrtf(static_cast<float>(D.d));
     return 1.0f / (static_cast<float>(D.gq) * static_cast<float>(D.gk) *
                    sqrtf(static_cast<float>(D.d)));
+}
+
+__global__ void static_budget_kernel(int Hl, int M, int ks, int* kstar, float* budget) {
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h < Hl) {
+        const int k = ks < M ? ks : M;
+        kstar[h] = k;
+        budget[h] = static_cast<float>(k) / M;
+    }
+}
+
+cudaError_t launch_static_budget(const Dims& D, int* kstar, float* budget, cudaStream_t st) {
+    static_budget_kernel<<<(D.Hl + 127) / 128, 128, 0, st>>>(D.Hl, D.M, D.static_kstar, kstar, budget);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_proxy_lse(const Dims& D, const void* Pq, const void* Pk, float* lse,

@@ -23,6 +23,8 @@ cudaError_t launch_budget_lse(const Dims& D, const void* Q, const void* K, float
                               cudaStream_t st);
 cudaError_t launch_budget_mass(const Dims& D, const void* Q, const void* K, const float* blse,
                                float* bmass, cudaStream_t st);
+// Static top-K baseline: kstar[h] = min(static_kstar, M) for every local head.
+cudaError_t launch_static_budget(const Dims& D, int* kstar, float* budget, cudaStream_t st);
 cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar, float* budget,
                                    cudaStream_t st);
 // A5-A6: per (group, row) ordering, per head compaction.

@@ -394,7 +394,9 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.n_tr = static_cast<int>(D.Ns / 128);
     p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
     // Eq. 2 means + 1/sqrt(d) folded into the scale (Z2, Z5), in log2 units.
-    p.sc2 = kLog2e / (static_cast<float>(D.gq) * static_cast<float>(D.gk) * sqrtf(static_cast<float>(D.d)));
+    p.sc2 = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD)
+                ? kLog2e / sqrtf(static_cast<float>(D.d))
+                : kLog2e / (static_cast<float>(D.gq) * static_cast<float>(D.gk) * sqrtf(static_cast<float>(D.d)));
     float* part_m = scratch;
     float* part_s = part_m + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;
     float* lse2 = part_s + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;

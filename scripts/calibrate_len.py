@@ -1,0 +1,36 @@
+"""Bisection of the structured generator's beta scale per sequence length so that the GPU
+estimate's sparsity matches Table 8 (Llama gamma = 0.9): 16K 73.31 %, 32K 78.27 %,
+64K 83.19 %, 128K 83.86 %.  beta_hi = 3 beta_lo, sigma = 0.93, rho = 0.999."""
+import json
+import sys
+
+import torch
+
+import paper_2509_24745_b200 as pa
+import workloads
+
+TARGET = {16384: 0.7331, 32768: 0.7827, 65536: 0.8319, 131072: 0.8386}
+dev = torch.device("cuda:0")
+for N, tgt in TARGET.items():
+    cfg = pa.Config(32, 8, 128, N, 128, 4, 1, 0.9, 0)
+
+    def sp(lo):
+        prm = workloads.StructParams(sigma=0.93, beta_lo=lo, beta_hi=3 * lo)
+        Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=prm, device=dev)
+        _, _, cnt, _ = pa.estimate(cfg, Q, K)
+        M = cfg.M
+        return float(1 - cnt.double().sum() / (32 * M * (M + 1) / 2))
+
+    a, b = 0.2, 0.8
+    sa, sb = sp(a), sp(b)
+    best = None
+    for it in range(14):
+        mid = 0.5 * (a + b)
+        sm = sp(mid)
+        if best is None or abs(sm - tgt) < abs(best[1] - tgt):
+            best = (mid, sm)
+        if (sm - tgt) * (sa - tgt) > 0:
+            a, sa = mid, sm
+        else:
+            b, sb = mid, sm
+    print(json.dumps({"N": N, "target": tgt, "beta_lo": round(best[0], 4), "sparsity": round(best[1], 4)}), flush=True)

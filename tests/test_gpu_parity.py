@@ -27,7 +27,9 @@ BF16_MAX, BF16_MEAN, FP32_TOL = 2e-2, 2e-3, 1e-4
 def ocfg_of(cfg: pa.Config) -> oracle.Cfg:
     return oracle.Cfg(cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.seq_len, cfg.block_size,
                       cfg.stride, cfg.n_groups, cfg.gamma, cfg.min_budget_tokens,
-                      round_bf16=not cfg.fp32_debug)
+                      round_bf16=not cfg.fp32_debug, force_sink=cfg.force_sink,
+                      constant_k=cfg.constant_k, designated_head=cfg.designated_head,
+                      static_kstar=cfg.static_kstar)
 
 
 def to_dev(*ts):
@@ -282,3 +284,48 @@ def test_forward_host_matches_device_path():
     O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
     torch.cuda.synchronize()
     assert torch.equal(ks, kstar.cpu()) and torch.equal(Oh, O.cpu())
+
+
+# ------------------------------------------------------------ method variants --
+@pytest.mark.parametrize("variant", [dict(designated_head=True), dict(static_kstar=7),
+                                     dict(constant_k=True), dict(force_sink=True),
+                                     dict(force_sink=True, constant_k=True, n_groups=2)],
+                         ids=["designated", "static7", "constantK", "sink", "sink+constK+g2"])
+def test_method_variants_match_oracle(variant):
+    variant = dict(variant)
+    g = variant.pop("n_groups", 1)
+    cfg = llama_small(N=2048, gamma=0.9, g=g).replace(**variant)
+    oc = ocfg_of(cfg)
+    Q, K, V, _ = workloads.structured(8, 2, 2048, 128, seed=11)
+    Qf, Kf, Vf = np32(Q), np32(K), np32(V)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    est = oracle.estimate(oc, Qf, Kf)
+    ks = kstar.cpu().numpy()
+    ok = est["budget_margin"] > MARGIN
+    assert np.array_equal(ks[ok], est["kstar"][ok])
+    if cfg.static_kstar:
+        assert np.all(ks == cfg.static_kstar)
+    checked, skipped = check_masks(oc, est["L"], ks, cnt, idx)
+    assert checked > 0.9 * (checked + skipped)
+    if cfg.force_sink:
+        c_np, i_np = cnt.cpu().numpy(), idx.cpu().numpy()
+        for h in range(8):
+            for m in range(1, cfg.M):
+                if c_np[h, m] >= 2:
+                    assert i_np[h, m, 0] == 0
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    check_out(O, oracle.attention(oc, Qf, Kf, Vf, cnt.cpu().numpy(), idx.cpu().numpy()), fp32=False)
+
+
+def test_variant_fp32_debug_designated_config_a():
+    cfg = CFG_A.replace(designated_head=True, force_sink=True)
+    oc = ocfg_of(cfg)
+    Q, K, V = workloads.iid(8, 2, 1024, 64, 3)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    est = oracle.estimate(oc, Q.numpy(), K.numpy())
+    ks = kstar.cpu().numpy()
+    ok = est["budget_margin"] > MARGIN
+    assert np.array_equal(ks[ok], est["kstar"][ok])
+    check_masks(oc, est["L"], ks, cnt, idx)

@@ -510,3 +510,64 @@ def test_determinism():
     b = oracle.pipeline(cfg, Q, K, V)
     for k in ("L", "kstar", "block_cnt", "block_idx", "O"):
         assert np.array_equal(a[k], b[k], equal_nan=True)
+
+
+# ------------------------------------------------------------- method variants --
+def test_designated_head_equals_mean_for_singleton_groups_and_first_head_brute_force():
+    # Z1 alternative ("a designated head"): with singleton groups it IS the mean
+    cfg = oracle.Cfg(4, 4, 8, 256, 32, 4, 4, 0.9, round_bf16=True)
+    Q, K, _ = rand_qkv(cfg, 31)
+    a = oracle.estimate(cfg, Q, K)
+    b = oracle.estimate(cfg.replace(designated_head=True), Q, K)
+    assert np.array_equal(a["L"], b["L"]) and np.array_equal(a["block_idx"], b["block_idx"])
+    # multi-head group, stride 1: exp(L) = block-max of the FIRST head's dense probabilities
+    cfg2 = oracle.Cfg(4, 2, 8, 64, 16, 1, 1, 0.9, designated_head=True)
+    Q2, K2, _ = rand_qkv(cfg2, 32, scale=2.0)
+    Pq, Pk, scale = oracle.pool(cfg2, Q2, K2)
+    assert scale == pytest.approx(1 / math.sqrt(8))
+    _, L = oracle.proxy_scores(cfg2, Pq, Pk, scale)
+    P = bf_probs(Q2[0], K2[0])
+    b_ = cfg2.block_size
+    for m in range(cfg2.M):
+        for n in range(m + 1):
+            ref = P[m * b_:(m + 1) * b_, n * b_:(n + 1) * b_].max()
+            assert math.exp(L[0, m, n]) == pytest.approx(ref, rel=1e-12, abs=1e-300)
+
+
+def test_static_topk_budgets_and_brute_force_masks():
+    # Fig. 6c static top-K baseline: every head gets the same K*
+    cfg = oracle.Cfg(4, 2, 16, 64 * 16, 64, 4, 1, 0.9, static_kstar=5)
+    Q, K, _ = rand_qkv(cfg, 33)
+    est = oracle.estimate(cfg, Q, K)
+    assert np.all(est["kstar"] == 5)
+    for h in range(4):
+        for m in range(cfg.M):
+            Kc = min(m + 1, max(-(-5 * (m + 1) // cfg.M), 1))
+            order = np.argsort(-est["L"][0, m, :m], kind="stable")
+            ref = sorted(set(order[:Kc - 1].tolist()) | {m})
+            assert list(est["block_idx"][h, m, :est["block_cnt"][h, m]]) == ref
+
+
+@pytest.mark.parametrize("case", GOLD["constant_k_sparsity"], ids=lambda c: str(c["M"]))
+def test_constant_k_reading_counts_and_sparsity(case):
+    M, ks = case["M"], case["kstar"]
+    cfg = oracle.Cfg(1, 1, 32, 128 * M, 128, 4, 1, 0.9, constant_k=True)
+    counts = [oracle.row_count(cfg, ks, m) for m in range(M)]
+    assert counts == [min(m + 1, ks) for m in range(M)]
+    assert 1 - sum(counts) / (M * (M + 1) / 2) == pytest.approx(case["sparsity"], abs=5e-5)
+
+
+def test_force_sink_selects_block_zero_counted():
+    cfg = oracle.Cfg(4, 2, 8, 64 * 20, 64, 4, 1, 0.9, force_sink=True)
+    M = cfg.M
+    L = np.random.default_rng(5).standard_normal((1, M, M))
+    kstar = [1, 4, 9, 20]
+    cnt, idx, _ = oracle.select(cfg, L, kstar)
+    for h in range(4):
+        for m in range(M):
+            K = oracle.row_count(cfg, kstar[h], m)
+            lst = idx[h, m, :cnt[h, m]].tolist()
+            assert cnt[h, m] == K and lst[-1] == m
+            others = [n for n in np.argsort(-L[0, m, :m], kind="stable").tolist() if n != 0]
+            ref = {m} | ({0} if (K >= 2 and m > 0) else set()) | set(others[:max(K - 2, 0)])
+            assert set(lst) == ref, (h, m)

@@ -47,6 +47,12 @@ PRESETS: dict[str, StructParams] = {
     "default": StructParams(),
     "llama-128k": StructParams(sigma=0.93, beta_lo=0.48, beta_hi=1.44),
     "qwen-64k": StructParams(sigma=0.9, beta_lo=0.5, beta_hi=1.5),
+    # scripts/calibrate_len.py (bisection on beta_lo, beta_hi = 3 beta_lo, sigma 0.93) against
+    # P:941 Table 8 Llama: 16K 73.31 % (got 73.31), 32K 78.27 (78.28), 64K 83.19 (83.19);
+    # 256K is not reported by the paper: the 128K preset is used there.
+    "llama-16k": StructParams(sigma=0.93, beta_lo=0.311, beta_hi=0.933),
+    "llama-32k": StructParams(sigma=0.93, beta_lo=0.4291, beta_hi=1.2873),
+    "llama-64k": StructParams(sigma=0.93, beta_lo=0.548, beta_hi=1.644),
 }
 
 
