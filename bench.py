@@ -41,6 +41,11 @@ WORKLOAD = dict(name="llama3.1-8b-attn-128k", n_q_heads=32, n_kv_heads=8, head_d
                 min_budget_tokens=0, seed=0, preset="llama-128k")
 WORKLOADS = {
     "llama3.1-8b-attn-128k": WORKLOAD,
+    # Llama3.1-70B attention shape (64 Q / 8 KV heads, g = 1) at 128K
+    "llama3.1-70b-attn-128k": dict(name="llama3.1-70b-attn-128k", n_q_heads=64, n_kv_heads=8,
+                                   head_dim=128, seq_len=131072, block_size=128, stride=4,
+                                   n_groups=1, gamma=0.9, min_budget_tokens=0, seed=0,
+                                   preset="llama-128k"),
     # BASELINE.json configs[3]: Qwen2.5-7B attention shape, 64K, g = 4, min budget 2048
     "qwen2.5-7b-attn-64k": dict(name="qwen2.5-7b-attn-64k", n_q_heads=28, n_kv_heads=4,
                                 head_dim=128, seq_len=65536, block_size=128, stride=4,

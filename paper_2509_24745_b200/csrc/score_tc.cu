@@ -42,6 +42,7 @@ struct __align__(8) SBars {
     uint64_t s_full[2];
     uint64_t s_empty[2];
     uint32_t tmem_base;
+    float red[4][2];        // MAXPOOL, bs >= 64: per lane-quarter window maxima
 };
 constexpr size_t kSmem = 1024 + kTile * (1 + kStages) + sizeof(SBars);
 
@@ -52,6 +53,7 @@ struct ScoreParams {
     int n_tr;        // proxy: tile rows per group (Ns / 128)
     int n_chunks;    // chunks per tile row (proxy) / per head (budget)
     int r;           // budget: GQA ratio (local head -> local kv head)
+    int bs;          // proxy: sampled rows (= keys) per block, b / s
     float sc2;       // logit scale in log2 units
     float* part_m;   // LSE: [gl][Ns][n_chunks]; BUDGET: [Hl][M][128]
     float* part_s;
@@ -171,23 +173,70 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_arrive(&bars->s_empty[j & 1]);
             const bool diag = (u == diag_u);
             if (p.mode == kMaxpool) {
-                // window c covers sampled key columns [32c, 32c + 32) = block column 4u + c
+                // Eq. 1 max-pool over (bs x bs) windows, bs = b/s sampled rows/keys per block
+                // (16, 32, 64 or 128): max of the raw logits over each 16-column group first
+                // (the scale is positive), then over the bs columns of a window, then over the
+                // bs rows of the block (lanes / warps), then scale and subtract lse.
+                float h8[8];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    // max of the raw logits first (the scale is positive), 4 chains
-                    float w4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                for (int g = 0; g < 8; ++g) {
+                    float w2[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int col = c * 32 + e;
-                        const float x = (diag && col > rr) ? -INFINITY : __uint_as_float(raw[c][e]);
-                        w4[e & 3] = fmaxf(w4[e & 3], x);
+                    for (int e = 0; e < 16; ++e) {
+                        const int col = g * 16 + e;
+                        const float x = (diag && col > rr) ? -INFINITY
+                                                           : __uint_as_float(raw[col >> 5][col & 31]);
+                        w2[e & 1] = fmaxf(w2[e & 1], x);
                     }
-                    float w = fmaxf(fmaxf(w4[0], w4[1]), fmaxf(w4[2], w4[3])) * p.sc2 - lse_row;
-                    w = warp_max(w);
-                    if (lane == 0) {
-                        const int m = tr * 4 + quarter, n = u * 4 + c;
-                        p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                    h8[g] = fmaxf(w2[0], w2[1]);
+                }
+                const int nwin = 128 / p.bs;                 // windows (block columns) per tile
+                float win[8];                                // window maxima (first nwin valid)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    win[c] = p.bs == 16 ? h8[c]
+                           : p.bs == 32 ? fmaxf(h8[(2 * c) & 7], h8[(2 * c + 1) & 7])
+                           : p.bs == 64 ? fmaxf(fmaxf(h8[(4 * c) & 7], h8[(4 * c + 1) & 7]),
+                                                fmaxf(h8[(4 * c + 2) & 7], h8[(4 * c + 3) & 7]))
+                                        : fmaxf(fmaxf(fmaxf(h8[0], h8[1]), fmaxf(h8[2], h8[3])),
+                                                fmaxf(fmaxf(h8[4], h8[5]), fmaxf(h8[6], h8[7])));
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (c >= nwin) break;
+                    float w = win[c] * p.sc2 - lse_row;
+                    const int n = u * nwin + c;
+                    if (p.bs == 16) {                        // block rows = half warps
+#pragma unroll
+                        for (int o = 8; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+                        if ((lane & 15) == 0) {
+                            const int m = tr * 8 + quarter * 2 + (lane >> 4);
+                            p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                        }
+                    } else {
+                        w = warp_max(w);
+                        if (p.bs == 32) {
+                            if (lane == 0) {
+                                const int m = tr * 4 + quarter;
+                                p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                            }
+                        } else {                              // 64 / 128: combine warps in smem
+                            if (lane == 0) bars->red[quarter][c] = w;
+                        }
                     }
+                }
+                if (p.bs >= 64) {
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    const int wpb = p.bs / 32;               // warps (lane quarters) per block row
+                    if (threadIdx.x % 32 == 0 && (quarter % wpb) == 0) {
+                        for (int c = 0; c < nwin; ++c) {   // nwin <= 2 here
+                            float w = -INFINITY;
+                            for (int q = quarter; q < quarter + wpb; ++q) w = fmaxf(w, bars->red[q][c]);
+                            const int m = tr * nwin + quarter / wpb, n = u * nwin + c;
+                            p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                        }
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
             } else {
                 // raw logits; causal mask inside the diagonal tile; 8 independent max chains
@@ -368,7 +417,8 @@ bool set_smem_attr() {
 }  // namespace
 
 bool score_tc_supported(const Dims& D) {
-    return !D.fp32 && D.d == 128 && D.b == 128 && D.s == 4 && (D.Ns % 128) == 0;
+    return !D.fp32 && D.d == 128 && D.b == 128 && (D.s == 1 || D.s == 2 || D.s == 4 || D.s == 8) &&
+           (D.Ns % 128) == 0;
 }
 
 size_t score_tc_scratch_bytes(const Dims& D) {
@@ -393,6 +443,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.M = D.M;
     p.n_tr = static_cast<int>(D.Ns / 128);
     p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
+    p.bs = D.bs;
     // Eq. 2 means + 1/sqrt(d) folded into the scale (Z2, Z5), in log2 units.
     p.sc2 = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD)
                 ? kLog2e / sqrtf(static_cast<float>(D.d))

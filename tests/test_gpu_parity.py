@@ -152,9 +152,9 @@ def test_config_a_fp32_end_to_end_matches_staged():
 
 
 # ------------------------------------------------- bf16, structured, small N --
-def llama_small(N=2048, gamma=0.9, heads=(8, 2), g=1, min_budget=0):
+def llama_small(N=2048, gamma=0.9, heads=(8, 2), g=1, min_budget=0, stride=4):
     return pa.Config(n_q_heads=heads[0], n_kv_heads=heads[1], head_dim=128, seq_len=N,
-                     block_size=128, stride=4, n_groups=g, gamma=gamma,
+                     block_size=128, stride=stride, n_groups=g, gamma=gamma,
                      min_budget_tokens=min_budget)
 
 
@@ -163,6 +163,9 @@ def llama_small(N=2048, gamma=0.9, heads=(8, 2), g=1, min_budget=0):
     dict(N=2048, gamma=0.95, heads=(8, 2), g=2, seed=1),
     dict(N=4096, gamma=0.9, heads=(7, 1), g=1, seed=2, min_budget=512),     # Qwen-like r=7
     dict(N=1152, gamma=0.7, heads=(4, 4), g=2, seed=3),                     # ragged: M=9
+    dict(N=1024, gamma=0.9, heads=(8, 2), g=1, seed=4, stride=1),           # b/s = 128
+    dict(N=2048, gamma=0.9, heads=(8, 2), g=2, seed=5, stride=2),           # b/s = 64
+    dict(N=4096, gamma=0.9, heads=(8, 2), g=1, seed=6, stride=8),           # b/s = 16
 ])
 def test_bf16_structured_staged(case):
     case = dict(case)
