@@ -34,7 +34,9 @@ extern "C" {
 /* ---------------------------------------------------------------- config -- */
 
 /* AttnConfig.  Invariants: Hq % Hkv == 0, Hkv % g == 0, b % s == 0,
- * N % b == 0 (Z19), 0 < gamma <= 1, min_budget_tokens >= 0.
+ * 0 < gamma <= 1, min_budget_tokens >= 0.  N need not be a multiple of b: M = ceil(N/b)
+ * blocks, the last one zero-padded with its padded keys masked and no output for padded
+ * rows; sampled positions are i*s < N, N/s rounded up.
  * bf16 build supports d == 128, b == 128; FP32_DEBUG supports d % 32 == 0, d <= 128,
  * any b with b % s == 0 (SIMT kernels, for the 1e-4 parity contract). */
 typedef struct {

@@ -76,11 +76,11 @@ class Cfg:
 
     @property
     def M(self) -> int:
-        return self.seq_len // self.block_size
+        return -(-self.seq_len // self.block_size)      # ceil: the last block may be padded
 
     @property
     def Ns(self) -> int:
-        return self.seq_len // self.stride
+        return -(-self.seq_len // self.stride)
 
     def c(self) -> _CCfg:
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,

@@ -26,14 +26,19 @@ int oracle_validate(const oracle_cfg* c) {
     if (c->n_q_heads % c->n_kv_heads != 0) return -1;   /* GQA ratio integral */
     if (c->n_kv_heads % c->n_groups != 0) return -1;    /* groups aligned with the keys */
     if (c->block_size % c->stride != 0) return -1;
-    if (c->seq_len % c->block_size != 0) return -1;     /* Z19: v1 rejects ragged N */
+    /* N % b != 0 is allowed: the last block is padded */
     if (!(c->gamma > 0.0 && c->gamma <= 1.0)) return -1;
     if (c->min_budget_tokens < 0) return -1;
     return 0;
 }
 
-static int n_blocks(const oracle_cfg* c) { return (int)(c->seq_len / c->block_size); }
-static long n_sampled(const oracle_cfg* c) { return c->seq_len / c->stride; }
+/* M = ceil(N / b) blocks; the last one is zero-padded when b does not divide N and the
+ * padded tokens are masked as keys and produce no output. */
+static int n_blocks(const oracle_cfg* c) {
+    return (int)((c->seq_len + c->block_size - 1) / c->block_size);
+}
+/* sampled positions p = i*s < N (keep the first token of every stride window) */
+static long n_sampled(const oracle_cfg* c) { return (c->seq_len + c->stride - 1) / c->stride; }
 
 /* "the group granularity will be aligned with the keys"; Z3: contiguous ranges. */
 static int group_of_kv(const oracle_cfg* c, int kvh) {
@@ -118,6 +123,7 @@ void oracle_proxy_scores(const oracle_cfg* c, const double* Pq, const double* Pk
             for (int n = 0; n < M; ++n) Lrow[n] = -INFINITY;     /* n > m stays -inf */
             for (int ii = 0; ii < bs; ++ii) {
                 long i = (long)m * bs + ii;
+                if (i >= Ns) break;                        /* padded sampled rows of the last block */
                 const double* qi = Pq + ((long)grp * Ns + i) * d;
                 /* O4: z_ij for sampled keys j <= i (causal by original positions j*s <= i*s) */
                 double mx = -INFINITY;
@@ -211,7 +217,7 @@ void oracle_budgets(const oracle_cfg* c, const float* Q, const float* K,
             for (int n = 0; n < M; ++n) a[n] = 0.0;
             /* Alg. 1 line 1: A^ = softmax(Q_last K^T / sqrt(d_k)), own head, full resolution,
              * causal inside the last block (Z7). */
-            for (long t = N - b; t < N; ++t) {
+            for (long t = (long)(M - 1) * b; t < N; ++t) {   /* the last block's query rows */
                 const float* q = Q + ((long)h * N + t) * d;
                 double mx = -INFINITY;
                 for (long k = 0; k <= t; ++k) {
@@ -303,7 +309,7 @@ static void attend_rows(const oracle_cfg* c, const float* Q, const float* K, con
     const long N = c->seq_len;
     const int kvh = h / (c->n_q_heads / c->n_kv_heads);
     const double sd = sqrt((double)d);
-    for (long t = (long)m * b; t < (long)(m + 1) * b; ++t) {
+    for (long t = (long)m * b; t < (long)(m + 1) * b && t < N; ++t) {
         const float* q = Q + ((long)h * N + t) * d;
         /* pass 1: logits over the selected blocks' keys with k <= t, and their max */
         long nk = 0;

@@ -41,7 +41,8 @@ typedef struct {
     int32_t static_kstar;       /* > 0: every head uses K* = static_kstar (Fig. 6c static top-K) */
 } oracle_cfg;
 
-/* O1: returns 0 when the config satisfies the DS-1 invariants, -1 otherwise. */
+/* O1: returns 0 when the config satisfies the DS-1 invariants, -1 otherwise.
+ * N need not be a multiple of b: M = ceil(N/b), the last block is zero-padded. */
 int oracle_validate(const oracle_cfg* c);
 
 /* O3 helper: round a double to the nearest bf16 value, ties to even (plain definition). */

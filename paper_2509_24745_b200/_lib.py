@@ -77,7 +77,11 @@ class Config:
 
     @property
     def M(self) -> int:
-        return self.seq_len // self.block_size
+        return -(-self.seq_len // self.block_size)     # ceil: a partial last block is padded
+
+    @property
+    def Ns(self) -> int:
+        return -(-self.seq_len // self.stride)
 
     @property
     def r(self) -> int:
@@ -224,7 +228,7 @@ def dense_prefill(cfg: Config, Q, K, V, O=None):
 def pool(cfg: Config, Q, K):
     """proxyattn_pool -> fp32 (qsum, ksum) [g_l][N/s][d]."""
     gl = _local_groups(cfg)
-    shape = (gl, cfg.seq_len // cfg.stride, cfg.head_dim)
+    shape = (gl, cfg.Ns, cfg.head_dim)
     qsum = torch.empty(shape, dtype=torch.float32, device=Q.device)
     ksum = torch.empty_like(qsum)
     _check(lib().proxyattn_pool(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(qsum), _ptr(ksum),

@@ -47,8 +47,6 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
         return fail(PROXYATTN_E_CONFIG, "n_kv_heads %% n_groups != 0 (S:31)");
     if (c->block_size % c->stride)
         return fail(PROXYATTN_E_CONFIG, "block_size %% stride != 0 (S:32)");
-    if (c->seq_len % c->block_size)
-        return fail(PROXYATTN_E_CONFIG, "seq_len %% block_size != 0 (Z19: padding not supported)");
     if (!(c->gamma > 0.f && c->gamma <= 1.f))
         return fail(PROXYATTN_E_CONFIG, "gamma must be in (0, 1] (S:33)");
     if (c->min_budget_tokens < 0) return fail(PROXYATTN_E_CONFIG, "min_budget_tokens < 0");
@@ -69,8 +67,8 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     D.g = c->n_groups;
     D.r = D.Hq / D.Hkv;
     D.N = c->seq_len;
-    D.M = static_cast<int>(D.N / D.b);
-    D.Ns = D.N / D.s;
+    D.M = static_cast<int>((D.N + D.b - 1) / D.b);   // last block zero-padded when b does not divide N
+    D.Ns = (D.N + D.s - 1) / D.s;                    // sampled positions i*s < N
     D.bs = D.b / D.s;
     D.gamma = c->gamma;
     D.flags = c->flags;
@@ -257,6 +255,8 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32) {
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
+        if (pa::attn_variant() != 3 && D.N % D.b)
+            return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0");
         if (pa::attn_variant() == 4)
             PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
         else if (pa::attn_variant() == 5)

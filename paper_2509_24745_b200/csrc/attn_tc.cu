@@ -308,7 +308,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, raw[c]);
             tmem_ld_wait();
-            if (n == m) {  // diagonal block: key index > row index is masked (causal)
+            if (n == m) {  // diagonal block: key index > row index is masked (causal); this
+                           // also masks the zero-padded keys of a partial last block
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -395,6 +396,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
         // ----------------------------------------------------------- epilogue --
         if (my_cnt > 0) {
+            const bool row_valid = static_cast<long long>(m) * kTileRows + rr < N;   // padded rows: no output
             mbar_wait(&bars->o_done[slot], (my_cnt - 1) & 1);
             tc_fence_after();
             const float inv = 1.f / l;
@@ -410,9 +412,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
                 for (int e = 0; e < 16; ++e)
                     pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+                if (row_valid) {
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    dst[c * 4 + v] = make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+                    for (int v = 0; v < 4; ++v)
+                        dst[c * 4 + v] = make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+                }
             }
         }
     }

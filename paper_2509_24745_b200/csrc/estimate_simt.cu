@@ -201,6 +201,7 @@ __global__ void proxy_maxpool_simt(Dims D, const T* __restrict__ Pq, const T* __
     float best = -INFINITY;
     for (int ii = 0; ii < D.bs; ++ii) {
         const long long i = static_cast<long long>(m) * D.bs + ii;
+        if (i >= D.Ns) break;                     // padded sampled rows of a partial last block
         float q[4];
         load_row(qb + i * D.d, lane, q, dv);
         const float li = lse[static_cast<long long>(c) * D.Ns + i];
@@ -227,7 +228,11 @@ __global__ void budget_lse_simt(Dims D, const T* __restrict__ Q, const T* __rest
     const int lane = threadIdx.x & 31;
     if (w >= static_cast<long long>(D.Hl) * D.b) return;
     const int hl = static_cast<int>(w / D.b);
-    const long long t = D.N - D.b + (w % D.b);
+    const long long t = static_cast<long long>(D.M - 1) * D.b + (w % D.b);   // last block's rows
+    if (t >= D.N) {                               // padded row of a partial last block
+        if (lane == 0) blse[w] = INFINITY;        // contributes exp(-inf) = 0 to the masses
+        return;
+    }
     const int dv = D.d >> 5;
     const float sc = rsqrtf(static_cast<float>(D.d));
     float q[4];
@@ -265,7 +270,8 @@ __global__ void budget_mass_simt(Dims D, const T* __restrict__ Q, const T* __res
     const T* kb = K + static_cast<long long>(hl / D.r) * D.N * D.d;
     float acc = 0.f;
     for (int tt = 0; tt < D.b; ++tt) {
-        const long long t = D.N - D.b + tt;
+        const long long t = static_cast<long long>(D.M - 1) * D.b + tt;
+        if (t >= D.N) break;
         float q[4];
         load_row(Q + (static_cast<long long>(hl) * D.N + t) * D.d, lane, q, dv);
         const float lt = blse[static_cast<long long>(hl) * D.b + tt];

@@ -73,7 +73,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int k = blockIdx.x % p.n_chunks;
         u_begin = k * kChunk;
         u_end = min(u_begin + kChunk, p.M);
-        a_row = prob * p.N + (p.N - 128);
+        a_row = prob * p.N + (p.M - 1) * 128;     // the last block's query rows (Alg. 1)
         b_row0 = (prob / p.r) * p.N;
         diag_u = p.M - 1;
     } else {
@@ -160,7 +160,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         float m_run = -INFINITY, s_run = 0.f;
         float lse_row = 0.f;
-        if (p.mode == kMaxpool) lse_row = p.lse2[static_cast<long long>(prob) * p.Ns + tr * 128 + rr];
+        // rows past the end (partial last tile / block): padded, excluded from every output
+        const bool row_ok = (p.mode == kBudget) ? ((p.M - 1) * 128 + rr < p.N) : (tr * 128 + rr < p.Ns);
+        if (p.mode == kMaxpool)
+            lse_row = row_ok ? p.lse2[static_cast<long long>(prob) * p.Ns + tr * 128 + rr] : INFINITY;
         for (int j = 0; j < nt; ++j) {
             const int u = u_begin + j;
             mbar_wait(&bars->s_full[j & 1], (j >> 1) & 1);
@@ -211,14 +214,14 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         for (int o = 8; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
                         if ((lane & 15) == 0) {
                             const int m = tr * 8 + quarter * 2 + (lane >> 4);
-                            p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                            if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
                         }
                     } else {
                         w = warp_max(w);
                         if (p.bs == 32) {
                             if (lane == 0) {
                                 const int m = tr * 4 + quarter;
-                                p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                                if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
                             }
                         } else {                              // 64 / 128: combine warps in smem
                             if (lane == 0) bars->red[quarter][c] = w;
@@ -233,7 +236,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             float w = -INFINITY;
                             for (int q = quarter; q < quarter + wpb; ++q) w = fmaxf(w, bars->red[q][c]);
                             const int m = tr * nwin + quarter / wpb, n = u * nwin + c;
-                            p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
+                            if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
                         }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -286,12 +289,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     m_run = ref;
                 } else {
                     const long long o = (static_cast<long long>(prob) * p.M + u) * 128 + rr;
-                    p.part_m[o] = tmax;
-                    p.part_s[o] = acc;
+                    p.part_m[o] = row_ok ? tmax : -INFINITY;   // padded rows carry no mass
+                    p.part_s[o] = row_ok ? acc : 0.f;
                 }
             }
         }
-        if (p.mode == kLse) {
+        if (p.mode == kLse && row_ok) {
             const int k = u_begin / kChunk;
             const long long o =
                 (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.n_chunks + k;
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float
     for (int u = u0; u < u1; ++u) {
         const float mu = __ldg(pm + static_cast<long long>(u) * 128 + t);
         const float su = __ldg(ps + static_cast<long long>(u) * 128 + t);
+        if (!(su > 0.f)) continue;                  // padded row (no mass)
         if (mu > m) {
             sum = sum * ex2(m - mu) + su;
             m = mu;
@@ -365,8 +369,8 @@ __global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float
         float mx = -INFINITY;
         for (int k = 0; k < 8; ++k) mx = fmaxf(mx, cm[k][t]);
         float s2 = 0.f;
-        for (int k = 0; k < 8; ++k) s2 += cs[k][t] * ex2(cm[k][t] - mx);
-        lse_s[t] = mx + __log2f(s2);
+        for (int k = 0; k < 8; ++k) s2 += (cs[k][t] > 0.f) ? cs[k][t] * ex2(cm[k][t] - mx) : 0.f;
+        lse_s[t] = (s2 > 0.f) ? mx + __log2f(s2) : INFINITY;   // padded row: no mass
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -378,7 +382,10 @@ __global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float
         const float* psu = ps + static_cast<long long>(u) * 128;
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a += __ldg(psu + lane + 32 * k) * ex2(__ldg(pmu + lane + 32 * k) - l4[k]);
+        for (int k = 0; k < 4; ++k) {
+            const float sv = __ldg(psu + lane + 32 * k);
+            if (sv > 0.f) a += sv * ex2(__ldg(pmu + lane + 32 * k) - l4[k]);
+        }
         a = warp_sum(a);
         if (lane == 0) bmass[static_cast<long long>(hl) * M + u] = a / (128.f * 128.f);
     }
@@ -417,12 +424,11 @@ bool set_smem_attr() {
 }  // namespace
 
 bool score_tc_supported(const Dims& D) {
-    return !D.fp32 && D.d == 128 && D.b == 128 && (D.s == 1 || D.s == 2 || D.s == 4 || D.s == 8) &&
-           (D.Ns % 128) == 0;
+    return !D.fp32 && D.d == 128 && D.b == 128 && (D.s == 1 || D.s == 2 || D.s == 4 || D.s == 8);
 }
 
 size_t score_tc_scratch_bytes(const Dims& D) {
-    const int n_tr = static_cast<int>(D.Ns / 128);
+    const int n_tr = static_cast<int>((D.Ns + 127) / 128);
     const int n_chunks = (n_tr + kChunk - 1) / kChunk;
     const size_t lse_parts = 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4;
     const size_t bud_parts = 2ull * D.Hl * D.M * 128 * 4;
@@ -441,7 +447,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     ScoreParams p{};
     p.Ns = static_cast<int>(D.Ns);
     p.M = D.M;
-    p.n_tr = static_cast<int>(D.Ns / 128);
+    p.n_tr = static_cast<int>((D.Ns + 127) / 128);
     p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
     p.bs = D.bs;
     // Eq. 2 means + 1/sqrt(d) folded into the scale (Z2, Z5), in log2 units.

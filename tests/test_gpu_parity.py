@@ -136,6 +136,23 @@ def test_config_a_fp32_staged(seed, gamma):
         assert torch.equal(O, Od) or torch.allclose(O, Od, atol=1e-6)   # AC2
 
 
+def test_config_a_fp32_ragged_n():
+    cfg = CFG_A.replace(seq_len=1000)                    # M = 16, last block 40 tokens
+    oc = ocfg_of(cfg)
+    Q, K, V = workloads.iid(8, 2, 1000, 64, 7)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    est = oracle.estimate(oc, Q.numpy(), K.numpy())
+    ks = kstar.cpu().numpy()
+    ok = est["budget_margin"] > MARGIN
+    assert np.array_equal(ks[ok], est["kstar"][ok])
+    check_masks(oc, est["L"], ks, cnt, idx)
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    check_out(O, oracle.attention(oc, Q.numpy(), K.numpy(), V.numpy(), cnt.cpu().numpy(),
+                                  idx.cpu().numpy()), fp32=True)
+    check_out(pa.dense_prefill(cfg, Qd, Kd, Vd), oracle.dense(oc, Q.numpy(), K.numpy(), V.numpy()), fp32=True)
+
+
 def test_config_a_fp32_end_to_end_matches_staged():
     cfg = CFG_A
     Q, K, V = to_dev(*workloads.iid(8, 2, 1024, 64, 5))
@@ -166,6 +183,9 @@ def llama_small(N=2048, gamma=0.9, heads=(8, 2), g=1, min_budget=0, stride=4):
     dict(N=1024, gamma=0.9, heads=(8, 2), g=1, seed=4, stride=1),           # b/s = 128
     dict(N=2048, gamma=0.9, heads=(8, 2), g=2, seed=5, stride=2),           # b/s = 64
     dict(N=4096, gamma=0.9, heads=(8, 2), g=1, seed=6, stride=8),           # b/s = 16
+    dict(N=2000, gamma=0.9, heads=(8, 2), g=1, seed=7),                     # ragged N
+    dict(N=3001, gamma=0.95, heads=(7, 1), g=1, seed=8, min_budget=256),    # ragged, N % s != 0
+    dict(N=700, gamma=0.7, heads=(4, 2), g=2, seed=9, stride=2),            # ragged, M = 6
 ])
 def test_bf16_structured_staged(case):
     case = dict(case)

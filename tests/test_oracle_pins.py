@@ -58,9 +58,10 @@ def bf_attention(q, k, v, allowed=None):
 # ------------------------------------------------------------------------------- O1 --
 def test_validate_rejects_invariant_violations():
     assert oracle.validate(CFG_A)
-    for bad in [dict(n_q_heads=7), dict(n_groups=3), dict(stride=3), dict(seq_len=1000),
+    for bad in [dict(n_q_heads=7), dict(n_groups=3), dict(stride=3), dict(seq_len=0),
                 dict(gamma=0.0), dict(gamma=1.5), dict(min_budget_tokens=-1)]:
         assert not oracle.validate(CFG_A.replace(**bad)), bad
+    assert oracle.validate(CFG_A.replace(seq_len=1000))        # ragged N: padded last block
 
 
 # ------------------------------------------------------------------------------- O2 --
@@ -571,3 +572,47 @@ def test_force_sink_selects_block_zero_counted():
             others = [n for n in np.argsort(-L[0, m, :m], kind="stable").tolist() if n != 0]
             ref = {m} | ({0} if (K >= 2 and m > 0) else set()) | set(others[:max(K - 2, 0)])
             assert set(lst) == ref, (h, m)
+
+
+# ------------------------------------------------------------------- ragged N --
+def test_ragged_n_dense_and_degenerate_proxy_brute_force():
+    # S:81 zero-pad + mask: the block structure must not change the textbook results
+    cfg = oracle.Cfg(2, 2, 8, 90, 16, 1, 2, 0.9)          # M = 6, last block has 10 tokens
+    assert cfg.M == 6 and cfg.Ns == 90
+    Q, K, V = rand_qkv(cfg, 41, scale=2.0)
+    O = oracle.dense(cfg, Q, K, V)
+    for h in range(2):
+        assert O[h] == pytest.approx(bf_attention(Q[h], K[h], V[h]), abs=1e-12)
+    Pq, Pk, scale = oracle.pool(cfg, Q, K)
+    _, L = oracle.proxy_scores(cfg, Pq, Pk, scale)
+    b = cfg.block_size
+    for h in range(2):
+        P = bf_probs(Q[h], K[h])
+        for m in range(cfg.M):
+            for n in range(m + 1):
+                ref = P[m * b:(m + 1) * b, n * b:(n + 1) * b].max()   # slices clip at N
+                assert math.exp(L[h, m, n]) == pytest.approx(ref, rel=1e-12, abs=1e-300)
+
+
+def test_ragged_n_budget_brute_force_uses_partial_last_block():
+    cfg = oracle.Cfg(2, 1, 16, 300, 64, 4, 1, 0.8)         # M = 5, last block rows 256..299
+    Q, K, _ = rand_qkv(cfg, 42, scale=1.5)
+    kstar, _, _, mass = oracle.budgets(cfg, Q, K)
+    b, M, N = 64, cfg.M, 300
+    for h in range(2):
+        P = bf_probs(Q[h], K[0])[(M - 1) * b:N]              # the last block's 44 real rows
+        a = np.array([P[:, n * b:(n + 1) * b].sum() for n in range(M)]) / b ** 2
+        assert mass[h] == pytest.approx(a, rel=1e-10, abs=1e-18)
+        srt = np.sort(a)[::-1]
+        ref = int(np.argmax(np.cumsum(srt / srt.sum()) >= cfg.gamma)) + 1
+        assert kstar[h] == ref
+
+
+def test_ragged_n_sampled_rows_and_gamma_one_equals_dense():
+    cfg = oracle.Cfg(4, 2, 16, 1000, 64, 4, 1, 1.0)          # Ns = 250, last block: 232 tokens
+    Q, K, V = rand_qkv(cfg, 43)
+    Pq, _, _ = oracle.pool(cfg, Q, K)
+    assert Pq.shape[1] == 250
+    assert np.array_equal(Pq[0, 249], Q[:, 996].astype(np.float64).sum(0))
+    est = oracle.pipeline(cfg, Q, K, V)
+    assert np.max(np.abs(est["O"] - oracle.dense(cfg, Q, K, V))) <= 1e-12
