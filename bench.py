@@ -53,7 +53,9 @@ WORKLOADS = {
                                 preset="qwen-64k"),
 }
 L2_FLUSH_BYTES = 256 << 20
-KERNELS_PER_STEP = 8   # pool, proxy_lse, proxy_maxpool, budget_lse, budget_mass, finalize, select, attn
+# kernels per step: estimate = pool, proxy lse, lse combine, -inf fill, proxy max-pool, budget
+# partials, budget combine, budget finalize, select (9); + one attention launch per row range
+ESTIMATE_KERNELS = 9
 
 
 def peaks() -> dict:
@@ -122,12 +124,14 @@ class ClockSampler:
                        "samples": len(rows), "reasons": reasons}
 
 
-def build_config(pa, rank: int, ws: int, w=WORKLOAD):
+def build_config(pa, rank: int, ws: int, w=WORKLOAD, sharding="rows"):
     from paper_2509_24745_b200 import shard
 
     cfg = pa.Config(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"],
                     w["block_size"], w["stride"], w["n_groups"], w["gamma"],
                     w["min_budget_tokens"])
+    if sharding == "rows":      # every rank holds the layer; rows are split (zig-zag)
+        return cfg
     return shard.shard_config(cfg, ws, rank)
 
 
@@ -220,11 +224,18 @@ def run_ours(args):
     import paper_2509_24745_b200 as pa
 
     ws, rank, local = dist_env()
+    # BENCH_SAME_DEVICE=1 (testing only): every rank on cuda:0, gloo only -> exercises the
+    # multi-rank code path on a one-GPU box (its timings are meaningless).
+    same_dev = os.environ.get("BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
+    cpu_group = None
     if ws > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if same_dev else "nccl")
+        cpu_group = dist.new_group(backend="gloo")      # timing / bookkeeping collectives
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     w = dict(WORKLOADS[args.workload])
@@ -236,7 +247,8 @@ def run_ours(args):
         cand = w["preset"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
         if cand in workloads.PRESETS:      # per-length calibration to Table 8
             w["preset"] = cand
-    cfg = build_config(pa, rank, ws, w)
+    sharding = args.shard if ws > 1 else "rows"
+    cfg = build_config(pa, rank, ws, w, sharding)
     Q, K, V, meta = gen_inputs(w, dev)
     hb, he = cfg.local_heads
     r = cfg.r
@@ -254,19 +266,26 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     from paper_2509_24745_b200 import shard
 
+    my_rows = shard.zigzag_rows(M, ws, rank) if sharding == "rows" else [(0, M)]
+
     def estimate():
-        # g < #ranks: pool -> NCCL all-reduce of the pooled sums -> scores
-        shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=(kstar, budget, cnt, idx))
+        if sharding == "rows":   # replicated estimate (~1 ms), no cross-GPU traffic
+            pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
+        else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums
+            shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=(kstar, budget, cnt, idx))
 
     def prefill():
-        pa.prefill(cfg, Ql, Kl, Vl, cnt, idx, O)
+        if sharding == "rows" and ws > 1:
+            shard.prefill_rows(cfg, Ql, Kl, Vl, cnt, idx, O, my_rows)
+        else:
+            pa.prefill(cfg, Ql, Kl, Vl, cnt, idx, O)
 
     def barrier():
         torch.cuda.synchronize()
         if ws > 1:
             import torch.distributed as dist
 
-            dist.barrier()
+            dist.barrier(group=cpu_group)
             torch.cuda.synchronize()
 
     st = torch.cuda.current_stream(dev)
@@ -307,16 +326,16 @@ def run_ours(args):
 
     # max over ranks
     vec = torch.tensor([total_ms / args.steps, float(np.mean(est_ms)), float(np.mean(att_ms)), dense],
-                       dtype=torch.float64, device=dev)
-    sel_blocks = float(cnt.sum().item())
-    blocks_t = torch.tensor([sel_blocks], dtype=torch.float64, device=dev)
+                       dtype=torch.float64)
+    sel_blocks = float(sum(cnt[:, b:e].sum().item() for b, e in my_rows))
+    blocks_t = torch.tensor([sel_blocks], dtype=torch.float64)
     per_rank_blocks = [sel_blocks]
-    if ws > 1:
+    if ws > 1:                       # max over ranks (device-timed), on the gloo group
         import torch.distributed as dist
 
-        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX, group=cpu_group)
         parts = [torch.empty_like(blocks_t) for _ in range(ws)]
-        dist.all_gather(parts, blocks_t)
+        dist.all_gather(parts, blocks_t, group=cpu_group)
         per_rank_blocks = [float(p.item()) for p in parts]
     layer_ms, est_m, att_m, dense_m = vec.tolist()
     total_blocks = float(sum(per_rank_blocks))
@@ -391,7 +410,8 @@ def run_ours(args):
                    "head_dim": d, "seq_len": w["seq_len"], "block": b, "stride": w["stride"],
                    "proxy_groups": w["n_groups"], "gamma": w["gamma"],
                    "min_budget_tokens": w["min_budget_tokens"],
-                   "parallelism": f"head-group x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": (f"zig-zag block rows x{ws}" if sharding == "rows" else
+                                   f"kv-head groups x{ws}") if ws > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "speedup_vs_dense": dense_m / layer_ms,
         "dense_ms": dense_m,
@@ -407,7 +427,7 @@ def run_ours(args):
         "work_share": [x / total_blocks for x in per_rank_blocks],
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "gpu_launches": (ESTIMATE_KERNELS + len(my_rows)) * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
@@ -425,6 +445,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq-len", type=int, default=0, help="override N (sweep)")
     ap.add_argument("--workload", default="llama3.1-8b-attn-128k", choices=sorted(WORKLOADS))
+    ap.add_argument("--shard", default="rows", choices=["rows", "heads"],
+                    help="N > 1: zig-zag query-block-row sharding (balanced, no traffic) or "
+                         "KV-head-group sharding (all-reduce of pooled sums when g < N)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()

@@ -54,6 +54,10 @@ typedef struct {
     int32_t  q_head_end;
     int32_t  static_kstar;       /* > 0: static top-K baseline (Fig. 6c): every head uses
                                     K* = static_kstar instead of Alg. 1's dynamic budget; 0 = Alg. 1 */
+    int32_t  row_begin;          /* prefill / dense_prefill only: compute query block rows
+                                    [row_begin, row_end) (row_end == 0: all rows); other rows of O
+                                    are left untouched (zig-zag row sharding) */
+    int32_t  row_end;
 } proxyattn_cfg;
 
 #define PROXYATTN_FLAG_FP32_DEBUG  0x1u  /* fp32 Q/K/V/O, SIMT FFMA kernels (1e-4 contract)   */

@@ -50,6 +50,8 @@ class _CCfg(ctypes.Structure):
         ("q_head_begin", ctypes.c_int32),
         ("q_head_end", ctypes.c_int32),
         ("static_kstar", ctypes.c_int32),
+        ("row_begin", ctypes.c_int32),
+        ("row_end", ctypes.c_int32),
     ]
 
 
@@ -74,6 +76,8 @@ class Config:
     constant_k: bool = False
     designated_head: bool = False
     static_kstar: int = 0
+    row_begin: int = 0              # prefill row range (zig-zag row sharding); 0/0 = all rows
+    row_end: int = 0
 
     @property
     def M(self) -> int:
@@ -111,7 +115,7 @@ class Config:
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
                      self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,
-                     self.static_kstar)
+                     self.static_kstar, self.row_begin, self.row_end)
 
 
 _lib = None

@@ -74,6 +74,10 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     D.flags = c->flags;
     if (c->static_kstar < 0) return fail(PROXYATTN_E_CONFIG, "static_kstar < 0");
     D.static_kstar = c->static_kstar;
+    D.rb = c->row_begin;
+    D.re = c->row_end == 0 ? D.M : c->row_end;
+    if (D.rb < 0 || D.re > D.M || D.rb >= D.re)
+        return fail(PROXYATTN_E_CONFIG, "bad row range [%d, %d) of %d block rows", D.rb, D.re, D.M);
     D.F = (c->min_budget_tokens + D.b - 1) / D.b;
     D.gq = D.Hq / D.g;
     D.gk = D.Hkv / D.g;
@@ -255,8 +259,8 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32) {
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
-        if (pa::attn_variant() != 3 && D.N % D.b)
-            return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0");
+        if (pa::attn_variant() != 3 && (D.N % D.b || D.rb != 0 || D.re != D.M))
+            return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0 and all rows");
         if (pa::attn_variant() == 4)
             PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
         else if (pa::attn_variant() == 5)

@@ -16,6 +16,7 @@ __global__ void attn_simt_kernel(Dims D, const float* __restrict__ Q, const floa
     const int hl = static_cast<int>(w / D.N);
     const long long t = w % D.N;
     const int m = static_cast<int>(t / D.b);
+    if (m < D.rb || m >= D.re) return;                      // outside the requested row range
     const int dv = D.d >> 5;
     const float sc = rsqrtf(static_cast<float>(D.d));
     const long long kvoff = static_cast<long long>(hl / D.r) * D.N * D.d;

@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-               int r, int Hl, int pair_mode, float scale_log2, long long* trace, int trace_bid) {
+               int r, int Hl, int pair_mode, float scale_log2, long long* trace, int trace_bid,
+               int row_lo, int row_hi) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -102,23 +103,24 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     // ordered kv-head major (so the ~148 resident CTAs stream one kv head's K/V through L2
     // together), heaviest rows first within a kv head.
     int hs0, hs1, ms0, ms1, nslots;
+    const int nrows = row_hi - row_lo;   // block rows [row_lo, row_hi) of this launch
     if (pair_mode == 0) {              // two heads of one kv head, same row
         const int ppk = (r + 1) >> 1;
-        const int per_kv = ppk * M;
+        const int per_kv = ppk * nrows;
         const int kvi = bid / per_kv, rem = bid % per_kv;
         const int i0 = 2 * (rem % ppk);
-        ms0 = ms1 = M - 1 - rem / ppk;
+        ms0 = ms1 = row_hi - 1 - rem / ppk;
         hs0 = kvi * r + i0;
         hs1 = hs0 + 1;
         nslots = (i0 + 1 < r) ? 2 : 1;
     } else {                           // one head, two adjacent rows
-        const int nrp = (M + 1) >> 1;
+        const int nrp = (nrows + 1) >> 1;
         const int per_kv = r * nrp;
         const int kvi = bid / per_kv, rem = bid % per_kv;
         hs0 = hs1 = kvi * r + rem % r;
-        ms0 = M - 1 - 2 * (rem / r);
+        ms0 = row_hi - 1 - 2 * (rem / r);
         ms1 = ms0 - 1;
-        nslots = ms1 >= 0 ? 2 : 1;
+        nslots = ms1 >= row_lo ? 2 : 1;
     }
     (void)Hl;
     const int kvl = hs0 / r;
@@ -480,9 +482,10 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
     const int mode = attn_pair_mode();
+    const int nrows = D.re - D.rb;
     const unsigned grid = mode == 0
-        ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(D.M)
-        : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((D.M + 1) / 2);
+        ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(nrows)
+        : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((nrows + 1) / 2);
     // PROXYATTN_TRACE=<cta>: per-event clock64 timeline of one CTA (diagnostics only), read
     // back with proxyattn_debug_trace().
     static long long* trace = nullptr;
@@ -496,7 +499,7 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
     attn_trace_ptr() = trace;
     kern<<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
-        D.M, D.r, D.Hl, mode, scale_log2, trace, trace_bid);
+        D.M, D.r, D.Hl, mode, scale_log2, trace, trace_bid, D.rb, D.re);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ struct Dims {
     uint32_t flags;
     bool fp32;    // FP32_DEBUG
     int static_kstar;   // > 0: static top-K baseline (Alg. 1 skipped)
+    int rb, re;         // prefill block-row range [rb, re)
 };
 
 __host__ __device__ __forceinline__ bool has_flag(const Dims& D, uint32_t f) { return (D.flags & f) != 0; }

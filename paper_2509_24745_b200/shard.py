@@ -9,6 +9,11 @@
   step: fp32 partial sums of the local heads are all-reduced (sum), then each rank rounds
   them and computes the group's block scores itself (replicated, ~0.3 ms at 128K).
 * all_gather of O is for verification only (not part of the timed step).
+* Balanced alternative: zig-zag query-block-row sharding.  Every rank holds
+  the whole layer, runs the (cheap, replicated) estimate for all heads, and computes the
+  attention of two row chunks p and 2P-1-p for all heads; since K_{h,m} grows ~linearly in
+  m for every head (reading Z12), the pair sums to the same work on every rank regardless
+  of how budgets differ between heads, with no cross-GPU traffic at all.
 
 The ops are the C-ABI calls of paper_2509_24745_b200 by default; tests inject other ops
 with the same signatures to check the orchestration on CPU with the gloo backend.
@@ -106,3 +111,37 @@ def work_share(block_cnt_full: torch.Tensor, n_kv_heads: int, world: int) -> lis
         b, e = head_shard(H, n_kv_heads, world, r)
         out.append(float(block_cnt_full[b:e].sum()) / tot)
     return out
+
+
+def zigzag_rows(M: int, world: int, rank: int) -> list[tuple[int, int]]:
+    """Block-row ranges of `rank` under zig-zag sharding: chunks p and 2P-1-p of 2P
+    near-equal chunks of [0, M) (empty ranges dropped)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    edges = [(M * k) // (2 * world) for k in range(2 * world + 1)]
+    out = []
+    for c in (rank, 2 * world - 1 - rank):
+        b, e = edges[c], edges[c + 1]
+        if e > b:
+            out.append((b, e))
+    return sorted(out)
+
+
+def prefill_rows(cfg, Q, K, V, block_cnt, block_idx, O, ranges, prefill=None):
+    """Attention for the given block-row ranges only (other rows of O untouched)."""
+    if prefill is None:
+        from . import _lib
+
+        prefill = _lib.prefill
+    for b, e in ranges:
+        prefill(cfg.replace(row_begin=b, row_end=e), Q, K, V, block_cnt, block_idx, O)
+    return O
+
+
+def row_work_share(block_cnt_full: torch.Tensor, world: int) -> list[float]:
+    """Executed (head, row, block) units per rank under zig-zag row sharding, as fractions."""
+    per_row = block_cnt_full.double().sum(dim=0)
+    tot = float(per_row.sum())
+    M = per_row.numel()
+    return [sum(float(per_row[b:e].sum()) for b, e in zigzag_rows(M, world, r)) / tot
+            for r in range(world)]

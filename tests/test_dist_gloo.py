@@ -158,3 +158,80 @@ def test_work_share_sums_to_one():
     cnt = torch.randint(1, 10, (32, 16))
     s = shard.work_share(cnt, 8, 4)
     assert len(s) == 4 and abs(sum(s) - 1) < 1e-12
+
+
+# ----------------------------------------------------------- zig-zag row sharding --
+def test_zigzag_rows_cover_exactly_once_and_balance_linear_rows():
+    for M in (16, 1000, 1024, 2048, 7):
+        for P in (1, 2, 4, 8):
+            if 2 * P > M:
+                continue
+            seen = np.zeros(M, int)
+            loads = []
+            for r in range(P):
+                rr = shard.zigzag_rows(M, P, r)
+                assert len(rr) <= 2
+                load = 0
+                for b, e in rr:
+                    seen[b:e] += 1
+                    load += sum(m + 1 for m in range(b, e))       # K_{h,m} ~ (m+1) (Z12)
+                loads.append(load)
+            assert np.all(seen == 1)
+            if M >= 64:
+                assert max(loads) / (sum(loads) / P) < 1.02, (M, P, loads)
+
+
+def test_zigzag_balance_on_bimodal_budgets_vs_head_sharding():
+    # bimodal per-head budgets (the calibrated generator's, recorded in scripts/union_stats.py)
+    ks = [3, 5, 84, 340, 3, 3, 121, 143, 3, 3, 3, 4, 3, 3, 178, 208,
+          3, 244, 468, 634, 3, 80, 91, 665, 3, 159, 514, 615, 3, 3, 5, 638]
+    M = 1024
+    m = np.arange(M)
+    cnt = torch.tensor(np.minimum(m + 1, np.maximum(-(-np.outer(ks, m + 1) // M), 1)))
+    rows = shard.row_work_share(cnt, 8)
+    heads = shard.work_share(cnt, 8, 8)
+    assert max(rows) * 8 < 1.02          # zig-zag: balanced
+    assert max(heads) * 8 > 1.8          # head sharding: the densest kv head dominates
+
+
+def _rows_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oc = oracle.Cfg(4, 2, 16, 1024, 64, 4, 1, 0.9, round_bf16=True)
+        Q, K, V, _ = workloads.structured(4, 2, 1024, 16, seed=5, dtype=torch.bfloat16)
+        Qf, Kf, Vf = Q.float().numpy(), K.float().numpy(), V.float().numpy()
+        est = oracle.estimate(oc, Qf, Kf)                    # replicated estimate
+        O = torch.zeros(4, 1024, 16, dtype=torch.float64)
+
+        def prefill(cfg, Q_, K_, V_, cnt, idx, O_):          # oracle op, rows [b, e) only
+            items = [(h, m) for h in range(4) for m in range(cfg.row_begin, cfg.row_end)]
+            Oh = oracle.attention(oc, Qf, Kf, Vf, cnt, idx, items=items)
+            for h, m in items:
+                O_[h, m * 64:(m + 1) * 64] = torch.from_numpy(Oh[h, m * 64:(m + 1) * 64])
+
+        cfg = Config(4, 2, 16, 1024, 64, 4, 1, 0.9)
+        shard.prefill_rows(cfg, None, None, None, est["block_cnt"], est["block_idx"], O,
+                           shard.zigzag_rows(oc.M, world, rank), prefill=prefill)
+        dist.all_reduce(O)                                    # disjoint rows: sum == gather
+        if rank == 0:
+            q.put(O.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zigzag_sharded_attention_equals_unsharded_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    O = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    oc = oracle.Cfg(4, 2, 16, 1024, 64, 4, 1, 0.9, round_bf16=True)
+    Q, K, V, _ = workloads.structured(4, 2, 1024, 16, seed=5, dtype=torch.bfloat16)
+    ref = oracle.pipeline(oc, Q.float().numpy(), K.float().numpy(), V.float().numpy())["O"]
+    assert np.max(np.abs(O - ref)) == 0.0

@@ -352,3 +352,22 @@ def test_variant_fp32_debug_designated_config_a():
     ok = est["budget_margin"] > MARGIN
     assert np.array_equal(ks[ok], est["kstar"][ok])
     check_masks(oc, est["L"], ks, cnt, idx)
+
+
+def test_row_range_prefill_matches_full_bitwise():
+    # zig-zag row sharding building block: rows [b, e) only, other rows untouched
+    from paper_2509_24745_b200 import shard
+    cfg = llama_small(N=4096)
+    Q, K, V, _ = workloads.structured(8, 2, 4096, 128, seed=12)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    _, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    full = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    for world in (2, 3):
+        O = torch.zeros_like(full)
+        for rank in range(world):
+            shard.prefill_rows(cfg, Qd, Kd, Vd, cnt, idx, O, shard.zigzag_rows(cfg.M, world, rank))
+        assert torch.equal(O, full)
+    part = torch.zeros_like(full)
+    pa.prefill(cfg.replace(row_begin=5, row_end=12), Qd, Kd, Vd, cnt, idx, part)
+    assert torch.equal(part[:, 5 * 128:12 * 128], full[:, 5 * 128:12 * 128])
+    assert torch.all(part[:, :5 * 128] == 0) and torch.all(part[:, 12 * 128:] == 0)
