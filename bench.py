@@ -379,7 +379,8 @@ def run_ours(args):
     pk = peaks()
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops_exec / (att_m * 1e-3) / 1e12
-    kname = "attn_tc4_kernel" if os.environ.get("PROXYATTN_ATTN", "3").startswith("4") else "attn_tc_kernel"
+    kname = {"3": "attn_tc_kernel", "4": "attn_tc4_kernel", "5": "attn_tc5_kernel",
+             "6": "attn_tc6_kernel"}.get(os.environ.get("PROXYATTN_ATTN", "6")[:1], "attn_tc6_kernel")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):

@@ -98,16 +98,18 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
 }  // namespace
 
 namespace pa {
-// A7 kernel variant: 3 = attn_tc (two query-row slots per CTA sharing K/V tiles; default,
-// measured fastest), 4 = attn_tc4 (double-buffered S, column-split softmax).
-// PROXYATTN_ATTN=3|4 overrides the default.
-int attn_variant() {
+// A7 kernel variant.  Sparse prefill: 6 = attn_tc6 (one row per CTA, key blocks in two
+// independent even/odd streams; default, measured fastest), 3 = attn_tc (two rows per CTA
+// sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3 (full lists make the two-row
+// union free and K/V shared; measured fastest).  PROXYATTN_ATTN=3..6 overrides both.
+int attn_variant(bool dense) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("PROXYATTN_ATTN");
-        v = (e && e[0] == '4') ? 4 : (e && e[0] == '5') ? 5 : 3;
+        v = (e && e[0] >= '3' && e[0] <= '6') ? e[0] - '0' : 0;
     }
-    return v;
+    if (v) return v;
+    return dense ? 3 : 6;
 }
 }  // namespace pa
 
@@ -259,12 +261,15 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32) {
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
-        if (pa::attn_variant() != 3 && (D.N % D.b || D.rb != 0 || D.re != D.M))
+        const int variant = pa::attn_variant(block_cnt == nullptr);
+        if ((variant == 4 || variant == 5) && (D.N % D.b || D.rb != 0 || D.re != D.M))
             return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0 and all rows");
-        if (pa::attn_variant() == 4)
+        if (variant == 4)
             PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
-        else if (pa::attn_variant() == 5)
+        else if (variant == 5)
             PA_CUDA(pa::launch_attn_tc5(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc5");
+        else if (variant == 6)
+            PA_CUDA(pa::launch_attn_tc6(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc6");
         else
             PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
     }
