@@ -380,7 +380,8 @@ def run_ours(args):
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops_exec / (att_m * 1e-3) / 1e12
     kname = {"3": "attn_tc_kernel", "4": "attn_tc4_kernel", "5": "attn_tc5_kernel",
-             "6": "attn_tc6_kernel"}.get(os.environ.get("PROXYATTN_ATTN", "6")[:1], "attn_tc6_kernel")
+             "6": "attn_tc6_kernel", "7": "attn_tc7_kernel"}.get(
+                 os.environ.get("PROXYATTN_ATTN", "7")[:1], "attn_tc7_kernel")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):

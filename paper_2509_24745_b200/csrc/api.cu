@@ -98,18 +98,19 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
 }  // namespace
 
 namespace pa {
-// A7 kernel variant.  Sparse prefill: 6 = attn_tc6 (one row per CTA, key blocks in two
-// independent even/odd streams; default, measured fastest), 3 = attn_tc (two rows per CTA
-// sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3 (full lists make the two-row
-// union free and K/V shared; measured fastest).  PROXYATTN_ATTN=3..6 overrides both.
+// A7 kernel variant.  Sparse prefill: 7 = attn_tc7 (one row per CTA, two key-block
+// streams sharing one O under a fixed per-row softmax reference; default, measured fastest),
+// 6 = attn_tc6 (two independent streams with online rescaling), 3 = attn_tc (two rows per CTA
+// sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3 unless measured otherwise.
+// PROXYATTN_ATTN=3..7 overrides both.
 int attn_variant(bool dense) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("PROXYATTN_ATTN");
-        v = (e && e[0] >= '3' && e[0] <= '6') ? e[0] - '0' : 0;
+        v = (e && e[0] >= '3' && e[0] <= '7') ? e[0] - '0' : 0;
     }
     if (v) return v;
-    return dense ? 3 : 6;
+    return dense ? 3 : 7;
 }
 }  // namespace pa
 
@@ -270,6 +271,8 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
             PA_CUDA(pa::launch_attn_tc5(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc5");
         else if (variant == 6)
             PA_CUDA(pa::launch_attn_tc6(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc6");
+        else if (variant == 7)
+            PA_CUDA(pa::launch_attn_tc7(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc7");
         else
             PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
     }

@@ -56,11 +56,12 @@ struct __align__(8) Bars6 {
 
 constexpr size_t kSmemBytes = 1024 + kTile * (1 + kKStages + kVStages) + sizeof(Bars6);
 
+template <int kEmu>   // of every 8 key-column pairs, kEmu use the FMA-pipe exp2 (ex2_poly2)
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-                int r, float scale_log2, int row_lo, int row_hi) {
+                int r, float scale_log2, int row_lo, int row_hi, long long* trace, int trace_bid) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -174,10 +175,13 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const int st = j % kVStages;
             const uint32_t tP = tbase + s * 128;
             const uint32_t tO = tbase + 256 + s * 128;
+            long long* tr = (trace && blockIdx.x == trace_bid && j < 512 && leader) ? trace + j * 8 : nullptr;
+            if (tr) tr[0] = clock64();                             // MMA: start waiting for V, P
             mbar_wait(&bars->v_full[st], (j / kVStages) & 1);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 mbar_wait(&bars->p_half[s][half], js & 1);
+                if (tr) tr[1 + half] = clock64();                  // MMA: P half ready
                 tc_fence_after();
                 if (leader) {
                     const uint64_t b0 = dv + (st * kTile >> 4);
@@ -196,6 +200,7 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             }
             __syncwarp();
             if (j + 2 < cnt) issue_s(j + 2);   // overwrites S_s = P_j after PV_j (in order)
+            if (tr) tr[3] = clock64();                             // MMA: PV + next S issued
         }
     } else {
         // ------------------------------------------------------------- softmax --
@@ -213,7 +218,11 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const int j = 2 * js + s;
             const int n = n_next;
             if (js + 1 < my_cnt) n_next = list ? __ldg(list + j + 2) : j + 2;
+            long long* tr = (trace && blockIdx.x == trace_bid && lane == 0 && quarter == 2 && js < 256)
+                                ? trace + 512 * 8 + (js * 2 + s) * 8 : nullptr;
+            if (tr) tr[0] = clock64();                             // SM: start waiting for S
             mbar_wait(&bars->s_full[s], js & 1);
+            if (tr) tr[1] = clock64();                             // SM: S ready
             tc_fence_after();
             uint32_t raw[4][32];
 #pragma unroll
@@ -245,6 +254,7 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 m_used = m_new;
                 l *= factor;
             }
+            if (tr) tr[2] = clock64();                             // SM: S loaded + row max
             const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
             const uint64_t nm2 = f2_pack(-m_used, -m_used);
             uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
@@ -257,15 +267,23 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
                                                        __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
                                                sc2, nm2);
-                    float x0, x1;
-                    f2_unpack(x2, x0, x1);
-                    const float p0 = ex2(x0), p1 = ex2(x1);
+                    float p0, p1;
+                    if ((c & 7) < kEmu) {
+                        ex2_poly2(x2, p0, p1);
+                    } else {
+                        float x0, x1;
+                        f2_unpack(x2, x0, x1);
+                        p0 = ex2(x0);
+                        p1 = ex2(x1);
+                    }
                     ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
                     pk[c] = pack_bf16(p0, p1);
                 }
+                if (tr) tr[5 + half] = clock64();                  // SM: exps of this half done
                 tmem_st32(tS + half * 32, pk);
                 if (half == 0 && js > 0) {
                     mbar_wait(&bars->o_done[s], (js - 1) & 1);   // PV of the stream's previous block
+                    if (tr) tr[7] = clock64();                     // SM: O ready for correction
                     tc_fence_after();
                     if (any) {
 #pragma unroll
@@ -283,6 +301,7 @@ attn_tc6_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&bars->p_half[s][half]);
+                if (tr) tr[3 + half] = clock64();                  // SM: P half released
             }
             {
                 const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
@@ -353,18 +372,37 @@ cudaError_t launch_attn_tc6(const Dims& D, const void* Q, const void* K, const v
         !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
         !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
         return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(attn_tc6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static int emu = -1;
+    if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe
+        const char* e = getenv("PROXYATTN_EXP_EMU");
+        emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
+    }
+    auto kern = emu == 0 ? attn_tc6_kernel<0> : emu == 1 ? attn_tc6_kernel<1>
+              : emu == 2 ? attn_tc6_kernel<2> : emu == 3 ? attn_tc6_kernel<3> : attn_tc6_kernel<4>;
+    static bool attr_set[5] = {false, false, false, false, false};
+    if (!attr_set[emu]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kSmemBytes));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[emu] = true;
     }
+    // PROXYATTN_TRACE=<cta>: per-event clock64 timeline of one CTA (diagnostics only), read
+    // back with proxyattn_debug_trace(): [512 j][8] MMA events, then [256 js][2 s][8] softmax.
+    constexpr size_t kTraceBytes = 2 * 512 * 8 * sizeof(long long);
+    static long long* trace = nullptr;
+    static int trace_bid = -1;
+    if (trace_bid < 0) {
+        const char* e = getenv("PROXYATTN_TRACE");
+        trace_bid = e ? atoi(e) : 1 << 30;
+        if (e && cudaMalloc(&trace, kTraceBytes) != cudaSuccess) trace = nullptr;
+    }
+    if (trace) cudaMemsetAsync(trace, 0, kTraceBytes, st);
+    attn_trace_ptr() = trace;
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
     const unsigned grid = static_cast<unsigned>(D.Hl) * static_cast<unsigned>(D.re - D.rb);
-    attn_tc6_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, static_cast<__nv_bfloat16*>(O),
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, static_cast<__nv_bfloat16*>(O),
                                                         block_cnt, block_idx, static_cast<int>(D.N),
-                                                        D.M, D.r, scale_log2, D.rb, D.re);
+                                                        D.M, D.r, scale_log2, D.rb, D.re, trace, trace_bid);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,4 @@
+export PROXYATTN_ATTN=7
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout=600 -p no:faulthandler 2>&1 | tail -15
+for e in 2 1 3; do echo "emu $e $(PROXYATTN_EXP_EMU=$e timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e 2>/dev/null | tail -1 | python -c 'import sys,json; j=json.loads(sys.stdin.read()); print(round(j["value"],3), round(j["prefill_ms"],3), round(j["roofline"]["frac"],4))')"; done
+PYTHONPATH=. timeout 600 python scripts/trace_attn7.py 2>&1 | tail -30

@@ -375,3 +375,30 @@ def test_row_range_prefill_matches_full_bitwise():
     pa.prefill(cfg.replace(row_begin=5, row_end=12), Qd, Kd, Vd, cnt, idx, part)
     assert torch.equal(part[:, 5 * 128:12 * 128], full[:, 5 * 128:12 * 128])
     assert torch.all(part[:, :5 * 128] == 0) and torch.all(part[:, 12 * 128:] == 0)
+
+
+def test_score_spikes_wide_dynamic_range():
+    # Keys whose scores jump far above (and below) the first blocks' maxima: the softmax
+    # reference of attn_tc7 is fixed per row (shift invariance of softmax), so
+    # these exercise its large-P fast path (+20 in log2 units) and its exact second pass
+    # (+80: the reference is replaced by the row's true max).  Head 3 sees the spikes negated.
+    cfg = llama_small(N=2048, gamma=1.0, heads=(4, 1))
+    g = torch.Generator().manual_seed(21)
+    Q = (torch.randn(4, 2048, 128, generator=g) * 0.5 + 0.5)
+    Q[3] = -Q[3]
+    K = torch.randn(1, 2048, 128, generator=g) * 0.5
+    V = torch.randn(1, 2048, 128, generator=g)
+    K[0, 7 * 128 + 5] = 2.5                                   # ~ +20 log2 over the reference
+    K[0, 9 * 128 + 77] = 10.0                                 # ~ +80: second pass
+    K[0, 12 * 128 + 1] = -20.0                                # far below: underflows to 0
+    Q, K, V = Q.bfloat16(), K.bfloat16(), V.bfloat16()
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    _, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    assert torch.all(cnt.cpu() == torch.arange(1, 17, dtype=torch.int32))
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    assert torch.isfinite(O.float()).all()
+    ref = oracle.attention(ocfg_of(cfg), np32(Q), np32(K), np32(V), cnt.cpu().numpy(),
+                           idx.cpu().numpy())
+    check_out(O, ref, fp32=False)
+    Od = pa.dense_prefill(cfg, Qd, Kd, Vd)
+    check_out(Od, ref, fp32=False)
