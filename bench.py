@@ -76,17 +76,61 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled every 5 ms
+    from a thread (nvidia-smi -lms 100 as the fallback when NVML is unavailable)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    NVML_BITS = [0x8, 0x40, 0x20, 0x4]      # nvmlClocksEventReason* of the NAMES above
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.rows = []
+
+    def _nvml_handle(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            import torch
+
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, nv, h):
+        import threading
+        import time
+
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                bits = int(get_reasons(h))
+                self.rows.append((sm, mx, ["Active" if bits & b else "Not Active" for b in self.NVML_BITS]))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        import threading
+
+        try:
+            nv, h = self._nvml_handle()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -98,30 +142,35 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.result = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
-        if self.proc is None:
-            return
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out = ""
-        rows = []
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
+        rows = self.rows
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
+            source = "nvml"
+        elif self.proc is not None:
+            source = "nvidia-smi"
+            self.proc.terminate()
             try:
-                rows.append((float(f[0]), float(f[1]), f[3:7]))
-            except ValueError:
-                pass
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            for line in out.strip().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[3:7]))
+                except ValueError:
+                    pass
+        else:
+            return
         if not rows:
             return
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
+        reasons = sorted({self.NAMES[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
         sm = [r[0] for r in rows]
         self.result = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": rows[0][1],
-                       "samples": len(rows), "reasons": reasons}
+                       "samples": len(rows), "source": source, "reasons": reasons}
 
 
 def build_config(pa, rank: int, ws: int, w=WORKLOAD, sharding="rows"):
@@ -380,8 +429,8 @@ def run_ours(args):
     peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     achieved = flops_exec / (att_m * 1e-3) / 1e12
     kname = {"3": "attn_tc_kernel", "4": "attn_tc4_kernel", "5": "attn_tc5_kernel",
-             "6": "attn_tc6_kernel", "7": "attn_tc7_kernel"}.get(
-                 os.environ.get("PROXYATTN_ATTN", "7")[:1], "attn_tc7_kernel")
+             "6": "attn_tc6_kernel", "7": "attn_tc7_kernel", "8": "attn_tc8_kernel"}.get(
+                 os.environ.get("PROXYATTN_ATTN", "8")[:1], "attn_tc8_kernel")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
@@ -429,7 +478,10 @@ def run_ours(args):
         "work_share": [x / total_blocks for x in per_rank_blocks],
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (ESTIMATE_KERNELS + len(my_rows)) * args.steps,
+        # attn_tc8 is two launches per prefill call: the fast pass and the exact re-run of
+        # the rows it flagged (an empty list at these inputs)
+        "gpu_launches": (ESTIMATE_KERNELS + len(my_rows) * (2 if kname == "attn_tc8_kernel" else 1))
+                        * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -98,19 +98,20 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
 }  // namespace
 
 namespace pa {
-// A7 kernel variant.  Sparse prefill: 7 = attn_tc7 (one row per CTA, two key-block
-// streams sharing one O under a fixed per-row softmax reference; default, measured fastest),
-// 6 = attn_tc6 (two independent streams with online rescaling), 3 = attn_tc (two rows per CTA
-// sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3 unless measured otherwise.
-// PROXYATTN_ATTN=3..7 overrides both.
+// A7 kernel variant.  Sparse prefill: 8 = attn_tc8 (persistent attn_tc7: rows pulled from
+// an atomic counter, next row's loads/S/softmax overlapping the previous row's tail; default),
+// 7 = attn_tc7 (one row per CTA, two key-block streams sharing one O under a fixed per-row
+// softmax reference), 6 = attn_tc6 (two independent streams with online rescaling), 3 =
+// attn_tc (two rows per CTA sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3.
+// PROXYATTN_ATTN=3..8 overrides both.
 int attn_variant(bool dense) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("PROXYATTN_ATTN");
-        v = (e && e[0] >= '3' && e[0] <= '7') ? e[0] - '0' : 0;
+        v = (e && e[0] >= '3' && e[0] <= '8') ? e[0] - '0' : 0;
     }
     if (v) return v;
-    return dense ? 3 : 7;
+    return dense ? 3 : 8;
 }
 }  // namespace pa
 
@@ -273,6 +274,8 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
             PA_CUDA(pa::launch_attn_tc6(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc6");
         else if (variant == 7)
             PA_CUDA(pa::launch_attn_tc7(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc7");
+        else if (variant == 8)
+            PA_CUDA(pa::launch_attn_tc8(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc8");
         else
             PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
     }

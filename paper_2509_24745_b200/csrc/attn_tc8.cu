@@ -1,0 +1,603 @@
+// attn_tc8.cu — bf16 block-sparse causal prefill attention on tcgen05 (A7 / A8), variant v8:
+// the attn_tc7 pipeline (two key-block streams sharing one O under a fixed per-row softmax
+// reference, separate P buffers, S released right after tcgen05.ld) made PERSISTENT: one
+// CTA per SM pulls (head, block-row) items from an atomic counter, and the ring / barrier
+// phases run on across items, so the next row's Q/K loads, its first S MMAs and its softmax
+// overlap the previous row's last PVs and its epilogue (dedicated epilogue warps).  In
+// attn_tc7 that per-row prologue/epilogue cost ~5 us per CTA, ~8 % of the launch at 128K.
+//
+// Method: O[h][t] = sum over keys k of the selected blocks, k <= t, of
+// softmax(Q[h][t] K[kv(h)][k] / sqrt(d)) V[kv(h)][k],
+// evaluated as sum 2^(x - m_ref) V / sum 2^(x - m_ref) with m_ref the max of the row's two
+// first blocks (softmax is shift invariant).  A row on which some P would exceed 2^32 is
+// appended to a list during the fast launch (its output is then overwritten) and the exact
+// launch recomputes the listed rows with m_ref = the true row max (max-only sweep, then the
+// fixed pass), so the result never depends on the fast path's bound.
+//
+// Warp roles (512 threads, 4 warpgroups):
+//   warp 0      item scheduler (atomic counter) + TMA producer of Q and K (3-stage ring)
+//   warp 1      TMEM allocator + S issuer          warp 2   PV issuer
+//   warp 3      TMA producer of V (2-stage ring)
+//   warps 4-7   epilogue: O (TMEM) * 1/l -> bf16 -> global; releases O for the next row
+//   warps 8-11  softmax of stream 0, warps 12-15 of stream 1 (thread = row = TMEM lane)
+// TMEM (512 columns): O [0,128)  S_0 [128,256)  S_1 [256,384)  P_0 [384,448)  P_1 [448,512).
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace pa {
+namespace {
+
+constexpr int kTileRows = 128;
+constexpr int kBox = kTileRows * 64 * 2;   // 16 KB: [128 rows][64 bf16] SW128 box
+constexpr int kTile = 2 * kBox;            // 32 KB: a 128 x 128 bf16 tile
+constexpr int kKStages = 3;
+constexpr int kVStages = 2;
+constexpr int kItemSlots = 4;
+constexpr int kThreads = 512;
+constexpr float kOverflow = 32.0f;         // log2 headroom of P over the fast reference
+constexpr uint32_t kColO = 0, kColS = 128, kColP = 384;
+constexpr int kItemConsumers = 1 + 1 + 1 + 4 + 8;   // S, PV, V, epilogue warps, softmax warps
+
+struct Item {
+    int item;   // -1: no more work
+    int cnt;
+};
+
+struct __align__(8) Bars8 {
+    uint64_t q_full, q_empty;
+    uint64_t k_full[kKStages];
+    uint64_t k_empty[kKStages];
+    uint64_t v_full[kVStages];
+    uint64_t v_empty[kVStages];
+    uint64_t s_full[2];
+    uint64_t s_free[2];
+    uint64_t p_full[2][2];   // [stream][half]
+    uint64_t p_free[2];
+    uint64_t o_final, o_free;
+    uint64_t l_ready[2];     // per item parity: both streams' row sums written
+    uint64_t item_full[kItemSlots];
+    uint64_t item_empty[kItemSlots];
+    Item items[kItemSlots];
+    uint32_t tmem_base;
+    float red[2][128];       // first-block / true row max exchange between the streams
+    float lsum[2][2][128];   // [item parity][stream][row] row sums for the epilogue
+};
+
+constexpr size_t kSmemBytes = 1024 + kTile * (1 + kKStages + kVStages) + sizeof(Bars8);
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct Sched {        // device-side scheduler state of one launch pair (zeroed before launch)
+    int next[2];      // item counters of the fast and the exact launch
+    int n_flagged;    // rows appended by the fast launch
+    int pad;
+};
+
+template <int kEmu>   // of every 8 key-column pairs, kEmu use the FMA-pipe exp2 (ex2_poly2)
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
+                const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
+                int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
+                int* flagged, int exact) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = smem + kTile;
+    uint8_t* sV = smem + kTile * (1 + kKStages);
+    Bars8* bars = reinterpret_cast<Bars8*>(smem + kTile * (1 + kKStages + kVStages));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nrows = row_hi - row_lo;
+    const int per_kv = r * nrows;
+    const int n_items = exact ? sched->n_flagged : n_total;
+    const bool dense = (block_cnt == nullptr);
+    const int passes = exact ? 2 : 1;   // exact: max sweep, then the fixed pass
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->q_full, 1);
+        mbar_init(&bars->q_empty, 1);
+        for (int s = 0; s < kKStages; ++s) {
+            mbar_init(&bars->k_full[s], 1);
+            mbar_init(&bars->k_empty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            mbar_init(&bars->v_full[s], 1);
+            mbar_init(&bars->v_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->s_free[s], 128);
+            mbar_init(&bars->p_full[s][0], 128);
+            mbar_init(&bars->p_full[s][1], 128);
+            mbar_init(&bars->p_free[s], 1);
+            mbar_init(&bars->l_ready[s], 256);
+        }
+        mbar_init(&bars->o_final, 1);
+        mbar_init(&bars->o_free, 128);
+        for (int i = 0; i < kItemSlots; ++i) {
+            mbar_init(&bars->item_full[i], 1);
+            mbar_init(&bars->item_empty[i], kItemConsumers);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = bars->tmem_base;
+
+    // item decode (same order as attn_tc7's grid: kv-head major, heavy rows first)
+    auto decode = [&](int item, int& hl, int& m, int& kvl) {
+        kvl = item / per_kv;
+        const int rem = item % per_kv;
+        m = row_hi - 1 - rem / r;
+        hl = kvl * r + rem % r;
+    };
+    auto get_item = [&](int it) -> Item {         // consumers: wait for slot, read, release
+        const int slot = it % kItemSlots;
+        mbar_wait(&bars->item_full[slot], (it / kItemSlots) & 1);
+        const Item x = bars->items[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->item_empty[slot]);
+        return x;
+    };
+    auto list_of = [&](int hl, int m) -> const int* {
+        return dense ? nullptr : block_idx + (static_cast<long long>(hl) * M + m) * M;
+    };
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+        if (warp == 0) {
+            // ---------------------------------------- scheduler + Q/K producer --
+            if (lane == 0) {
+                tma_prefetch(&tmQ);
+                tma_prefetch(&tmK);
+                int gk = 0;
+                for (int it = 0;; ++it) {
+                    const int slot = it % kItemSlots;
+                    if (it >= kItemSlots) mbar_wait(&bars->item_empty[slot], ((it / kItemSlots) - 1) & 1);
+                    int k = atomicAdd(&sched->next[exact], 1);
+                    Item x{-1, 0};
+                    if (k < n_items) {
+                        x.item = exact ? flagged[k] : k;
+                        int hl, m, kvl;
+                        decode(x.item, hl, m, kvl);
+                        x.cnt = dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(hl) * M + m);
+                    }
+                    bars->items[slot] = x;
+                    mbar_arrive(&bars->item_full[slot]);   // release semantics publish x
+                    if (x.item < 0) break;
+                    int hl, m, kvl;
+                    decode(x.item, hl, m, kvl);
+                    const int* list = list_of(hl, m);
+                    if (it > 0) mbar_wait(&bars->q_empty, (it - 1) & 1);   // last S of it-1 done
+                    const int qrow = hl * N + m * kTileRows;
+                    mbar_expect_tx(&bars->q_full, kTile);
+                    tma_load_2d(sQ, &tmQ, &bars->q_full, 0, qrow);
+                    tma_load_2d(sQ + kBox, &tmQ, &bars->q_full, 64, qrow);
+                    for (int pass = 0; pass < passes; ++pass) {
+                        for (int j = 0; j < x.cnt; ++j, ++gk) {
+                            const int st = gk % kKStages;
+                            if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
+                            const int n = dense ? j : __ldg(list + j);
+                            const int krow = kvl * N + n * kTileRows;
+                            mbar_expect_tx(&bars->k_full[st], kTile);
+                            tma_load_2d(sK + st * kTile, &tmK, &bars->k_full[st], 0, krow);
+                            tma_load_2d(sK + st * kTile + kBox, &tmK, &bars->k_full[st], 64, krow);
+                        }
+                    }
+                }
+            }
+        } else if (warp == 3) {
+            // ------------------------------------------------------- V producer --
+            if (lane == 0) tma_prefetch(&tmV);
+            int gv = 0;
+            for (int it = 0;; ++it) {
+                const Item x = get_item(it);
+                if (x.item < 0) break;
+                if (lane == 0) {
+                    int hl, m, kvl;
+                    decode(x.item, hl, m, kvl);
+                    const int* list = list_of(hl, m);
+                    for (int j = 0; j < x.cnt; ++j, ++gv) {
+                        const int st = gv % kVStages;
+                        if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
+                        const int n = dense ? j : __ldg(list + j);
+                        const int vrow = kvl * N + n * kTileRows;
+                        mbar_expect_tx(&bars->v_full[st], kTile);
+                        tma_load_2d(sV + st * kTile, &tmV, &bars->v_full[st], 0, vrow);
+                        tma_load_2d(sV + st * kTile + kBox, &tmV, &bars->v_full[st], 64, vrow);
+                    }
+                }
+                __syncwarp();
+            }
+        } else if (warp == 1) {
+            // -------------------------------------------------------- S issuer --
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+            const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+            const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
+            const bool leader = elect_one();
+            int gk = 0, gs[2] = {0, 0};
+            for (int it = 0;; ++it) {
+                const Item x = get_item(it);
+                if (x.item < 0) break;
+                mbar_wait(&bars->q_full, it & 1);
+                for (int pass = 0; pass < passes; ++pass) {
+                    for (int j = 0; j < x.cnt; ++j, ++gk) {
+                        const int s = j & 1;
+                        if (gs[s] > 0) mbar_wait(&bars->s_free[s], (gs[s] - 1) & 1);
+                        ++gs[s];
+                        const int st = gk % kKStages;
+                        mbar_wait(&bars->k_full[st], (gk / kKStages) & 1);
+                        tc_fence_after();
+                        if (leader) {
+                            const uint64_t b0 = dk + (st * kTile >> 4);
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk) {
+                                const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
+                                umma_ss(tbase + kColS + s * 128, dq + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
+                            }
+                            tc_commit(&bars->k_empty[st]);
+                            tc_commit(&bars->s_full[s]);
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (leader) tc_commit(&bars->q_empty);   // Q may be replaced by the next row's
+                __syncwarp();
+            }
+        } else {
+            // ------------------------------------------------------- PV issuer --
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+            const uint64_t dv = sdesc_sw128(smem_u32(sV), kBox, 1024);
+            const bool leader = elect_one();
+            int gv = 0, gp[2] = {0, 0};
+            for (int it = 0;; ++it) {
+                const Item x = get_item(it);
+                if (x.item < 0) break;
+                for (int j = 0; j < x.cnt; ++j, ++gv) {
+                    const int s = j & 1;
+                    const int st = gv % kVStages;
+                    mbar_wait(&bars->v_full[st], (gv / kVStages) & 1);
+                    if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);   // O read out
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        mbar_wait(&bars->p_full[s][half], gp[s] & 1);
+                        tc_fence_after();
+                        if (leader) {
+                            const uint64_t b0 = dv + (st * kTile >> 4);
+#pragma unroll
+                            for (int k4 = 0; k4 < 4; ++k4) {
+                                const int kk = half * 4 + k4;
+                                umma_ts(tbase + kColO, tbase + kColP + s * 64 + kk * 8,
+                                        b0 + (kk * 2048 >> 4), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    ++gp[s];
+                    if (leader) {
+                        tc_commit(&bars->v_empty[st]);
+                        tc_commit(&bars->p_free[s]);
+                    }
+                    __syncwarp();
+                }
+                if (leader) tc_commit(&bars->o_final);
+                __syncwarp();
+            }
+        }
+    } else if (warp < 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+        // ------------------------------------------------------------- epilogue --
+        const int quarter = warp & 3;
+        const int rr = quarter * 32 + lane;
+        const uint32_t tO = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + kColO;
+        for (int it = 0;; ++it) {
+            const Item x = get_item(it);
+            if (x.item < 0) break;
+            int hl, m, kvl;
+            decode(x.item, hl, m, kvl);
+            mbar_wait(&bars->l_ready[it & 1], (it >> 1) & 1);
+            const float l0 = bars->lsum[it & 1][0][rr], l1 = bars->lsum[it & 1][1][rr];
+            const float inv = 1.f / (l0 + l1);
+            if (!exact) {   // a row whose P exceeded the bound (l = +inf marker): exact re-run
+                const bool bad = !(l0 + l1 <= 2.f * exp2f(kOverflow));
+                if (__any_sync(0xffffffffu, bad) && lane == 0)
+                    flagged[atomicAdd(&sched->n_flagged, 1)] = x.item;   // <= 4 duplicates, benign
+            }
+            mbar_wait(&bars->o_final, it & 1);
+            tc_fence_after();
+            const bool row_valid = static_cast<long long>(m) * kTileRows + rr < N;
+            uint4* dst = reinterpret_cast<uint4*>(
+                O + (static_cast<long long>(hl) * N + static_cast<long long>(m) * kTileRows + rr) * 128);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t o[2][32];
+                tmem_ld32(tO + h2 * 64, o[0]);
+                tmem_ld32(tO + h2 * 64 + 32, o[1]);
+                tmem_ld_wait();
+                if (h2 == 1) {
+                    tc_fence_before();
+                    mbar_arrive(&bars->o_free);           // the next row's PV may overwrite O
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t pkd[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        pkd[e] = pack_bf16(__uint_as_float(o[c][2 * e]) * inv,
+                                           __uint_as_float(o[c][2 * e + 1]) * inv);
+                    if (row_valid) {
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            dst[h2 * 8 + c * 4 + v] =
+                                make_uint4(pkd[4 * v], pkd[4 * v + 1], pkd[4 * v + 2], pkd[4 * v + 3]);
+                    }
+                }
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 184;\n" ::: "memory");
+        // -------------------------------------------------------------- softmax --
+        const int s = (warp - 8) >> 2;                  // stream
+        const int quarter = warp & 3;
+        const int rr = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t tS = tbase + lane_off + kColS + s * 128;
+        const uint32_t tP = tbase + lane_off + kColP + s * 64;
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+        int gs = 0, gp = 0;                             // this stream's S / P counters
+        float xhi = -INFINITY;
+
+        auto p_chunk = [&](const uint32_t (&x)[32], uint64_t nm2, uint64_t (&ls)[4], uint32_t tdst,
+                           bool wait_free) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int p = 0; p < 16; ++p) {
+                const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(x[2 * p]), __uint_as_float(x[2 * p + 1])),
+                                           sc2, nm2);
+                float p0, p1;
+                if ((p & 7) < kEmu) {
+                    float x0, x1;
+                    f2_unpack(x2, x0, x1);
+                    xhi = fmaxf(xhi, fmaxf(x0, x1));      // the poly wraps for x >= 128
+                    ex2_poly2(x2, p0, p1);
+                } else {
+                    float x0, x1;
+                    f2_unpack(x2, x0, x1);
+                    p0 = ex2(x0);
+                    p1 = ex2(x1);
+                }
+                ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
+                pk[p] = pack_bf16(p0, p1);
+            }
+            if (wait_free && gp > 0) {                   // the previous PV has read P_s
+                mbar_wait(&bars->p_free[s], (gp - 1) & 1);
+                tc_fence_after();
+            }
+            tmem_st16(tdst, pk);
+        };
+        auto mask_chunk = [&](uint32_t (&x)[32], int c) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+                if (c * 32 + e > rr) x[e] = 0xff800000u;
+        };
+        auto release_p = [&](int half) {
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&bars->p_full[s][half]);
+        };
+        auto sum_ls = [&](uint64_t (&ls)[4]) {
+            const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
+            float a, b;
+            f2_unpack(t, a, b);
+            return a + b;
+        };
+        auto wait_s = [&]() {
+            mbar_wait(&bars->s_full[s], gs & 1);
+            ++gs;
+            tc_fence_after();
+        };
+        auto release_s = [&]() {
+            tc_fence_before();
+            mbar_arrive(&bars->s_free[s]);
+        };
+        // P of the block in S_s (already landed), with the reference known: chunked TMEM
+        // loads overlapped with the exp2s; S released once its last chunk is in registers
+        auto block_exps = [&](float m_ref, bool diag) -> float {
+            const uint64_t nm2 = f2_pack(-m_ref, -m_ref);
+            uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
+            uint32_t xa[32], xb[32];
+            tmem_ld32(tS, xa);
+            tmem_ld_wait_regs(xa);
+            tmem_ld32(tS + 32, xb);
+            if (diag) mask_chunk(xa, 0);
+            p_chunk(xa, nm2, ls, tP, true);
+            tmem_ld_wait_regs(xb);
+            tmem_ld32(tS + 64, xa);
+            if (diag) mask_chunk(xb, 1);
+            p_chunk(xb, nm2, ls, tP + 16, false);
+            release_p(0);
+            tmem_ld_wait_regs(xa);
+            tmem_ld32(tS + 96, xb);
+            if (diag) mask_chunk(xa, 2);
+            p_chunk(xa, nm2, ls, tP + 32, false);
+            tmem_ld_wait_regs(xb);
+            release_s();
+            if (diag) mask_chunk(xb, 3);
+            p_chunk(xb, nm2, ls, tP + 48, false);
+            release_p(1);
+            ++gp;
+            return sum_ls(ls);
+        };
+        // row max of the block in S_s (raw logits), chunked; S stays in TMEM
+        auto block_max = [&](bool diag) -> float {
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            uint32_t xa[32], xb[32];
+            auto fold = [&](uint32_t (&x)[32], int c) {
+                if (diag) mask_chunk(x, c);
+#pragma unroll
+                for (int e = 0; e < 32; e += 2)
+                    mx[(e >> 1) & 3] = fmaxf(mx[(e >> 1) & 3], fmaxf(__uint_as_float(x[e]), __uint_as_float(x[e + 1])));
+            };
+            tmem_ld32(tS, xa);
+            tmem_ld_wait_regs(xa);
+            tmem_ld32(tS + 32, xb);
+            fold(xa, 0);
+            tmem_ld_wait_regs(xb);
+            tmem_ld32(tS + 64, xa);
+            fold(xb, 1);
+            tmem_ld_wait_regs(xa);
+            tmem_ld32(tS + 96, xb);
+            fold(xa, 2);
+            tmem_ld_wait_regs(xb);
+            fold(xb, 3);
+            return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        };
+        auto exchange_max = [&](float v) {
+            bars->red[s][rr] = v;
+            softmax_bar();
+            const float r2 = fmaxf(bars->red[0][rr], bars->red[1][rr]) * scale_log2;
+            softmax_bar();
+            return r2;
+        };
+
+        for (int it = 0;; ++it) {
+            const Item x = get_item(it);
+            if (x.item < 0) break;
+            int hl, m, kvl;
+            decode(x.item, hl, m, kvl);
+            const int* list = list_of(hl, m);
+            const int my_cnt = (x.cnt - s + 1) >> 1;   // blocks j = s, s + 2, ...
+            auto block_n = [&](int js) { return dense ? 2 * js + s : __ldg(list + 2 * js + s); };
+            float l = 0.f;
+            float m_ref;
+            if (!exact) {
+                // reference = max of the two streams' first blocks (read twice from TMEM)
+                float rmax = -INFINITY;
+                const bool diag0 = (my_cnt > 0) && block_n(0) == m;
+                if (my_cnt > 0) {
+                    wait_s();
+                    rmax = block_max(diag0);
+                }
+                m_ref = exchange_max(rmax);
+                xhi = -INFINITY;
+                if (my_cnt > 0) l = block_exps(m_ref, diag0);
+                int n_next = (my_cnt > 1) ? block_n(1) : 0;
+                for (int js = 1; js < my_cnt; ++js) {
+                    const int n = n_next;
+                    if (js + 1 < my_cnt) n_next = block_n(js + 1);
+                    wait_s();
+                    l += block_exps(m_ref, n == m);
+                }
+                if (!(l <= exp2f(kOverflow)) || xhi > kOverflow) l = INFINITY;   // flag the row
+            } else {
+                // exact: the row's true max first (S only), then the fixed pass
+                float tmax = -INFINITY;
+                for (int js = 0; js < my_cnt; ++js) {
+                    wait_s();
+                    tmax = fmaxf(tmax, block_max(block_n(js) == m));
+                    release_s();
+                }
+                m_ref = exchange_max(tmax);
+                for (int js = 0; js < my_cnt; ++js) {
+                    wait_s();
+                    l += block_exps(m_ref, block_n(js) == m);
+                }
+            }
+            bars->lsum[it & 1][s][rr] = l;
+            mbar_arrive(&bars->l_ready[it & 1]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tbase, 512);
+    }
+}
+
+// Per-stream scheduler state + flagged-row list (grown on demand, never freed).
+struct SchedBuf {
+    Sched* sched = nullptr;
+    int* flagged = nullptr;
+    size_t cap = 0;
+};
+
+SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, SchedBuf> bufs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    SchedBuf& b = bufs[{dev, st}];
+    if (!b.sched && cudaMalloc(&b.sched, sizeof(Sched)) != cudaSuccess) return nullptr;
+    if (b.cap < 4 * n_items) {   // each row can be appended by up to 4 epilogue warps
+        if (b.flagged) cudaFree(b.flagged);
+        b.flagged = nullptr;
+        if (cudaMalloc(&b.flagged, 4 * n_items * sizeof(int)) != cudaSuccess) return nullptr;
+        b.cap = 4 * n_items;
+    }
+    return &b;
+}
+
+}  // namespace
+
+cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
+                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
+    CUtensorMap mq, mk, mv;
+    if (!make_map_bf16_sw128(&mq, Q, static_cast<uint64_t>(D.Hl) * D.N, 128, 128) ||
+        !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
+        !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
+        return cudaErrorInvalidValue;
+    static int emu = -1;
+    if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe
+        const char* e = getenv("PROXYATTN_EXP_EMU");
+        emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
+    }
+    auto kern = emu == 0 ? attn_tc8_kernel<0> : emu == 1 ? attn_tc8_kernel<1>
+              : emu == 2 ? attn_tc8_kernel<2> : emu == 3 ? attn_tc8_kernel<3> : attn_tc8_kernel<4>;
+    static bool attr_set[5] = {false, false, false, false, false};
+    if (!attr_set[emu]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kSmemBytes));
+        if (e != cudaSuccess) return e;
+        attr_set[emu] = true;
+    }
+    int dev = 0, n_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const size_t n_items = static_cast<size_t>(D.Hl) * static_cast<size_t>(D.re - D.rb);
+    SchedBuf* sb = sched_for(st, n_items);
+    if (!sb) return cudaErrorMemoryAllocation;
+    cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);
+    if (e != cudaSuccess) return e;
+    const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
+    // fast launch over every row, then the exact launch over the rows it flagged (usually
+    // none: its CTAs find an empty list and exit)
+    for (int exact = 0; exact < 2; ++exact) {
+        const int grid = exact ? n_sm : static_cast<int>(n_items < static_cast<size_t>(n_sm) ? n_items : n_sm);
+        kern<<<grid, kThreads, kSmemBytes, st>>>(
+            mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
+            D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace pa

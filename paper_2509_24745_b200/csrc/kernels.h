@@ -45,6 +45,8 @@ cudaError_t launch_attn_tc6(const Dims& D, const void* Q, const void* K, const v
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 cudaError_t launch_attn_tc7(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
+cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
+                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 long long*& attn_trace_ptr();
 // tcgen05 estimation (bf16, d = b = 128, s = 4): A2+A3 and A4 (see score_tc.cu).
 bool score_tc_supported(const Dims& D);
