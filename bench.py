@@ -104,33 +104,41 @@ class ClockSampler:
         except Exception:
             return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
-    def _poll(self, nv, h):
-        import threading
+    def _sample(self):
+        nv, h = self.nv, self.h
+        sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+        bits = int(self.get_reasons(h))
+        self.rows.append((sm, self.mx, ["Active" if bits & b else "Not Active" for b in self.NVML_BITS]))
+
+    def _poll(self):
         import time
 
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
         while not self.stop.is_set():
             try:
-                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                bits = int(get_reasons(h))
-                self.rows.append((sm, mx, ["Active" if bits & b else "Not Active" for b in self.NVML_BITS]))
-            except Exception:
-                pass
+                self._sample()
+            except Exception as e:      # keep polling; report the last error
+                self.error = repr(e)
             time.sleep(0.005)
 
     def __enter__(self):
         import threading
 
+        self.error = None
         try:
-            nv, h = self._nvml_handle()
+            self.nv, self.h = self._nvml_handle()
+            nv = self.nv
+            self.get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self._sample()                  # synchronous first sample: NVML is usable
             self.stop = threading.Event()
-            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
             return self
-        except Exception:
+        except Exception as e:
+            self.error = repr(e)
             self.thread = None
+            self.rows = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -146,6 +154,10 @@ class ClockSampler:
         if self.thread is not None:
             self.stop.set()
             self.thread.join(timeout=5)
+            try:
+                self._sample()              # and one at the end of the timed region
+            except Exception:
+                pass
             source = "nvml"
         elif self.proc is not None:
             source = "nvidia-smi"
@@ -164,8 +176,12 @@ class ClockSampler:
                 except ValueError:
                     pass
         else:
+            if self.error:
+                self.result["error"] = self.error
             return
         if not rows:
+            if self.error:
+                self.result["error"] = self.error
             return
         reasons = sorted({self.NAMES[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
         sm = [r[0] for r in rows]

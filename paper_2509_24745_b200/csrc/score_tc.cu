@@ -59,6 +59,8 @@ struct ScoreParams {
     float* part_s;
     const float* lse2;  // MAXPOOL: [gl][Ns] (log2 units)
     float* L;           // MAXPOOL: [gl][M][M] (natural log)
+    float* W;           // LSE (optional): [gl][Ns][M] raw-logit max of each row over the
+                        // bs sampled keys of block n (causal mask applied)
 };
 
 template <int kEmu>   // of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4)
@@ -258,6 +260,25 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         mx[c * 2 + (e >> 4)] = fmaxf(mx[c * 2 + (e >> 4)], __uint_as_float(raw[c][e]));
+                if (p.mode == kLse && p.W != nullptr && row_ok) {
+                    // A3 by-product: mx[k] is the max of 16-column group k, so the window
+                    // maxima of A3 are folds of it; the max-pool itself runs afterwards
+                    // from W and lse (maxpool_from_windows_kernel), bit-identical to kMaxpool
+                    const int nwin = 128 / p.bs;
+                    float* wrow = p.W + (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.M;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (c >= nwin) break;
+                        const float w = p.bs == 16 ? mx[c]
+                                      : p.bs == 32 ? fmaxf(mx[(2 * c) & 7], mx[(2 * c + 1) & 7])
+                                      : p.bs == 64 ? fmaxf(fmaxf(mx[(4 * c) & 7], mx[(4 * c + 1) & 7]),
+                                                           fmaxf(mx[(4 * c + 2) & 7], mx[(4 * c + 3) & 7]))
+                                                   : fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                        const int n = u * nwin + c;
+                        if (n < p.M) wrow[n] = w;
+                    }
+                }
                 const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                          fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.sc2;
                 const float ref = (p.mode == kLse) ? fmaxf(m_run, tmax) : tmax;
@@ -331,24 +352,54 @@ __global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, con
     (void)n_tr;
 }
 
+// A3 from the window maxima of the lse pass: L[c][m][n] = ln2 * max over the block's valid
+// sampled rows i of (W[c][i][n] * sc2 - lse2[c][i]) for n <= m, -inf above the diagonal.
+// The operations of kMaxpool (window max of raw logits, scale, subtract lse, max over rows,
+// ln2) without its second GEMM pass; one CTA per (group, block row).
+__global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, float sc2,
+                                                                   const float* __restrict__ W,
+                                                                   const float* __restrict__ lse2,
+                                                                   float* __restrict__ L) {
+    __shared__ float lse_s[128];
+    const int m = blockIdx.x % M, c = blockIdx.x / M;
+    const int i0 = m * bs, i1 = min(i0 + bs, Ns);
+    for (int i = threadIdx.x; i < i1 - i0; i += blockDim.x)
+        lse_s[i] = lse2[static_cast<long long>(c) * Ns + i0 + i];
+    __syncthreads();
+    float* Lrow = L + (static_cast<long long>(c) * M + m) * M;
+    const float* Wc = W + static_cast<long long>(c) * Ns * M;
+    for (int n = threadIdx.x; n < M; n += blockDim.x) {
+        float w = -INFINITY;
+        if (n <= m) {
+            for (int i = i0; i < i1; ++i)
+                w = fmaxf(w, fmaf(__ldg(Wc + static_cast<long long>(i) * M + n), sc2, -lse_s[i - i0]));
+            w *= kLn2;
+        }
+        Lrow[n] = w;
+    }
+}
+
 __global__ void fill_neg_inf_kernel(float* L, long long n) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) L[i] = -INFINITY;
 }
 
-// Alg. 1 lines 1-2 for one local head per CTA (1024 threads): combine the per-(row, block)
-// partials [u][t] into the row lse (8 chunk partials per row, merged in a fixed order),
-// then block masses a[u] = (1/b^2) sum_t s_tu 2^(m_tu - lse_t), one warp per block.
-__global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float* __restrict__ part_m,
-                                                              const float* __restrict__ part_s,
-                                                              float* __restrict__ bmass) {
-    __shared__ float cm[8][128], cs[8][128], lse_s[128];
-    const int hl = blockIdx.x;
+// Alg. 1 lines 1-2 from the per-(block u, row t) partials (m_tu, s_tu) of the budget pass,
+// in two grid-wide phases (the single-CTA-per-head version left 116 of 148 SMs idle):
+//   phase 1: per (head, chunk of kCombChunks blocks) and row t, the online (max, sum) of
+//            the chunk's partials -> cm/cs [Hl][n_chunks][128]
+//   phase 2: per (head, chunk): row lse_t from the chunk partials (fixed order), then the
+//            block masses a[u] = (1/b^2) sum_t s_tu 2^(m_tu - lse_t) of the chunk's blocks.
+constexpr int kCombChunk = 16;   // blocks per chunk
+
+__global__ void __launch_bounds__(128) budget_part_kernel(int M, int n_chunks, const float* __restrict__ part_m,
+                                                          const float* __restrict__ part_s,
+                                                          float* __restrict__ cm, float* __restrict__ cs) {
+    const int hl = blockIdx.x / n_chunks, k = blockIdx.x % n_chunks;
+    const int t = threadIdx.x;
+    const int u0 = k * kCombChunk, u1 = min(u0 + kCombChunk, M);
     const float* pm = part_m + static_cast<long long>(hl) * M * 128;
     const float* ps = part_s + static_cast<long long>(hl) * M * 128;
-    const int t = threadIdx.x & 127, c = threadIdx.x >> 7;
-    const int per = (M + 7) / 8;
-    const int u0 = c * per, u1 = min(u0 + per, M);
     float m = -INFINITY, sum = 0.f;
 #pragma unroll 4
     for (int u = u0; u < u1; ++u) {
@@ -362,29 +413,47 @@ __global__ void __launch_bounds__(1024) budget_combine_kernel(int M, const float
             sum += su * ex2(mu - m);
         }
     }
-    cm[c][t] = m;
-    cs[c][t] = sum;
-    __syncthreads();
-    if (c == 0) {
+    const long long o = (static_cast<long long>(hl) * n_chunks + k) * 128 + t;
+    cm[o] = m;
+    cs[o] = sum;
+}
+
+__global__ void __launch_bounds__(256) budget_mass_kernel(int M, int n_chunks, const float* __restrict__ part_m,
+                                                          const float* __restrict__ part_s,
+                                                          const float* __restrict__ cm,
+                                                          const float* __restrict__ cs,
+                                                          float* __restrict__ bmass) {
+    __shared__ float lse_s[128];
+    const int hl = blockIdx.x / n_chunks, k = blockIdx.x % n_chunks;
+    if (threadIdx.x < 128) {
+        const int t = threadIdx.x;
+        const float* pcm = cm + static_cast<long long>(hl) * n_chunks * 128 + t;
+        const float* pcs = cs + static_cast<long long>(hl) * n_chunks * 128 + t;
         float mx = -INFINITY;
-        for (int k = 0; k < 8; ++k) mx = fmaxf(mx, cm[k][t]);
+        for (int q = 0; q < n_chunks; ++q) mx = fmaxf(mx, pcm[q * 128]);
         float s2 = 0.f;
-        for (int k = 0; k < 8; ++k) s2 += (cs[k][t] > 0.f) ? cs[k][t] * ex2(cm[k][t] - mx) : 0.f;
+        for (int q = 0; q < n_chunks; ++q) {
+            const float sq = pcs[q * 128];
+            s2 += (sq > 0.f) ? sq * ex2(pcm[q * 128] - mx) : 0.f;
+        }
         lse_s[t] = (s2 > 0.f) ? mx + __log2f(s2) : INFINITY;   // padded row: no mass
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float l4[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) l4[k] = lse_s[lane + 32 * k];
-    for (int u = w; u < M; u += 32) {
+    for (int q = 0; q < 4; ++q) l4[q] = lse_s[lane + 32 * q];
+    const float* pm = part_m + static_cast<long long>(hl) * M * 128;
+    const float* ps = part_s + static_cast<long long>(hl) * M * 128;
+    const int u1 = min((k + 1) * kCombChunk, M);
+    for (int u = k * kCombChunk + w; u < u1; u += 8) {
         const float* pmu = pm + static_cast<long long>(u) * 128;
         const float* psu = ps + static_cast<long long>(u) * 128;
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float sv = __ldg(psu + lane + 32 * k);
-            if (sv > 0.f) a += sv * ex2(__ldg(pmu + lane + 32 * k) - l4[k]);
+        for (int q = 0; q < 4; ++q) {
+            const float sv = __ldg(psu + lane + 32 * q);
+            if (sv > 0.f) a += sv * ex2(__ldg(pmu + lane + 32 * q) - l4[q]);
         }
         a = warp_sum(a);
         if (lane == 0) bmass[static_cast<long long>(hl) * M + u] = a / (128.f * 128.f);
@@ -400,6 +469,17 @@ int score_emu() {
         v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
     }
     return v;
+}
+
+// PROXYATTN_MAXPOOL_PASS=1: A3 as a second tcgen05 pass (kMaxpool) instead of from the
+// window maxima the lse pass stores (diagnostics / comparison only).
+bool maxpool_pass() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PROXYATTN_MAXPOOL_PASS");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
@@ -430,8 +510,12 @@ bool score_tc_supported(const Dims& D) {
 size_t score_tc_scratch_bytes(const Dims& D) {
     const int n_tr = static_cast<int>((D.Ns + 127) / 128);
     const int n_chunks = (n_tr + kChunk - 1) / kChunk;
-    const size_t lse_parts = 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4;
-    const size_t bud_parts = 2ull * D.Hl * D.M * 128 * 4;
+    // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]; A4: (m, s) partials + the
+    // combine's chunk partials.  The two passes run one after the other and share it.
+    const size_t lse_parts = 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 +
+                             static_cast<size_t>(D.gl) * D.Ns * D.M * 4;
+    const size_t n_comb = (D.M + kCombChunk - 1) / kCombChunk;
+    const size_t bud_parts = 2ull * D.Hl * D.M * 128 * 4 + 2ull * D.Hl * n_comb * 128 * 4;
     return lse_parts > bud_parts ? lse_parts : bud_parts;
 }
 
@@ -459,6 +543,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     float* lse2 = part_s + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;
     p.part_m = part_m;
     p.part_s = part_s;
+    p.W = maxpool_pass() ? nullptr : lse2 + static_cast<size_t>(D.gl) * D.Ns;
     const unsigned grid = static_cast<unsigned>(D.gl) * p.n_tr * p.n_chunks;
     p.mode = kLse;
     score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
@@ -468,6 +553,11 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
         static_cast<int>(rws), p.n_tr, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!maxpool_pass()) {
+        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * D.M, 256, 0, st>>>(
+            D.M, p.Ns, p.bs, p.sc2, p.W, lse2, L);
+        return cudaGetLastError();
+    }
     const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
     fill_neg_inf_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(L, cells);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -499,7 +589,12 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
     score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    budget_combine_kernel<<<D.Hl, 1024, 0, st>>>(D.M, p.part_m, p.part_s, bmass);
+    const int n_comb = (D.M + kCombChunk - 1) / kCombChunk;
+    float* cm = p.part_s + static_cast<size_t>(D.Hl) * D.M * 128;
+    float* cs = cm + static_cast<size_t>(D.Hl) * n_comb * 128;
+    budget_part_kernel<<<D.Hl * n_comb, 128, 0, st>>>(D.M, n_comb, p.part_m, p.part_s, cm, cs);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    budget_mass_kernel<<<D.Hl * n_comb, 256, 0, st>>>(D.M, n_comb, p.part_m, p.part_s, cm, cs, bmass);
     return cudaGetLastError();
 }
 
