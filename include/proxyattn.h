@@ -6,10 +6,15 @@
  * Steps A1-A8 are SURVEY.md §8(a); readings Z1-Z23 are listed in DESIGN.md.
  *
  * Conventions (every entry point):
- *  - All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors), contiguous,
- *    16-byte aligned.  Layout is head-major: Q [Hl][N][d], K/V [Hkv_l][N][d], O [Hl][N][d],
- *    where Hl = q_head_end - q_head_begin is the local query-head shard and Hkv_l = Hl / r
- *    (r = Hq/Hkv) the kv heads it uses, starting at kv head q_head_begin / r.
+ *  - All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors), 16-byte
+ *    aligned.  Default layout is head-major and contiguous: Q [Hl][N][d], K/V [Hkv_l][N][d],
+ *    O [Hl][N][d], where Hl = q_head_end - q_head_begin is the local query-head shard and
+ *    Hkv_l = Hl / r (r = Hq/Hkv) the kv heads it uses, starting at kv head q_head_begin / r.
+ *    With PROXYATTN_FLAG_TOKEN_MAJOR the layout is token-major with a token stride (the
+ *    packed [tokens][heads][d] layout of serving engines): element (local head h, token t,
+ *    i) of Q / O is at Q[t * q_token_stride + h * d + i], of K / V at
+ *    K[t * kv_token_stride + h_kv * d + i]; Q, O, K, V point at the first LOCAL head.
+ *    Strides 0 mean the packed defaults Hl * d and Hkv_l * d.
  *  - Element type: bf16 (__nv_bfloat16) by default; fp32 when PROXYATTN_FLAG_FP32_DEBUG.
  *  - Per-head outputs (kstar, budget, block_cnt, block_idx) are indexed by local head.
  *  - All work is enqueued on `stream` (a cudaStream_t, passed as void*); no call
@@ -58,6 +63,9 @@ typedef struct {
                                     [row_begin, row_end) (row_end == 0: all rows); other rows of O
                                     are left untouched (zig-zag row sharding) */
     int32_t  row_end;
+    int64_t  q_token_stride;     /* TOKEN_MAJOR only: elements between consecutive tokens of Q / O
+                                    (>= Hl * d, a multiple of 8; 0 = Hl * d) */
+    int64_t  kv_token_stride;    /* TOKEN_MAJOR only: the same for K / V (>= Hkv_l * d; 0 = Hkv_l * d) */
 } proxyattn_cfg;
 
 #define PROXYATTN_FLAG_FP32_DEBUG  0x1u  /* fp32 Q/K/V/O, SIMT FFMA kernels (1e-4 contract)   */
@@ -67,6 +75,8 @@ typedef struct {
 #define PROXYATTN_FLAG_CONSTANT_K  0x8u  /* Eq. 3 K = ceil(b_i M) on every row, capped at m+1 (Z12 alt.) */
 #define PROXYATTN_FLAG_DESIGNATED_HEAD 0x10u /* proxy = the group's first query / kv head instead of
                                                 the Eq. 2 mean ("a designated head"; Z1 alt.) */
+/* Layout: token-major Q/K/V/O with token strides (see Conventions). */
+#define PROXYATTN_FLAG_TOKEN_MAJOR 0x20u
 
 #define PROXYATTN_OK               0
 #define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */
@@ -150,6 +160,24 @@ int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out
 int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const void* K_host,
                            const void* V_host, void* O_host, int32_t* kstar_host,
                            void* device_ws, size_t device_ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- varlen -- */
+
+/* Variable-length batch (batch / varlen packing): n_seqs independent
+ * sequences packed along the token axis, sequence i = tokens [cu_seqlens[i],
+ * cu_seqlens[i+1]) (cu_seqlens: HOST int64 array of n_seqs + 1 entries, cu_seqlens[0] = 0,
+ * non-decreasing).  Requires PROXYATTN_FLAG_TOKEN_MAJOR (Q/K/V/O are [total][heads][d] with
+ * the cfg's token strides); cfg->seq_len is ignored.  Each sequence is one ProxyAttn layer
+ * of its own (estimate A1-A6 + prefill A7, the paper's method per sequence):
+ * its pooling, budgets and selection see only its own tokens.  Empty sequences are skipped.
+ * Everything is enqueued on `stream`; the workspace is reused sequence after sequence.
+ * kstar (optional, DEVICE [n_seqs][Hl] int32) receives each sequence's K*_h. */
+int proxyattn_varlen_workspace_bytes(const proxyattn_cfg* cfg, int32_t n_seqs,
+                                     const int64_t* cu_seqlens, size_t* out_bytes);
+int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int64_t* cu_seqlens,
+                             const void* Q, const void* K, const void* V, void* O,
+                             void* workspace, size_t workspace_bytes, int32_t* kstar,
+                             void* stream);
 
 /* ----------------------------------------------------------------- misc -- */
 

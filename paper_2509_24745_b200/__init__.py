@@ -17,10 +17,13 @@ from ._lib import (  # noqa: F401
     estimate,
     forward_host,
     forward_host_workspace_bytes,
+    forward_varlen,
     lib,
     pool,
     prefill,
     proxy_scores,
     select,
+    varlen_workspace_bytes,
+    with_strides,
     workspace_bytes,
 )

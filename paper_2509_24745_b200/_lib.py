@@ -20,6 +20,7 @@ FLAG_CHECK = 0x2
 FLAG_FORCE_SINK = 0x4
 FLAG_CONSTANT_K = 0x8
 FLAG_DESIGNATED_HEAD = 0x10
+FLAG_TOKEN_MAJOR = 0x20
 
 OK = 0
 E_CONFIG = -1
@@ -52,6 +53,8 @@ class _CCfg(ctypes.Structure):
         ("static_kstar", ctypes.c_int32),
         ("row_begin", ctypes.c_int32),
         ("row_end", ctypes.c_int32),
+        ("q_token_stride", ctypes.c_int64),
+        ("kv_token_stride", ctypes.c_int64),
     ]
 
 
@@ -78,6 +81,9 @@ class Config:
     static_kstar: int = 0
     row_begin: int = 0              # prefill row range (zig-zag row sharding); 0/0 = all rows
     row_end: int = 0
+    token_major: bool = False       # Q/K/V/O as [N][heads][d] with token strides (0 = packed)
+    q_token_stride: int = 0
+    kv_token_stride: int = 0
 
     @property
     def M(self) -> int:
@@ -111,11 +117,13 @@ class Config:
         flags = ((FLAG_FP32_DEBUG if self.fp32_debug else 0) | (FLAG_CHECK if self.check else 0)
                  | (FLAG_FORCE_SINK if self.force_sink else 0)
                  | (FLAG_CONSTANT_K if self.constant_k else 0)
-                 | (FLAG_DESIGNATED_HEAD if self.designated_head else 0))
+                 | (FLAG_DESIGNATED_HEAD if self.designated_head else 0)
+                 | (FLAG_TOKEN_MAJOR if self.token_major else 0))
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
                      self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,
-                     self.static_kstar, self.row_begin, self.row_end)
+                     self.static_kstar, self.row_begin, self.row_end, self.q_token_stride,
+                     self.kv_token_stride)
 
 
 _lib = None
@@ -138,6 +146,10 @@ _SIGS = {
     "proxyattn_build_info": ([], ctypes.c_char_p),
     "proxyattn_debug_umma": ([_P, _P, _P, _P, _P], ctypes.c_int),
     "proxyattn_debug_trace": ([_P, ctypes.c_size_t], ctypes.c_int),
+    "proxyattn_varlen_workspace_bytes": ([_CP, ctypes.c_int32, _P, ctypes.POINTER(ctypes.c_size_t)],
+                                         ctypes.c_int),
+    "proxyattn_forward_varlen": ([_CP, ctypes.c_int32, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P],
+                                 ctypes.c_int),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -173,6 +185,31 @@ def _ptr(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _tptr(t: torch.Tensor | None, cfg: "Config"):
+    """Pointer of a Q/K/V/O tensor: contiguous head-major, or token-major [N][heads][d]
+    whose token stride is the one in cfg (rows of d contiguous elements)."""
+    if t is None or not cfg.token_major:
+        return _ptr(t)
+    if t.dim() != 3 or t.stride(2) != 1 or (t.shape[1] > 1 and t.stride(1) != t.shape[2]):
+        raise ValueError("token-major tensors must be [N][heads][d] with contiguous heads x d rows")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def with_strides(cfg: "Config", Q: torch.Tensor, K: torch.Tensor) -> "Config":
+    """Token-major config whose token strides are taken from the tensors (e.g. head slices
+    of a packed [N][H][d] activation)."""
+    return cfg.replace(token_major=True, q_token_stride=Q.stride(0), kv_token_stride=K.stride(0))
+
+
+def _like_q(cfg: "Config", Q: torch.Tensor) -> torch.Tensor:
+    """An output with Q's layout (token-major outputs share Q's token stride)."""
+    if not cfg.token_major or Q.is_contiguous():
+        return torch.empty_like(Q)
+    n, h, d = Q.shape
+    buf = torch.empty(n * Q.stride(0), dtype=Q.dtype, device=Q.device)
+    return buf.as_strided((n, h, d), (Q.stride(0), d, 1))
+
+
 def _stream(device: torch.device):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -205,7 +242,7 @@ def estimate(cfg: Config, Q: torch.Tensor, K: torch.Tensor, workspace: torch.Ten
                torch.empty(Hl, M, dtype=torch.int32, device=dev),
                torch.empty(Hl, M, M, dtype=torch.int32, device=dev))
     kstar, budget, cnt, idx = out
-    _check(lib().proxyattn_estimate(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(workspace),
+    _check(lib().proxyattn_estimate(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(workspace),
                                     workspace.numel(), _ptr(kstar), _ptr(budget), _ptr(cnt),
                                     _ptr(idx), _stream(dev)))
     return kstar, budget, cnt, idx
@@ -214,18 +251,18 @@ def estimate(cfg: Config, Q: torch.Tensor, K: torch.Tensor, workspace: torch.Ten
 def prefill(cfg: Config, Q, K, V, block_cnt, block_idx, O=None):
     """proxyattn_prefill -> O [Hl][N][d]."""
     if O is None:
-        O = torch.empty_like(Q)
-    _check(lib().proxyattn_prefill(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(block_cnt),
-                                   _ptr(block_idx), _ptr(O), _stream(Q.device)))
+        O = _like_q(cfg, Q)
+    _check(lib().proxyattn_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg),
+                                   _ptr(block_cnt), _ptr(block_idx), _tptr(O, cfg), _stream(Q.device)))
     return O
 
 
 def dense_prefill(cfg: Config, Q, K, V, O=None):
     """proxyattn_dense_prefill -> O [Hl][N][d]."""
     if O is None:
-        O = torch.empty_like(Q)
-    _check(lib().proxyattn_dense_prefill(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
-                                         _stream(Q.device)))
+        O = _like_q(cfg, Q)
+    _check(lib().proxyattn_dense_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg),
+                                         _tptr(O, cfg), _stream(Q.device)))
     return O
 
 
@@ -235,7 +272,7 @@ def pool(cfg: Config, Q, K):
     shape = (gl, cfg.Ns, cfg.head_dim)
     qsum = torch.empty(shape, dtype=torch.float32, device=Q.device)
     ksum = torch.empty_like(qsum)
-    _check(lib().proxyattn_pool(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(qsum), _ptr(ksum),
+    _check(lib().proxyattn_pool(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(qsum), _ptr(ksum),
                                 _stream(Q.device)))
     return qsum, ksum
 
@@ -256,7 +293,7 @@ def budgets(cfg: Config, Q, K, workspace=None):
         workspace = alloc_workspace(cfg, Q.device)
     kstar = torch.empty(cfg.Hl, dtype=torch.int32, device=Q.device)
     budget = torch.empty(cfg.Hl, dtype=torch.float32, device=Q.device)
-    _check(lib().proxyattn_budgets(_cfg_ref(cfg), _ptr(Q), _ptr(K), _ptr(workspace),
+    _check(lib().proxyattn_budgets(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(workspace),
                                    workspace.numel(), _ptr(kstar), _ptr(budget),
                                    _stream(Q.device)))
     return kstar, budget
@@ -283,6 +320,42 @@ def forward_host(cfg: Config, Qh, Kh, Vh, Oh, device_ws, kstar_h=None):
                                         _ptr(kstar_h), _ptr(device_ws), device_ws.numel(),
                                         _stream(device_ws.device)))
     return Oh
+
+
+def _cu(cu_seqlens) -> torch.Tensor:
+    cu = torch.as_tensor(cu_seqlens, dtype=torch.int64).cpu().contiguous()
+    if cu.dim() != 1 or cu.numel() < 1:
+        raise ValueError("cu_seqlens must be a 1-D list of n_seqs + 1 offsets")
+    return cu
+
+
+def varlen_workspace_bytes(cfg: Config, cu_seqlens) -> int:
+    cu = _cu(cu_seqlens)
+    n = ctypes.c_size_t(0)
+    _check(lib().proxyattn_varlen_workspace_bytes(_cfg_ref(cfg), cu.numel() - 1,
+                                                  ctypes.c_void_p(cu.data_ptr()), ctypes.byref(n)))
+    return n.value
+
+
+def forward_varlen(cfg: Config, cu_seqlens, Q, K, V, O=None, workspace=None, kstar=None):
+    """proxyattn_forward_varlen: packed token-major Q/K/V [total][heads][d], sequence i =
+    tokens [cu[i], cu[i+1]); each sequence is its own ProxyAttn layer.  Returns (O, kstar
+    [n_seqs][Hl] int32)."""
+    if not cfg.token_major:
+        cfg = with_strides(cfg, Q, K)
+    cu = _cu(cu_seqlens)
+    n = cu.numel() - 1
+    if workspace is None:
+        workspace = torch.empty(varlen_workspace_bytes(cfg, cu), dtype=torch.uint8, device=Q.device)
+    if O is None:
+        O = _like_q(cfg, Q)
+    if kstar is None:
+        kstar = torch.zeros(max(n, 1), cfg.Hl, dtype=torch.int32, device=Q.device)
+    _check(lib().proxyattn_forward_varlen(_cfg_ref(cfg), n, ctypes.c_void_p(cu.data_ptr()),
+                                          _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg), _tptr(O, cfg),
+                                          _ptr(workspace), workspace.numel(), _ptr(kstar),
+                                          _stream(Q.device)))
+    return O, kstar[:n]
 
 
 def cost_ratio(cfg: Config) -> float:

@@ -92,6 +92,22 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     D.Hkvl = D.Hl / D.r;
     D.gb = pa::group_of_q(D, D.qb);
     D.gl = pa::group_of_q(D, D.qe - 1) - D.gb + 1;
+    D.tok = (c->flags & PROXYATTN_FLAG_TOKEN_MAJOR) != 0;
+    if (D.tok) {
+        D.q_ts = c->q_token_stride ? c->q_token_stride : static_cast<long long>(D.Hl) * D.d;
+        D.kv_ts = c->kv_token_stride ? c->kv_token_stride : static_cast<long long>(D.Hkvl) * D.d;
+        if (D.q_ts < static_cast<long long>(D.Hl) * D.d || D.kv_ts < static_cast<long long>(D.Hkvl) * D.d)
+            return fail(PROXYATTN_E_CONFIG, "token stride smaller than the local heads (%lld / %lld)",
+                        D.q_ts, D.kv_ts);
+        if (D.q_ts % 8 || D.kv_ts % 8)
+            return fail(PROXYATTN_E_CONFIG, "token strides must be multiples of 8 elements (16-byte rows)");
+        D.q_hs = D.kv_hs = D.d;
+    } else {
+        if (c->q_token_stride || c->kv_token_stride)
+            return fail(PROXYATTN_E_CONFIG, "token strides need PROXYATTN_FLAG_TOKEN_MAJOR");
+        D.q_ts = D.kv_ts = D.d;
+        D.q_hs = D.kv_hs = D.N * D.d;
+    }
     return PROXYATTN_OK;
 }
 
@@ -263,7 +279,12 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32) {
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
-        const int variant = pa::attn_variant(block_cnt == nullptr);
+        int variant = pa::attn_variant(block_cnt == nullptr);
+        if (D.tok) {   // only the persistent kernel reads token-major tensors (3-D TMA maps)
+            if (block_cnt == nullptr) variant = 8;
+            if (variant != 8)
+                return fail(PROXYATTN_E_UNSUPPORTED, "PROXYATTN_FLAG_TOKEN_MAJOR needs attention variant 8");
+        }
         if ((variant == 4 || variant == 5) && (D.N % D.b || D.rb != 0 || D.re != D.M))
             return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0 and all rows");
         if (variant == 4)
@@ -293,18 +314,27 @@ int proxyattn_dense_prefill(const proxyattn_cfg* cfg, const void* Q, const void*
     return attention(cfg, Q, K, V, nullptr, nullptr, O, stream);
 }
 
+// Bytes spanned by Q (= O) and by K (= V) in the configured layout.
+static size_t q_bytes(const pa::Dims& D) {
+    const size_t el = D.fp32 ? 4 : 2;
+    return (D.tok ? (size_t)D.N * D.q_ts : (size_t)D.Hl * D.N * D.d) * el;
+}
+static size_t kv_bytes(const pa::Dims& D) {
+    const size_t el = D.fp32 ? 4 : 2;
+    return (D.tok ? (size_t)D.N * D.kv_ts : (size_t)D.Hkvl * D.N * D.d) * el;
+}
+
 // Device workspace of the host path: Q, K, V, O, per-head outputs, then the estimate scratch.
 struct HostLayout {
     size_t q, k, v, o, kstar, budget, cnt, idx, ws, total;
 };
 static HostLayout host_layout(const pa::Dims& D) {
     HostLayout h{};
-    const size_t el = D.fp32 ? 4 : 2;
     size_t off = 0;
-    h.q = off;      off = pa::align256(off + (size_t)D.Hl * D.N * D.d * el);
-    h.k = off;      off = pa::align256(off + (size_t)D.Hkvl * D.N * D.d * el);
-    h.v = off;      off = pa::align256(off + (size_t)D.Hkvl * D.N * D.d * el);
-    h.o = off;      off = pa::align256(off + (size_t)D.Hl * D.N * D.d * el);
+    h.q = off;      off = pa::align256(off + q_bytes(D));
+    h.k = off;      off = pa::align256(off + kv_bytes(D));
+    h.v = off;      off = pa::align256(off + kv_bytes(D));
+    h.o = off;      off = pa::align256(off + q_bytes(D));
     h.kstar = off;  off = pa::align256(off + (size_t)D.Hl * 4);
     h.budget = off; off = pa::align256(off + (size_t)D.Hl * 4);
     h.cnt = off;    off = pa::align256(off + (size_t)D.Hl * D.M * 4);
@@ -332,8 +362,7 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     if (!dws || dws_bytes < H.total) return fail(PROXYATTN_E_WORKSPACE, "device workspace needs %zu bytes", H.total);
     if (!Qh || !Kh || !Vh || !Oh) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
     cudaStream_t st = S(stream);
-    const size_t el = D.fp32 ? 4 : 2;
-    const size_t qb = (size_t)D.Hl * D.N * D.d * el, kb = (size_t)D.Hkvl * D.N * D.d * el;
+    const size_t qb = q_bytes(D), kb = kv_bytes(D);
     PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.q), Qh, qb, cudaMemcpyHostToDevice, st), "H2D Q");
     PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, st), "H2D K");
     PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, st), "H2D V");
@@ -352,6 +381,86 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     return PROXYATTN_OK;
 }
 
+// ------------------------------------------------------------------ varlen --
+// One ProxyAttn layer per packed sequence: the cfg with seq_len = the sequence's length and
+// the pointers advanced by cu_seqlens[i] tokens; per-sequence outputs and estimate scratch
+// live in the caller's workspace (sized for the longest sequence) and are reused in stream order.
+struct VarlenLayout {
+    size_t kstar, budget, cnt, idx, ws, total;
+};
+static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu, VarlenLayout& L,
+                         int64_t& max_len) {
+    if (!cfg || !(cfg->flags & PROXYATTN_FLAG_TOKEN_MAJOR))
+        return fail(PROXYATTN_E_CONFIG, "varlen needs PROXYATTN_FLAG_TOKEN_MAJOR (packed [tokens][heads][d])");
+    if (n < 0 || !cu || cu[0] != 0) return fail(PROXYATTN_E_CONFIG, "cu_seqlens must start at 0");
+    max_len = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (cu[i + 1] < cu[i]) return fail(PROXYATTN_E_CONFIG, "cu_seqlens must be non-decreasing");
+        max_len = cu[i + 1] - cu[i] > max_len ? cu[i + 1] - cu[i] : max_len;
+    }
+    proxyattn_cfg c = *cfg;
+    c.seq_len = max_len > 0 ? max_len : 1;
+    pa::Dims D;
+    int rc = derive(&c, D);
+    if (rc) return rc;
+    size_t off = 0;
+    L.kstar = off;  off = pa::align256(off + (size_t)D.Hl * 4);
+    L.budget = off; off = pa::align256(off + (size_t)D.Hl * 4);
+    L.cnt = off;    off = pa::align256(off + (size_t)D.Hl * D.M * 4);
+    L.idx = off;    off = pa::align256(off + (size_t)D.Hl * D.M * D.M * 4);
+    L.ws = off;     off = pa::align256(off + pa::workspace_layout(D).total);
+    L.total = off;
+    return PROXYATTN_OK;
+}
+
+int proxyattn_varlen_workspace_bytes(const proxyattn_cfg* cfg, int32_t n_seqs, const int64_t* cu,
+                                     size_t* out) {
+    VarlenLayout L;
+    int64_t mx = 0;
+    int rc = varlen_layout(cfg, n_seqs, cu, L, mx);
+    if (rc) return rc;
+    if (!out) return fail(PROXYATTN_E_CONFIG, "out is NULL");
+    *out = L.total;
+    return PROXYATTN_OK;
+}
+
+int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int64_t* cu,
+                             const void* Q, const void* K, const void* V, void* O, void* ws,
+                             size_t ws_bytes, int32_t* kstar, void* stream) {
+    VarlenLayout L;
+    int64_t mx = 0;
+    int rc = varlen_layout(cfg, n_seqs, cu, L, mx);
+    if (rc) return rc;
+    if (!ws || ws_bytes < L.total) return fail(PROXYATTN_E_WORKSPACE, "varlen workspace needs %zu bytes", L.total);
+    if (!Q || !K || !V || !O) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    proxyattn_cfg c = *cfg;
+    c.seq_len = 1;
+    pa::Dims D0;
+    if ((rc = derive(&c, D0))) return rc;
+    const size_t el = D0.fp32 ? 4 : 2;
+    c.q_token_stride = D0.q_ts;      // pin the strides: the defaults depend on nothing per sequence,
+    c.kv_token_stride = D0.kv_ts;    // but make it explicit
+    for (int32_t i = 0; i < n_seqs; ++i) {
+        const int64_t n = cu[i + 1] - cu[i];
+        if (n == 0) continue;
+        c.seq_len = n;
+        const size_t qo = (size_t)cu[i] * D0.q_ts * el, ko = (size_t)cu[i] * D0.kv_ts * el;
+        int32_t* ks = at<int32_t>(ws, L.kstar);
+        rc = proxyattn_estimate(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
+                                at<char>(ws, L.ws), ws_bytes - L.ws, ks, at<float>(ws, L.budget),
+                                at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), stream);
+        if (rc) return rc;
+        rc = proxyattn_prefill(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
+                               static_cast<const char*>(V) + ko, at<int32_t>(ws, L.cnt),
+                               at<int32_t>(ws, L.idx), static_cast<char*>(O) + qo, stream);
+        if (rc) return rc;
+        if (kstar)
+            PA_CUDA(cudaMemcpyAsync(kstar + (size_t)i * D0.Hl, ks, (size_t)D0.Hl * 4,
+                                    cudaMemcpyDeviceToDevice, S(stream)), "varlen kstar");
+    }
+    return PROXYATTN_OK;
+}
+
 double proxyattn_cost_ratio(const proxyattn_cfg* cfg) {
     if (!cfg || cfg->n_q_heads <= 0 || cfg->stride <= 0) return 0.0;
     return static_cast<double>(cfg->n_groups) /
@@ -361,7 +470,7 @@ double proxyattn_cost_ratio(const proxyattn_cfg* cfg) {
 const char* proxyattn_last_error(void) { return g_err.c_str(); }
 
 const char* proxyattn_build_info(void) {
-    return "libproxyattn sm_100a (tcgen05/TMEM/TMA attention; SIMT estimation v1)";
+    return "libproxyattn sm_100a (tcgen05/TMEM/TMA attention and estimation)";
 }
 
 int proxyattn_debug_trace(long long* host_out, size_t n) {

@@ -19,10 +19,11 @@ __global__ void attn_simt_kernel(Dims D, const float* __restrict__ Q, const floa
     if (m < D.rb || m >= D.re) return;                      // outside the requested row range
     const int dv = D.d >> 5;
     const float sc = rsqrtf(static_cast<float>(D.d));
-    const long long kvoff = static_cast<long long>(hl / D.r) * D.N * D.d;
+    const long long kvoff = kv_off(D, hl / D.r, 0);
+    const long long qoff = q_off(D, hl, t);
     float q[4], o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) q[j] = (j < dv) ? Q[w * D.d + lane * dv + j] : 0.f;
+    for (int j = 0; j < 4; ++j) q[j] = (j < dv) ? Q[qoff + lane * dv + j] : 0.f;
     const bool dense = (block_cnt == nullptr);
     const long long row = static_cast<long long>(hl) * D.M + m;
     const int cnt = dense ? m + 1 : block_cnt[row];
@@ -32,8 +33,8 @@ __global__ void attn_simt_kernel(Dims D, const float* __restrict__ Q, const floa
         const long long n = dense ? u : list[u];
         const long long kend = min((n + 1) * D.b, t + 1);  // causal mask inside the diagonal block
         for (long long k = n * D.b; k < kend; ++k) {
-            const float* kr = K + kvoff + k * D.d + lane * dv;
-            const float* vr = V + kvoff + k * D.d + lane * dv;
+            const float* kr = K + kvoff + k * D.kv_ts + lane * dv;
+            const float* vr = V + kvoff + k * D.kv_ts + lane * dv;
             float part = 0.f;
 #pragma unroll
             for (int j = 0; j < 4; ++j) part = fmaf(q[j], (j < dv) ? kr[j] : 0.f, part);
@@ -53,7 +54,7 @@ __global__ void attn_simt_kernel(Dims D, const float* __restrict__ Q, const floa
         }
     }
     const float inv = 1.f / l;
-    for (int j = 0; j < dv; ++j) O[w * D.d + lane * dv + j] = o[j] * inv;
+    for (int j = 0; j < dv; ++j) O[qoff + lane * dv + j] = o[j] * inv;
 }
 
 }  // namespace

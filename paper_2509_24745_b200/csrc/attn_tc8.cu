@@ -89,7 +89,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
-                int* flagged, int exact) {
+                int* flagged, int exact, long long o_hs, long long o_ts) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -184,19 +184,17 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     decode(x.item, hl, m, kvl);
                     const int* list = list_of(hl, m);
                     if (it > 0) mbar_wait(&bars->q_empty, (it - 1) & 1);   // last S of it-1 done
-                    const int qrow = hl * N + m * kTileRows;
                     mbar_expect_tx(&bars->q_full, kTile);
-                    tma_load_2d(sQ, &tmQ, &bars->q_full, 0, qrow);
-                    tma_load_2d(sQ + kBox, &tmQ, &bars->q_full, 64, qrow);
+                    tma_load_3d(sQ, &tmQ, &bars->q_full, 0, m * kTileRows, hl);
+                    tma_load_3d(sQ + kBox, &tmQ, &bars->q_full, 64, m * kTileRows, hl);
                     for (int pass = 0; pass < passes; ++pass) {
                         for (int j = 0; j < x.cnt; ++j, ++gk) {
                             const int st = gk % kKStages;
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             const int n = dense ? j : __ldg(list + j);
-                            const int krow = kvl * N + n * kTileRows;
                             mbar_expect_tx(&bars->k_full[st], kTile);
-                            tma_load_2d(sK + st * kTile, &tmK, &bars->k_full[st], 0, krow);
-                            tma_load_2d(sK + st * kTile + kBox, &tmK, &bars->k_full[st], 64, krow);
+                            tma_load_3d(sK + st * kTile, &tmK, &bars->k_full[st], 0, n * kTileRows, kvl);
+                            tma_load_3d(sK + st * kTile + kBox, &tmK, &bars->k_full[st], 64, n * kTileRows, kvl);
                         }
                     }
                 }
@@ -216,10 +214,9 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         const int st = gv % kVStages;
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         const int n = dense ? j : __ldg(list + j);
-                        const int vrow = kvl * N + n * kTileRows;
                         mbar_expect_tx(&bars->v_full[st], kTile);
-                        tma_load_2d(sV + st * kTile, &tmV, &bars->v_full[st], 0, vrow);
-                        tma_load_2d(sV + st * kTile + kBox, &tmV, &bars->v_full[st], 64, vrow);
+                        tma_load_3d(sV + st * kTile, &tmV, &bars->v_full[st], 0, n * kTileRows, kvl);
+                        tma_load_3d(sV + st * kTile + kBox, &tmV, &bars->v_full[st], 64, n * kTileRows, kvl);
                     }
                 }
                 __syncwarp();
@@ -322,7 +319,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             tc_fence_after();
             const bool row_valid = static_cast<long long>(m) * kTileRows + rr < N;
             uint4* dst = reinterpret_cast<uint4*>(
-                O + (static_cast<long long>(hl) * N + static_cast<long long>(m) * kTileRows + rr) * 128);
+                O + static_cast<long long>(hl) * o_hs + (static_cast<long long>(m) * kTileRows + rr) * o_ts);
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
                 uint32_t o[2][32];
@@ -560,9 +557,9 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
     CUtensorMap mq, mk, mv;
-    if (!make_map_bf16_sw128(&mq, Q, static_cast<uint64_t>(D.Hl) * D.N, 128, 128) ||
-        !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
-        !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
+    if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128) ||
+        !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128) ||
+        !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128))
         return cudaErrorInvalidValue;
     static int emu = -1;
     if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe
@@ -593,7 +590,8 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         const int grid = exact ? n_sm : static_cast<int>(n_items < static_cast<size_t>(n_sm) ? n_items : n_sm);
         kern<<<grid, kThreads, kSmemBytes, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
-            D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact);
+            D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
+            D.q_hs, D.q_ts);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

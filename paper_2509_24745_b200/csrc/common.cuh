@@ -28,7 +28,19 @@ struct Dims {
     bool fp32;    // FP32_DEBUG
     int static_kstar;   // > 0: static top-K baseline (Alg. 1 skipped)
     int rb, re;         // prefill block-row range [rb, re)
+    // Q/O and K/V element strides (local head, token): head-major (d, N d) by default,
+    // token-major (token stride, d) with PROXYATTN_FLAG_TOKEN_MAJOR
+    bool tok;
+    long long q_hs, q_ts, kv_hs, kv_ts;
 };
+
+// Element offset of (local query head hl, token t) in Q / O, and of (local kv head, t) in K / V.
+__host__ __device__ __forceinline__ long long q_off(const Dims& D, int hl, long long t) {
+    return static_cast<long long>(hl) * D.q_hs + t * D.q_ts;
+}
+__host__ __device__ __forceinline__ long long kv_off(const Dims& D, int kvl, long long t) {
+    return static_cast<long long>(kvl) * D.kv_hs + t * D.kv_ts;
+}
 
 __host__ __device__ __forceinline__ bool has_flag(const Dims& D, uint32_t f) { return (D.flags & f) != 0; }
 

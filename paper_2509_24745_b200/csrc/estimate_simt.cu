@@ -49,13 +49,13 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
     double aq[4] = {0., 0., 0., 0.}, ak[4] = {0., 0., 0., 0.};
     for (int h = h0; h < h1; ++h) {  // fixed ascending order
         float x[4];
-        load_row(Q + (static_cast<long long>(h - D.qb) * D.N + p) * D.d, lane, x, dv);
+        load_row(Q + q_off(D, h - D.qb, p), lane, x, dv);
 #pragma unroll
         for (int j = 0; j < 4; ++j) aq[j] += x[j];
     }
     for (int k = k0; k < k1; ++k) {
         float x[4];
-        load_row(K + (static_cast<long long>(k - D.kvb) * D.N + p) * D.d, lane, x, dv);
+        load_row(K + kv_off(D, k - D.kvb, p), lane, x, dv);
 #pragma unroll
         for (int j = 0; j < 4; ++j) ak[j] += x[j];
     }
@@ -88,14 +88,15 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
     const int gke = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gk;
     const int h0 = max(grp * D.gq, D.qb), h1 = min(grp * D.gq + gqe, D.qe);
     const int k0 = max(grp * D.gk, D.kvb), k1 = min(grp * D.gk + gke, D.kvb + D.Hkvl);
-    auto accumulate = [&](const __nv_bfloat16* base, int a, int b, int head0, double (&acc)[8]) {
+    auto accumulate = [&](const __nv_bfloat16* base, int a, int b, int head0, long long hs, long long ts,
+                          double (&acc)[8]) {
         for (int h = a; h < b; h += 4) {
             uint4 v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (h + k < b)
                     v[k] = __ldg(reinterpret_cast<const uint4*>(
-                        base + (static_cast<long long>(h + k - head0) * D.N + p) * D.d + part * 8));
+                        base + static_cast<long long>(h + k - head0) * hs + p * ts + part * 8));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (h + k >= b) break;
@@ -110,8 +111,8 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
         }
     };
     double aq[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ak[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    accumulate(Q, h0, h1, D.qb, aq);
-    accumulate(K, k0, k1, D.kvb, ak);
+    accumulate(Q, h0, h1, D.qb, D.q_hs, D.q_ts, aq);
+    accumulate(K, k0, k1, D.kvb, D.kv_hs, D.kv_ts, ak);
     const long long o = row * D.d + part * 8;
     if (qsum) {
 #pragma unroll
@@ -236,12 +237,12 @@ __global__ void budget_lse_simt(Dims D, const T* __restrict__ Q, const T* __rest
     const int dv = D.d >> 5;
     const float sc = rsqrtf(static_cast<float>(D.d));
     float q[4];
-    load_row(Q + (static_cast<long long>(hl) * D.N + t) * D.d, lane, q, dv);
-    const T* kb = K + static_cast<long long>(hl / D.r) * D.N * D.d;
+    load_row(Q + q_off(D, hl, t), lane, q, dv);
+    const T* kb = K + kv_off(D, hl / D.r, 0);
     float mx = -INFINITY, sum = 0.f;
     for (long long k = 0; k <= t; ++k) {
         float kv[4];
-        load_row(kb + k * D.d, lane, kv, dv);
+        load_row(kb + k * D.kv_ts, lane, kv, dv);
         float part = 0.f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) part = fmaf(q[e], kv[e], part);
@@ -267,19 +268,19 @@ __global__ void budget_mass_simt(Dims D, const T* __restrict__ Q, const T* __res
     const int n = static_cast<int>(w % D.M);
     const int dv = D.d >> 5;
     const float sc = rsqrtf(static_cast<float>(D.d));
-    const T* kb = K + static_cast<long long>(hl / D.r) * D.N * D.d;
+    const T* kb = K + kv_off(D, hl / D.r, 0);
     float acc = 0.f;
     for (int tt = 0; tt < D.b; ++tt) {
         const long long t = static_cast<long long>(D.M - 1) * D.b + tt;
         if (t >= D.N) break;
         float q[4];
-        load_row(Q + (static_cast<long long>(hl) * D.N + t) * D.d, lane, q, dv);
+        load_row(Q + q_off(D, hl, t), lane, q, dv);
         const float lt = blse[static_cast<long long>(hl) * D.b + tt];
         for (int kk = 0; kk < D.b; ++kk) {
             const long long k = static_cast<long long>(n) * D.b + kk;
             if (k > t) break;
             float kv[4];
-            load_row(kb + k * D.d, lane, kv, dv);
+            load_row(kb + k * D.kv_ts, lane, kv, dv);
             float part = 0.f;
 #pragma unroll
             for (int e = 0; e < 4; ++e) part = fmaf(q[e], kv[e], part);

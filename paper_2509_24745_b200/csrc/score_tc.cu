@@ -69,14 +69,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 ScoreParams p) {
     // ---------------------------------------------------------------- problem --
     int a_row, b_row0, u_begin, u_end, diag_u, prob;  // prob: group (proxy) / local head
+    int a_head = 0, b_head = 0;                        // budget: 3-D maps (any Q/K layout)
     int tr = 0;                                        // proxy tile row
     if (p.mode == kBudget) {
         prob = blockIdx.x / p.n_chunks;
         const int k = blockIdx.x % p.n_chunks;
         u_begin = k * kChunk;
         u_end = min(u_begin + kChunk, p.M);
-        a_row = prob * p.N + (p.M - 1) * 128;     // the last block's query rows (Alg. 1)
-        b_row0 = (prob / p.r) * p.N;
+        a_row = (p.M - 1) * 128;                   // the last block's query rows (Alg. 1)
+        a_head = prob;
+        b_row0 = 0;
+        b_head = prob / p.r;
         diag_u = p.M - 1;
     } else {
         const int per_group = p.n_tr * p.n_chunks;
@@ -123,16 +126,20 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) {
             tma_prefetch(&tmA);
             tma_prefetch(&tmB);
+            auto load = [&](uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int col, int row, int head) {
+                if (p.mode == kBudget) tma_load_3d(dst, map, bar, col, row, head);
+                else tma_load_2d(dst, map, bar, col, row);
+            };
             mbar_expect_tx(&bars->a_full, kTile);
-            tma_load_2d(sA, &tmA, &bars->a_full, 0, a_row);
-            tma_load_2d(sA + kBox, &tmA, &bars->a_full, 64, a_row);
+            load(sA, &tmA, &bars->a_full, 0, a_row, a_head);
+            load(sA + kBox, &tmA, &bars->a_full, 64, a_row, a_head);
             for (int j = 0; j < nt; ++j) {
                 const int s = j % kStages;
                 if (j >= kStages) mbar_wait(&bars->b_empty[s], ((j / kStages) - 1) & 1);
                 const int brow = b_row0 + (u_begin + j) * 128;
                 mbar_expect_tx(&bars->b_full[s], kTile);
-                tma_load_2d(sB + s * kTile, &tmB, &bars->b_full[s], 0, brow);
-                tma_load_2d(sB + s * kTile + kBox, &tmB, &bars->b_full[s], 64, brow);
+                load(sB + s * kTile, &tmB, &bars->b_full[s], 0, brow, b_head);
+                load(sB + s * kTile + kBox, &tmB, &bars->b_full[s], 64, brow, b_head);
             }
         }
     } else if (warp == 1) {
@@ -573,8 +580,8 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
                              float* bmass, cudaStream_t st) {
     if (!set_smem_attr()) return cudaErrorInvalidValue;
     CUtensorMap ma, mb;
-    if (!make_map_bf16_sw128(&ma, Q, static_cast<uint64_t>(D.Hl) * D.N, 128, 128) ||
-        !make_map_bf16_sw128(&mb, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
+    if (!make_map_bf16_sw128_3d(&ma, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128) ||
+        !make_map_bf16_sw128_3d(&mb, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128))
         return cudaErrorInvalidValue;
     ScoreParams p{};
     p.mode = kBudget;

@@ -85,3 +85,28 @@ def test_shard_group_arithmetic():
     # Llama g=1 over 8 ranks: every rank touches the single (partial) group
     cfg = pa.Config(32, 8, 128, 4096, 128, 4, 1, 0.9, q_head_begin=4, q_head_end=8)
     assert pa._lib._local_groups(cfg) == 1
+
+
+def test_token_major_and_varlen_configs_on_host(so):
+    good = pa.Config(32, 8, 128, 4096, 128, 4, 1, 0.9)
+    tok = good.replace(token_major=True)
+    assert pa.workspace_bytes(tok) == pa.workspace_bytes(good)   # scratch is layout-free
+    assert pa.workspace_bytes(tok.replace(q_token_stride=4096 + 8, kv_token_stride=1024)) > 0
+    bad = {
+        "q stride below the local heads": tok.replace(q_token_stride=32 * 128 - 8),
+        "kv stride below the local heads": tok.replace(kv_token_stride=8 * 128 - 8),
+        "stride not 16-byte": tok.replace(q_token_stride=32 * 128 + 4),
+        "strides without the flag": good.replace(q_token_stride=8192),
+    }
+    for name, cfg in bad.items():
+        with pytest.raises(pa.ProxyAttnError) as ei:
+            pa.workspace_bytes(cfg)
+        assert ei.value.code == pa._lib.E_CONFIG, name
+    # varlen: workspace sized by the longest sequence; validation of cu_seqlens
+    assert pa.varlen_workspace_bytes(tok, [0, 1000, 5096, 5096]) == \
+        pa.varlen_workspace_bytes(tok, [0, 4096])
+    for cu in ([1, 100], [0, 100, 50]):
+        with pytest.raises(pa.ProxyAttnError):
+            pa.varlen_workspace_bytes(tok, cu)
+    with pytest.raises(pa.ProxyAttnError):                     # needs the token-major layout
+        pa.varlen_workspace_bytes(good, [0, 100])
