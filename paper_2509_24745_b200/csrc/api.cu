@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -353,6 +356,26 @@ int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out
     return PROXYATTN_OK;
 }
 
+// Auxiliary streams of the host path (created once per device, non-blocking): one for the
+// V uploads, one for the O downloads, so PCIe traffic in both directions overlaps compute.
+struct HostStreams {
+    cudaStream_t up = nullptr, down = nullptr;
+};
+static int host_streams(HostStreams& hs) {
+    static std::mutex mu;
+    static std::map<int, HostStreams> per_dev;
+    int dev = 0;
+    PA_CUDA(cudaGetDevice(&dev), "get device");
+    std::lock_guard<std::mutex> lock(mu);
+    HostStreams& h = per_dev[dev];
+    if (!h.up) {
+        PA_CUDA(cudaStreamCreateWithFlags(&h.up, cudaStreamNonBlocking), "stream create");
+        PA_CUDA(cudaStreamCreateWithFlags(&h.down, cudaStreamNonBlocking), "stream create");
+    }
+    hs = h;
+    return PROXYATTN_OK;
+}
+
 int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void* Kh, const void* Vh,
                            void* Oh, int32_t* kstar_h, void* dws, size_t dws_bytes, void* stream) {
     pa::Dims D;
@@ -363,21 +386,59 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     if (!Qh || !Kh || !Vh || !Oh) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
     cudaStream_t st = S(stream);
     const size_t qb = q_bytes(D), kb = kv_bytes(D);
-    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.q), Qh, qb, cudaMemcpyHostToDevice, st), "H2D Q");
+    // Pipeline (head-major): K and Q up on `stream` -> estimate; V up per KV head on the
+    // upload stream meanwhile; attention per KV head (its r query heads) as soon as that
+    // head's V has landed; each head's O down on the download stream while the next head
+    // computes.  Token-major tensors interleave heads, so they take the serial order.
+    const int chunks = D.tok ? 1 : D.Hkvl;
+    HostStreams hs;
+    if ((rc = host_streams(hs))) return rc;
+    std::vector<cudaEvent_t> ev(2 * chunks + 2);
+    for (auto& e : ev) PA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    auto cleanup = [&]() { for (auto& e : ev) cudaEventDestroy(e); };
+    cudaEvent_t ev_qk = ev[0], ev_done = ev[1];
     PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, st), "H2D K");
-    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, st), "H2D V");
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.q), Qh, qb, cudaMemcpyHostToDevice, st), "H2D Q");
+    PA_CUDA(cudaEventRecord(ev_qk, st), "record");
+    PA_CUDA(cudaStreamWaitEvent(hs.up, ev_qk, 0), "wait");        // V after Q/K on the link
+    const size_t vchunk = kb / chunks;
+    for (int c = 0; c < chunks; ++c) {
+        PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v) + c * vchunk, static_cast<const char*>(Vh) + c * vchunk,
+                                vchunk, cudaMemcpyHostToDevice, hs.up), "H2D V");
+        PA_CUDA(cudaEventRecord(ev[2 + c], hs.up), "record");
+    }
     rc = proxyattn_estimate(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws),
                             dws_bytes - H.ws, at<int32_t>(dws, H.kstar), at<float>(dws, H.budget),
                             at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), stream);
-    if (rc) return rc;
-    rc = proxyattn_prefill(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.v),
-                           at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), at<char>(dws, H.o), stream);
-    if (rc) return rc;
-    PA_CUDA(cudaMemcpyAsync(Oh, at<char>(dws, H.o), qb, cudaMemcpyDeviceToHost, st), "D2H O");
+    if (rc) { cleanup(); return rc; }
+    const size_t el = D.fp32 ? 4 : 2;
+    const size_t qchunk = qb / chunks;
+    const int hq = D.Hl / chunks;                               // query heads per chunk (= r)
+    for (int c = 0; c < chunks; ++c) {
+        PA_CUDA(cudaStreamWaitEvent(st, ev[2 + c], 0), "wait");
+        proxyattn_cfg cc = *cfg;
+        if (chunks > 1) {
+            cc.q_head_begin = D.qb + c * hq;
+            cc.q_head_end = cc.q_head_begin + hq;
+        }
+        rc = proxyattn_prefill(&cc, at<char>(dws, H.q) + c * qchunk, at<char>(dws, H.k) + c * vchunk,
+                               at<char>(dws, H.v) + c * vchunk, at<int32_t>(dws, H.cnt) + (size_t)c * hq * D.M,
+                               at<int32_t>(dws, H.idx) + (size_t)c * hq * D.M * D.M,
+                               at<char>(dws, H.o) + c * qchunk, stream);
+        if (rc) { cleanup(); return rc; }
+        PA_CUDA(cudaEventRecord(ev[2 + chunks + c], st), "record");
+        PA_CUDA(cudaStreamWaitEvent(hs.down, ev[2 + chunks + c], 0), "wait");
+        PA_CUDA(cudaMemcpyAsync(static_cast<char*>(Oh) + c * qchunk, at<char>(dws, H.o) + c * qchunk, qchunk,
+                                cudaMemcpyDeviceToHost, hs.down), "D2H O");
+    }
+    (void)el;
+    PA_CUDA(cudaEventRecord(ev_done, hs.down), "record");
+    PA_CUDA(cudaStreamWaitEvent(st, ev_done, 0), "wait");
     if (kstar_h)
         PA_CUDA(cudaMemcpyAsync(kstar_h, at<char>(dws, H.kstar), (size_t)D.Hl * 4, cudaMemcpyDeviceToHost, st),
                 "D2H kstar");
     PA_CUDA(cudaStreamSynchronize(st), "forward_host sync");
+    cleanup();
     return PROXYATTN_OK;
 }
 
