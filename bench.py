@@ -334,7 +334,9 @@ def run_ours(args):
     my_rows = shard.zigzag_rows(M, ws, rank) if sharding == "rows" else [(0, M)]
 
     def estimate():
-        if sharding == "rows":   # replicated estimate (~1 ms), no cross-GPU traffic
+        if sharding == "rows" and ws > 1:   # lists of this rank's rows only, no cross-GPU traffic
+            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx))
+        elif sharding == "rows":
             pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
         else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums
             shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=(kstar, budget, cnt, idx))
@@ -382,7 +384,11 @@ def run_ours(args):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        pa.dense_prefill(cfg, Ql, Kl, Vl, Od)
+        if sharding == "rows" and ws > 1:     # the same row shard as the sparse step
+            for b, e in my_rows:
+                pa.dense_prefill(cfg.replace(row_begin=b, row_end=e), Ql, Kl, Vl, Od)
+        else:
+            pa.dense_prefill(cfg, Ql, Kl, Vl, Od)
         e1.record(st)
         torch.cuda.synchronize()
         if i >= args.warmup:
@@ -496,8 +502,9 @@ def run_ours(args):
         "e2e": e2e,
         # attn_tc8 is two launches per prefill call: the fast pass and the exact re-run of
         # the rows it flagged (an empty list at these inputs)
-        "gpu_launches": (ESTIMATE_KERNELS + len(my_rows) * (2 if kname == "attn_tc8_kernel" else 1))
-                        * args.steps,
+        # estimate: 9 kernels (4 of them Alg. 1); a row-range estimate adds 5 per extra range
+        "gpu_launches": (ESTIMATE_KERNELS + 5 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
+                         + len(my_rows) * (2 if kname == "attn_tc8_kernel" else 1)) * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

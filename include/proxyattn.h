@@ -59,9 +59,11 @@ typedef struct {
     int32_t  q_head_end;
     int32_t  static_kstar;       /* > 0: static top-K baseline (Fig. 6c): every head uses
                                     K* = static_kstar instead of Alg. 1's dynamic budget; 0 = Alg. 1 */
-    int32_t  row_begin;          /* prefill / dense_prefill only: compute query block rows
-                                    [row_begin, row_end) (row_end == 0: all rows); other rows of O
-                                    are left untouched (zig-zag row sharding) */
+    int32_t  row_begin;          /* prefill / dense_prefill / estimate / select: compute query
+                                    block rows [row_begin, row_end) only (row_end == 0: all rows);
+                                    other rows of O / block_cnt / block_idx are left untouched
+                                    (zig-zag row sharding); kstar / budget always
+                                    cover every local head */
     int32_t  row_end;
     int64_t  q_token_stride;     /* TOKEN_MAJOR only: elements between consecutive tokens of Q / O
                                     (>= Hl * d, a multiple of 8; 0 = Hl * d) */
@@ -77,6 +79,9 @@ typedef struct {
                                                 the Eq. 2 mean ("a designated head"; Z1 alt.) */
 /* Layout: token-major Q/K/V/O with token strides (see Conventions). */
 #define PROXYATTN_FLAG_TOKEN_MAJOR 0x20u
+/* estimate only: kstar is an INPUT (from an earlier call over another row range of the same
+ * layer); Alg. 1 is skipped and budget is left untouched. */
+#define PROXYATTN_FLAG_KSTAR_GIVEN 0x40u
 
 #define PROXYATTN_OK               0
 #define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */

@@ -21,6 +21,7 @@ FLAG_FORCE_SINK = 0x4
 FLAG_CONSTANT_K = 0x8
 FLAG_DESIGNATED_HEAD = 0x10
 FLAG_TOKEN_MAJOR = 0x20
+FLAG_KSTAR_GIVEN = 0x40
 
 OK = 0
 E_CONFIG = -1
@@ -81,6 +82,7 @@ class Config:
     static_kstar: int = 0
     row_begin: int = 0              # prefill row range (zig-zag row sharding); 0/0 = all rows
     row_end: int = 0
+    kstar_given: bool = False       # estimate: kstar is an input (row-range calls after the first)
     token_major: bool = False       # Q/K/V/O as [N][heads][d] with token strides (0 = packed)
     q_token_stride: int = 0
     kv_token_stride: int = 0
@@ -118,7 +120,8 @@ class Config:
                  | (FLAG_FORCE_SINK if self.force_sink else 0)
                  | (FLAG_CONSTANT_K if self.constant_k else 0)
                  | (FLAG_DESIGNATED_HEAD if self.designated_head else 0)
-                 | (FLAG_TOKEN_MAJOR if self.token_major else 0))
+                 | (FLAG_TOKEN_MAJOR if self.token_major else 0)
+                 | (FLAG_KSTAR_GIVEN if self.kstar_given else 0))
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
                      self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,

@@ -2,6 +2,7 @@
 // workspace carve-up and kernel launches.  No torch types cross this boundary.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <map>
 #include <mutex>
@@ -146,10 +147,10 @@ T* at(void* base, size_t off) {
 }
 
 int run_proxy_from_pooled(const pa::Dims& D, void* Pq, void* Pk, void* ws, const pa::Workspace& W,
-                          float* L, cudaStream_t st) {
+                          float* L, cudaStream_t st, int tr0 = 0, int tr1 = -1) {
     float* lse = at<float>(ws, W.lse);
     if (pa::score_tc_supported(D)) {
-        PA_CUDA(pa::launch_proxy_tc(D, Pq, Pk, at<float>(ws, W.scratch), lse, L, st), "proxy_tc");
+        PA_CUDA(pa::launch_proxy_tc(D, Pq, Pk, at<float>(ws, W.scratch), lse, L, st, tr0, tr1), "proxy_tc");
         return PROXYATTN_OK;
     }
     PA_CUDA(pa::launch_proxy_lse(D, Pq, Pk, lse, st), "proxy_lse");
@@ -252,11 +253,25 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
     void* Pq = at<char>(ws, W.pq);
     void* Pk = at<char>(ws, W.pk);
     float* L = at<float>(ws, W.L);
-    PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st), "pool");
-    rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st);
+    // Row-range estimate (rows [rb, re), zig-zag row sharding): the lists of those rows need
+    // the proxies of their sampled rows and of every key before them, the lse / max-pool of
+    // the 128-row proxy tiles covering them, and Alg. 1 (per head, replicated unless
+    // KSTAR_GIVEN).  The tcgen05 path restricts every stage; the fp32 SIMT path pools all.
+    int tr0 = 0, tr1 = -1;
+    long long q_i0 = 0, i_end = -1;
+    if ((D.rb != 0 || D.re != D.M) && pa::score_tc_supported(D)) {
+        i_end = std::min<long long>(D.Ns, static_cast<long long>(D.re) * D.bs);
+        tr0 = static_cast<int>((static_cast<long long>(D.rb) * D.bs) / 128);
+        tr1 = static_cast<int>((i_end + 127) / 128);
+        q_i0 = static_cast<long long>(tr0) * 128;
+    }
+    PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st, q_i0, i_end), "pool");
+    rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st, tr0, tr1);
     if (rc) return rc;
-    rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
-    if (rc) return rc;
+    if (!(D.flags & PROXYATTN_FLAG_KSTAR_GIVEN)) {
+        rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
+        if (rc) return rc;
+    }
     PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, st), "select");
     return PROXYATTN_OK;
 }

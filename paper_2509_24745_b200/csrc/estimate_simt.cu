@@ -30,12 +30,14 @@ __device__ __forceinline__ void load_row(const T* p, int lane, float (&x)[4], in
 template <typename T>
 __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict__ K,
                             float* __restrict__ qsum, float* __restrict__ ksum,
-                            T* __restrict__ Pq, T* __restrict__ Pk) {
+                            T* __restrict__ Pq, T* __restrict__ Pk, long long q_i0, long long i_end) {
     const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= static_cast<long long>(D.gl) * D.Ns) return;
     const int c = static_cast<int>(w / D.Ns);
     const long long i = w % D.Ns;
+    if (i >= i_end) return;                       // row-range estimate: rows past the range
+    const bool do_q = i >= q_i0;                  // ... and keys only before it
     const long long p = i * D.s;  // first token of each stride window
     const int grp = D.gb + c;
     const int dv = D.d >> 5;
@@ -47,7 +49,7 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
     // fp64 accumulation: the sum of <= 64 bf16 (or fp32) values is then exact, so the proxy
     // rounding below is one RNE of the exact sum, as in the oracle (precision contract c.3).
     double aq[4] = {0., 0., 0., 0.}, ak[4] = {0., 0., 0., 0.};
-    for (int h = h0; h < h1; ++h) {  // fixed ascending order
+    for (int h = h0; h < (do_q ? h1 : h0); ++h) {  // fixed ascending order
         float x[4];
         load_row(Q + q_off(D, h - D.qb, p), lane, x, dv);
 #pragma unroll
@@ -61,9 +63,9 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
     }
     const long long o = w * D.d + lane * dv;
     for (int j = 0; j < dv; ++j) {
-        if (qsum) qsum[o + j] = static_cast<float>(aq[j]);
+        if (qsum && do_q) qsum[o + j] = static_cast<float>(aq[j]);
         if (ksum) ksum[o + j] = static_cast<float>(ak[j]);
-        if (Pq) Pq[o + j] = from_f64<T>(aq[j]);
+        if (Pq && do_q) Pq[o + j] = from_f64<T>(aq[j]);
         if (Pk) Pk[o + j] = from_f64<T>(ak[j]);
     }
 }
@@ -73,7 +75,7 @@ __global__ void pool_kernel(Dims D, const T* __restrict__ Q, const T* __restrict
 __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
                                  const __nv_bfloat16* __restrict__ K, float* __restrict__ qsum,
                                  float* __restrict__ ksum, __nv_bfloat16* __restrict__ Pq,
-                                 __nv_bfloat16* __restrict__ Pk) {
+                                 __nv_bfloat16* __restrict__ Pk, long long q_i0, long long i_end) {
     const int tpr = D.d >> 3;
     const long long gt = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long row = gt / tpr;
@@ -81,12 +83,14 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
     if (row >= static_cast<long long>(D.gl) * D.Ns) return;
     const int c = static_cast<int>(row / D.Ns);
     const long long i = row % D.Ns;
+    if (i >= i_end) return;                       // row-range estimate: rows past the range
+    const bool do_q = i >= q_i0;                  // ... and keys only before it
     const long long p = i * D.s;
     const int grp = D.gb + c;
     // group's query heads / kv heads inside the shard (designated head: only the first)
     const int gqe = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gq;
     const int gke = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD) ? 1 : D.gk;
-    const int h0 = max(grp * D.gq, D.qb), h1 = min(grp * D.gq + gqe, D.qe);
+    const int h0 = max(grp * D.gq, D.qb), h1 = do_q ? min(grp * D.gq + gqe, D.qe) : h0;
     const int k0 = max(grp * D.gk, D.kvb), k1 = min(grp * D.gk + gke, D.kvb + D.Hkvl);
     auto accumulate = [&](const __nv_bfloat16* base, int a, int b, int head0, long long hs, long long ts,
                           double (&acc)[8]) {
@@ -117,7 +121,7 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
     if (qsum) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            qsum[o + q] = static_cast<float>(aq[q]);
+            if (do_q) qsum[o + q] = static_cast<float>(aq[q]);
             ksum[o + q] = static_cast<float>(ak[q]);
         }
     }
@@ -132,7 +136,7 @@ __global__ void pool_bf16_kernel(Dims D, const __nv_bfloat16* __restrict__ Q,
             wq[q] = *reinterpret_cast<const uint32_t*>(&bq);
             wk[q] = *reinterpret_cast<const uint32_t*>(&bk);
         }
-        *reinterpret_cast<uint4*>(Pq + o) = oq;
+        if (do_q) *reinterpret_cast<uint4*>(Pq + o) = oq;
         *reinterpret_cast<uint4*>(Pk + o) = ok;
     }
 }
@@ -389,8 +393,9 @@ __global__ void budget_finalize_kernel(Dims D, const float* __restrict__ bmass,
 __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __restrict__ kstar,
                               int* __restrict__ block_cnt, int* __restrict__ block_idx) {
     extern __shared__ unsigned char sm[];
-    const int c = blockIdx.x / D.M;
-    const int m = D.M - 1 - (blockIdx.x % D.M);  // long rows first
+    const int nr = D.re - D.rb;                  // block rows [rb, re) (all by default)
+    const int c = blockIdx.x / nr;
+    const int m = D.re - 1 - (blockIdx.x % nr);  // long rows first
     const int P = next_pow2(max(m, 1));
     float* key = reinterpret_cast<float*>(sm);
     int* id = reinterpret_cast<int*>(key + next_pow2(D.M));
@@ -451,21 +456,22 @@ inline unsigned blocks_for(long long threads, int bs) {
 }  // namespace
 
 cudaError_t launch_pool(const Dims& D, const void* Q, const void* K, float* qsum, float* ksum,
-                        void* Pq, void* Pk, cudaStream_t st) {
+                        void* Pq, void* Pk, cudaStream_t st, long long q_i0, long long i_end) {
+    if (i_end < 0) i_end = D.Ns;
     const long long thr = static_cast<long long>(D.gl) * D.Ns * 32;
     if (D.fp32)
         pool_kernel<float><<<blocks_for(thr, 256), 256, 0, st>>>(
             D, static_cast<const float*>(Q), static_cast<const float*>(K), qsum, ksum,
-            static_cast<float*>(Pq), static_cast<float*>(Pk));
+            static_cast<float*>(Pq), static_cast<float*>(Pk), q_i0, i_end);
     else if (D.d % 8 == 0 && (qsum == nullptr) == (ksum == nullptr) && (Pq == nullptr) == (Pk == nullptr)) {
         const long long t2 = static_cast<long long>(D.gl) * D.Ns * (D.d / 8);
         pool_bf16_kernel<<<blocks_for(t2, 256), 256, 0, st>>>(
             D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), qsum,
-            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));
+            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk), q_i0, i_end);
     } else
         pool_kernel<__nv_bfloat16><<<blocks_for(thr, 256), 256, 0, st>>>(
             D, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(K), qsum,
-            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk));
+            ksum, static_cast<__nv_bfloat16*>(Pq), static_cast<__nv_bfloat16*>(Pk), q_i0, i_end);
     return cudaGetLastError();
 }
 
@@ -574,7 +580,7 @@ cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* 
                                              static_cast<int>(sm));
         if (e != cudaSuccess) return e;
     }
-    select_kernel<<<D.gl * D.M, 512, sm, st>>>(D, L, kstar, block_cnt, block_idx);
+    select_kernel<<<D.gl * (D.re - D.rb), 512, sm, st>>>(D, L, kstar, block_cnt, block_idx);
     return cudaGetLastError();
 }
 

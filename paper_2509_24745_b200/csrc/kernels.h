@@ -8,8 +8,10 @@ namespace pa {
 
 // A1: pooled group sums at sampled positions.  qsum/ksum (fp32) and/or Pq/Pk (element type
 // of the build, bf16 RNE or fp32) — any of the four may be null.
+// [q_i0, i_end): sampled rows whose Q is pooled; K is pooled for [0, i_end) (row-range
+// estimate); defaults: every row.
 cudaError_t launch_pool(const Dims& D, const void* Q, const void* K, float* qsum, float* ksum,
-                        void* Pq, void* Pk, cudaStream_t st);
+                        void* Pq, void* Pk, cudaStream_t st, long long q_i0 = 0, long long i_end = -1);
 // A1 (staged path): round complete fp32 sums to the proxy element type.
 cudaError_t launch_round_proxies(const Dims& D, const float* qsum, const float* ksum, void* Pq,
                                  void* Pk, cudaStream_t st);
@@ -51,8 +53,9 @@ long long*& attn_trace_ptr();
 // tcgen05 estimation (bf16, d = b = 128, s = 4): A2+A3 and A4 (see score_tc.cu).
 bool score_tc_supported(const Dims& D);
 size_t score_tc_scratch_bytes(const Dims& D);
+// tile rows [tr0, tr1) of 128 sampled rows (tr1 < 0: all); L written for block rows [rb, re)
 cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float* scratch,
-                            float* lse_nat, float* L, cudaStream_t st);
+                            float* lse_nat, float* L, cudaStream_t st, int tr0 = 0, int tr1 = -1);
 cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float* scratch,
                              float* bmass, cudaStream_t st);
 // Device-side validation of block lists; *bad_out (device int) receives the violation count.

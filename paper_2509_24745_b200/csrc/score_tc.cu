@@ -51,6 +51,7 @@ struct ScoreParams {
     int Ns;          // proxy: sampled rows per group
     int N, M;        // budget: tokens, blocks
     int n_tr;        // proxy: tile rows per group (Ns / 128)
+    int tr_lo, tr_hi;   // proxy: tile rows computed (row-range estimate), [0, n_tr) by default
     int n_chunks;    // chunks per tile row (proxy) / per head (budget)
     int r;           // budget: GQA ratio (local head -> local kv head)
     int bs;          // proxy: sampled rows (= keys) per block, b / s
@@ -82,10 +83,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         b_head = prob / p.r;
         diag_u = p.M - 1;
     } else {
-        const int per_group = p.n_tr * p.n_chunks;
+        const int per_group = (p.tr_hi - p.tr_lo) * p.n_chunks;
         prob = blockIdx.x / per_group;
         const int rem = blockIdx.x % per_group;
-        tr = p.n_tr - 1 - rem / p.n_chunks;        // long rows first
+        tr = p.tr_hi - 1 - rem / p.n_chunks;       // long rows first
         const int k = rem % p.n_chunks;
         u_begin = k * kChunk;
         if (u_begin > tr) return;                  // chunk beyond the causal diagonal
@@ -341,9 +342,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
 // lse2[c][i] = m* + log2(sum_k s_k 2^(m_k - m*)) over the row's chunks (fixed order).
 __global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, const float* part_m,
-                                   const float* part_s, float* lse2, float* lse_nat) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= rows) return;
+                                   const float* part_s, float* lse2, float* lse_nat, int i0, int i1) {
+    // rows [i0, i1) of every group (row-range estimate); rows = groups * (i1 - i0)
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= rows) return;
+    const long long i = (t / (i1 - i0)) * Ns + i0 + t % (i1 - i0);
     const int row_in_group = static_cast<int>(i % Ns);
     const int tr = row_in_group / 128;
     const int nk = (tr + kChunk) / kChunk;   // chunks that exist for this tile row
@@ -366,9 +369,9 @@ __global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, con
 __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, float sc2,
                                                                    const float* __restrict__ W,
                                                                    const float* __restrict__ lse2,
-                                                                   float* __restrict__ L) {
+                                                                   float* __restrict__ L, int rb, int re) {
     __shared__ float lse_s[128];
-    const int m = blockIdx.x % M, c = blockIdx.x / M;
+    const int m = rb + blockIdx.x % (re - rb), c = blockIdx.x / (re - rb);   // block rows [rb, re)
     const int i0 = m * bs, i1 = min(i0 + bs, Ns);
     for (int i = threadIdx.x; i < i1 - i0; i += blockDim.x)
         lse_s[i] = lse2[static_cast<long long>(c) * Ns + i0 + i];
@@ -529,7 +532,7 @@ size_t score_tc_scratch_bytes(const Dims& D) {
 // A2 + A3 on tcgen05.  scratch: score_tc_scratch_bytes(D); lse_nat (may be null) receives
 // the natural-log lse for inspection.
 cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float* scratch,
-                            float* lse_nat, float* L, cudaStream_t st) {
+                            float* lse_nat, float* L, cudaStream_t st, int tr0, int tr1) {
     if (!set_smem_attr()) return cudaErrorInvalidValue;
     CUtensorMap ma, mb;
     const uint64_t rows = static_cast<uint64_t>(D.gl) * D.Ns;
@@ -540,6 +543,8 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.M = D.M;
     p.n_tr = static_cast<int>((D.Ns + 127) / 128);
     p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
+    p.tr_lo = tr0;
+    p.tr_hi = tr1 < 0 ? p.n_tr : tr1;
     p.bs = D.bs;
     // Eq. 2 means + 1/sqrt(d) folded into the scale (Z2, Z5), in log2 units.
     p.sc2 = has_flag(D, PROXYATTN_FLAG_DESIGNATED_HEAD)
@@ -551,18 +556,19 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.part_m = part_m;
     p.part_s = part_s;
     p.W = maxpool_pass() ? nullptr : lse2 + static_cast<size_t>(D.gl) * D.Ns;
-    const unsigned grid = static_cast<unsigned>(D.gl) * p.n_tr * p.n_chunks;
+    const unsigned grid = static_cast<unsigned>(D.gl) * (p.tr_hi - p.tr_lo) * p.n_chunks;
     p.mode = kLse;
     score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const long long rws = static_cast<long long>(D.gl) * D.Ns;
+    const int i0 = p.tr_lo * 128, i1 = static_cast<int>(p.tr_hi * 128 < D.Ns ? p.tr_hi * 128 : D.Ns);
+    const long long rws = static_cast<long long>(D.gl) * (i1 - i0);
     lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
-        static_cast<int>(rws), p.n_tr, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat);
+        static_cast<int>(rws), p.n_tr, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat, i0, i1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (!maxpool_pass()) {
-        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * D.M, 256, 0, st>>>(
-            D.M, p.Ns, p.bs, p.sc2, p.W, lse2, L);
+        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
+            D.M, p.Ns, p.bs, p.sc2, p.W, lse2, L, D.rb, D.re);
         return cudaGetLastError();
     }
     const long long cells = static_cast<long long>(D.gl) * D.M * D.M;

@@ -10,10 +10,11 @@
   them and computes the group's block scores itself (replicated, ~0.3 ms at 128K).
 * all_gather of O is for verification only (not part of the timed step).
 * Balanced alternative: zig-zag query-block-row sharding.  Every rank holds
-  the whole layer, runs the (cheap, replicated) estimate for all heads, and computes the
-  attention of two row chunks p and 2P-1-p for all heads; since K_{h,m} grows ~linearly in
-  m for every head (reading Z12), the pair sums to the same work on every rank regardless
-  of how budgets differ between heads, with no cross-GPU traffic at all.
+  the whole layer and computes, for all heads, the block lists (estimate_rows: proxies,
+  scores and selection of its rows only; Alg. 1 replicated) and the attention of two row
+  chunks p and 2P-1-p; since K_{h,m} grows ~linearly in m for every head (reading Z12), the
+  pair sums to the same work on every rank regardless of how budgets differ between heads,
+  with no cross-GPU traffic at all.
 
 The ops are the C-ABI calls of paper_2509_24745_b200 by default; tests inject other ops
 with the same signatures to check the orchestration on CPU with the gloo backend.
@@ -125,6 +126,19 @@ def zigzag_rows(M: int, world: int, rank: int) -> list[tuple[int, int]]:
         if e > b:
             out.append((b, e))
     return sorted(out)
+
+
+def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None):
+    """A1-A6 for the block-row ranges only (zig-zag row sharding): the first call computes
+    Alg. 1's kstar for every head, the others reuse it (KSTAR_GIVEN); block lists are
+    written for the rows of the ranges only.  Returns (kstar, budget, block_cnt, block_idx)."""
+    if estimate is None:
+        from . import _lib
+
+        estimate = _lib.estimate
+    for k, (b, e) in enumerate(ranges):
+        out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=k > 0), Q, K, workspace, out)
+    return out
 
 
 def prefill_rows(cfg, Q, K, V, block_cnt, block_idx, O, ranges, prefill=None):

@@ -402,3 +402,32 @@ def test_score_spikes_wide_dynamic_range():
     check_out(O, ref, fp32=False)
     Od = pa.dense_prefill(cfg, Qd, Kd, Vd)
     check_out(Od, ref, fp32=False)
+
+
+@pytest.mark.parametrize("N", [4096, 3001])
+def test_row_range_estimate_matches_full_bitwise(N):
+    # zig-zag row sharding of the estimate: each rank computes the lists of its rows only
+    # (proxies of its sampled rows and the keys before them, the covering proxy tiles,
+    # selection of its rows), Alg. 1 once per rank; the lists must equal the full estimate's
+    from paper_2509_24745_b200 import shard
+    cfg = llama_small(N=N)
+    Q, K, V, _ = workloads.structured(8, 2, N, 128, seed=13)
+    Qd, Kd, _ = to_dev(Q, K, V)
+    kstar, budget, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    for world in (2, 3):
+        for rank in range(world):
+            rows = shard.zigzag_rows(cfg.M, world, rank)
+            out = (torch.zeros_like(kstar), torch.zeros_like(budget), torch.zeros_like(cnt),
+                   torch.full_like(idx, -7))
+            k2, b2, c2, i2 = shard.estimate_rows(cfg, Qd, Kd, rows, out=out)
+            assert torch.equal(k2, kstar) and torch.equal(b2, budget)
+            for b, e in rows:
+                assert torch.equal(c2[:, b:e], cnt[:, b:e])
+                for h in range(8):
+                    for m in range(b, e):
+                        c = int(cnt[h, m])
+                        assert torch.equal(i2[h, m, :c], idx[h, m, :c])
+            covered = torch.zeros(cfg.M, dtype=torch.bool)
+            for b, e in rows:
+                covered[b:e] = True
+            assert torch.all(c2[:, ~covered.to(c2.device)] == 0)   # other rows untouched
