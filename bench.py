@@ -356,22 +356,41 @@ def run_ours(args):
             torch.cuda.synchronize()
 
     st = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        flush.zero_()
-        estimate()
-        prefill()
-    barrier()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        barrier()
-        for i in range(args.steps):
-            flush.zero_()                    # L2 flush, outside the events
-            ev[i][0].record(st)
+    # The step is replayed from two CUDA graphs (estimate, prefill) captured after warm-up:
+    # the same kernels, without the host launch gaps that would otherwise show at short N
+    # (the head-sharded path all-reduces through NCCL inside the estimate: not captured).
+    use_graph = not args.no_graph and sharding == "rows"
+    if use_graph:
+        st = torch.cuda.Stream(dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+    run_est, run_pre = estimate, prefill
+    with torch.cuda.stream(st):
+        for _ in range(args.warmup):
+            flush.zero_()
             estimate()
-            ev[i][1].record(st)
             prefill()
-            ev[i][2].record(st)
         barrier()
+        if use_graph:
+            g_est, g_pre = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_est, stream=st):
+                estimate()
+            with torch.cuda.graph(g_pre, stream=st):
+                prefill()
+            run_est, run_pre = g_est.replay, g_pre.replay
+            run_est()
+            run_pre()
+            barrier()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            barrier()
+            for i in range(args.steps):
+                flush.zero_()                    # L2 flush, outside the events
+                ev[i][0].record(st)
+                run_est()
+                ev[i][1].record(st)
+                run_pre()
+                ev[i][2].record(st)
+            barrier()
     est_ms = [e[0].elapsed_time(e[1]) for e in ev]
     att_ms = [e[1].elapsed_time(e[2]) for e in ev]
     step_ms = [a + b for a, b in zip(est_ms, att_ms)]
@@ -485,7 +504,8 @@ def run_ours(args):
                    "min_budget_tokens": w["min_budget_tokens"],
                    "parallelism": (f"zig-zag block rows x{ws}" if sharding == "rows" else
                                    f"kv-head groups x{ws}") if ws > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "launch": "CUDA graphs (estimate, prefill)" if use_graph else "eager"},
         "speedup_vs_dense": dense_m / layer_ms,
         "dense_ms": dense_m,
         "estimate_ms": est_m,
@@ -531,6 +551,7 @@ def main():
                          "KV-head-group sharding (all-reduce of pooled sums when g < N)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graphs)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

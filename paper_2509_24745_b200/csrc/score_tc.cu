@@ -31,7 +31,7 @@ constexpr int kBox = 128 * 64 * 2;   // one [128 rows][64 bf16] SWIZZLE_128B box
 constexpr int kTile = 2 * kBox;      // 128 x 128 bf16
 constexpr int kStages = 2;
 constexpr int kThreads = 192;
-constexpr int kChunk = 16;           // key tiles per CTA (proxy) / per CTA (budget)
+constexpr int kChunk = 16;           // default key tiles per CTA (proxy / budget)
 
 enum Mode { kLse = 0, kMaxpool = 1, kBudget = 2 };
 
@@ -52,6 +52,7 @@ struct ScoreParams {
     int N, M;        // budget: tokens, blocks
     int n_tr;        // proxy: tile rows per group (Ns / 128)
     int tr_lo, tr_hi;   // proxy: tile rows computed (row-range estimate), [0, n_tr) by default
+    int chunk;          // key tiles per CTA
     int n_chunks;    // chunks per tile row (proxy) / per head (budget)
     int r;           // budget: GQA ratio (local head -> local kv head)
     int bs;          // proxy: sampled rows (= keys) per block, b / s
@@ -75,8 +76,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (p.mode == kBudget) {
         prob = blockIdx.x / p.n_chunks;
         const int k = blockIdx.x % p.n_chunks;
-        u_begin = k * kChunk;
-        u_end = min(u_begin + kChunk, p.M);
+        u_begin = k * p.chunk;
+        u_end = min(u_begin + p.chunk, p.M);
         a_row = (p.M - 1) * 128;                   // the last block's query rows (Alg. 1)
         a_head = prob;
         b_row0 = 0;
@@ -88,9 +89,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int rem = blockIdx.x % per_group;
         tr = p.tr_hi - 1 - rem / p.n_chunks;       // long rows first
         const int k = rem % p.n_chunks;
-        u_begin = k * kChunk;
+        u_begin = k * p.chunk;
         if (u_begin > tr) return;                  // chunk beyond the causal diagonal
-        u_end = min(u_begin + kChunk, tr + 1);
+        u_end = min(u_begin + p.chunk, tr + 1);
         a_row = prob * p.Ns + tr * 128;
         b_row0 = prob * p.Ns;
         diag_u = tr;
@@ -324,7 +325,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
         }
         if (p.mode == kLse && row_ok) {
-            const int k = u_begin / kChunk;
+            const int k = u_begin / p.chunk;
             const long long o =
                 (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.n_chunks + k;
             p.part_m[o] = m_run;
@@ -341,7 +342,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // lse2[c][i] = m* + log2(sum_k s_k 2^(m_k - m*)) over the row's chunks (fixed order).
-__global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, const float* part_m,
+__global__ void lse_combine_kernel(int rows, int chunk, int Ns, int n_chunks, const float* part_m,
                                    const float* part_s, float* lse2, float* lse_nat, int i0, int i1) {
     // rows [i0, i1) of every group (row-range estimate); rows = groups * (i1 - i0)
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -349,7 +350,7 @@ __global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, con
     const long long i = (t / (i1 - i0)) * Ns + i0 + t % (i1 - i0);
     const int row_in_group = static_cast<int>(i % Ns);
     const int tr = row_in_group / 128;
-    const int nk = (tr + kChunk) / kChunk;   // chunks that exist for this tile row
+    const int nk = (tr + chunk) / chunk;     // chunks that exist for this tile row
     const float* pm = part_m + i * n_chunks;
     const float* ps = part_s + i * n_chunks;
     float mx = -INFINITY;
@@ -359,7 +360,6 @@ __global__ void lse_combine_kernel(int rows, int n_tr, int Ns, int n_chunks, con
     const float l2 = mx + __log2f(s);
     lse2[i] = l2;
     if (lse_nat) lse_nat[i] = l2 * kLn2;
-    (void)n_tr;
 }
 
 // A3 from the window maxima of the lse pass: L[c][m][n] = ln2 * max over the block's valid
@@ -483,6 +483,17 @@ int score_emu() {
 
 // PROXYATTN_MAXPOOL_PASS=1: A3 as a second tcgen05 pass (kMaxpool) instead of from the
 // window maxima the lse pass stores (diagnostics / comparison only).
+// Key tiles per CTA of the score passes; PROXYATTN_SCORE_CHUNK=16/32/64 overrides.
+int score_chunk() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PROXYATTN_SCORE_CHUNK");
+        const int x = e ? atoi(e) : 0;
+        v = (x == 16 || x == 32 || x == 64) ? x : kChunk;
+    }
+    return v;
+}
+
 bool maxpool_pass() {
     static int v = -1;
     if (v < 0) {
@@ -542,7 +553,8 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.Ns = static_cast<int>(D.Ns);
     p.M = D.M;
     p.n_tr = static_cast<int>((D.Ns + 127) / 128);
-    p.n_chunks = (p.n_tr + kChunk - 1) / kChunk;
+    p.chunk = score_chunk();
+    p.n_chunks = (p.n_tr + p.chunk - 1) / p.chunk;
     p.tr_lo = tr0;
     p.tr_hi = tr1 < 0 ? p.n_tr : tr1;
     p.bs = D.bs;
@@ -564,7 +576,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     const int i0 = p.tr_lo * 128, i1 = static_cast<int>(p.tr_hi * 128 < D.Ns ? p.tr_hi * 128 : D.Ns);
     const long long rws = static_cast<long long>(D.gl) * (i1 - i0);
     lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
-        static_cast<int>(rws), p.n_tr, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat, i0, i1);
+        static_cast<int>(rws), p.chunk, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat, i0, i1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (!maxpool_pass()) {
         maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
@@ -594,7 +606,8 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
     p.N = static_cast<int>(D.N);
     p.M = D.M;
     p.r = D.r;
-    p.n_chunks = (D.M + kChunk - 1) / kChunk;
+    p.chunk = score_chunk();
+    p.n_chunks = (D.M + p.chunk - 1) / p.chunk;
     p.sc2 = kLog2e / sqrtf(static_cast<float>(D.d));
     p.part_m = scratch;
     p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
