@@ -397,22 +397,31 @@ def run_ours(args):
     total_ms = float(np.sum(step_ms))
 
     # dense baseline (same run, same inputs), fewer iterations
+    # (launched on `st`, the stream the events are recorded on)
     dense_ms = []
     Od = torch.empty_like(Ql)
-    for i in range(args.warmup + max(2, args.steps // 2)):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        if sharding == "rows" and ws > 1:     # the same row shard as the sparse step
-            for b, e in my_rows:
-                pa.dense_prefill(cfg.replace(row_begin=b, row_end=e), Ql, Kl, Vl, Od)
-        else:
-            pa.dense_prefill(cfg, Ql, Kl, Vl, Od)
-        e1.record(st)
-        torch.cuda.synchronize()
-        if i >= args.warmup:
-            dense_ms.append(e0.elapsed_time(e1))
+    with torch.cuda.stream(st):
+        for i in range(args.warmup + max(2, args.steps // 2)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            if sharding == "rows" and ws > 1:     # the same row shard as the sparse step
+                for b, e in my_rows:
+                    pa.dense_prefill(cfg.replace(row_begin=b, row_end=e), Ql, Kl, Vl, Od)
+            else:
+                pa.dense_prefill(cfg, Ql, Kl, Vl, Od)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                dense_ms.append(e0.elapsed_time(e1))
     dense = float(np.mean(dense_ms))
+
+    # context only: a library dense kernel on the same inputs (torch SDPA, cuDNN backend
+    # first, then FlashAttention), so "speedup vs dense" can be read against a vendor kernel
+    lib_dense = None
+    if ws == 1 and not args.no_lib_dense:
+        lib_dense = library_dense(Ql, Kl, Vl, cfg.r, st, flush, args.warmup, max(2, args.steps // 2))
+    del Od
 
     # max over ranks
     vec = torch.tensor([total_ms / args.steps, float(np.mean(est_ms)), float(np.mean(att_ms)), dense],
@@ -508,6 +517,10 @@ def run_ours(args):
                    "launch": "CUDA graphs (estimate, prefill)" if use_graph else "eager"},
         "speedup_vs_dense": dense_m / layer_ms,
         "dense_ms": dense_m,
+        # A8's algorithmic FLOP (every causal block whole) over the library kernel's time
+        "dense_library": (dict(lib_dense, speedup_vs_library=lib_dense["ms"] / layer_ms,
+                               tflops=4.0 * b * b * d * dense_blocks / (lib_dense["ms"] * 1e-3) / 1e12)
+                          if lib_dense else None),
         "estimate_ms": est_m,
         "prefill_ms": att_m,
         "sparsity": sparsity,
@@ -538,6 +551,39 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def library_dense(Q, K, V, r, st, flush, warmup, iters):
+    """Dense causal attention through torch SDPA (cuDNN, else FlashAttention backend) on
+    the same [H][N][d] bf16 inputs: a vendor kernel for context, never the product path."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    import torch.nn.functional as F
+
+    q = Q.unsqueeze(0)
+    k = K.repeat_interleave(r, dim=0).unsqueeze(0)   # GQA expanded (not timed)
+    v = V.repeat_interleave(r, dim=0).unsqueeze(0)
+    out = None
+    for name, be in (("torch SDPA / cuDNN", SDPBackend.CUDNN_ATTENTION),
+                     ("torch SDPA / FlashAttention", SDPBackend.FLASH_ATTENTION)):
+        try:
+            with torch.cuda.stream(st), sdpa_kernel([be]):
+                ts = []
+                for i in range(warmup + iters):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    F.scaled_dot_product_attention(q, k, v, is_causal=True)
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    if i >= warmup:
+                        ts.append(e0.elapsed_time(e1))
+            out = {"kernel": name, "ms": float(np.mean(ts))}
+            break
+        except Exception as ex:   # backend unavailable for this shape / build
+            out = {"kernel": name, "error": str(ex).splitlines()[0][:160]}
+    del q, k, v
+    torch.cuda.empty_cache()
+    return out if out and "ms" in out else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -551,6 +597,8 @@ def main():
                          "KV-head-group sharding (all-reduce of pooled sums when g < N)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--no-lib-dense", action="store_true",
+                    help="skip the library dense context timing (torch SDPA)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graphs)")
     args = ap.parse_args()
     if args.impl == "reference":
