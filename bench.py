@@ -51,6 +51,16 @@ WORKLOADS = {
                                 head_dim=128, seq_len=65536, block_size=128, stride=4,
                                 n_groups=4, gamma=0.9, min_budget_tokens=2048, seed=0,
                                 preset="qwen-64k"),
+    # SURVEY §8(b) shapes beyond d = b = 128 (same structured inputs, llama-128k preset):
+    # block size 64 (the pair kernel) and head_dim 64 (Llama-3.2-1B: 32 Q / 8 KV heads, d = 64)
+    "llama3.1-8b-attn-128k-b64": dict(name="llama3.1-8b-attn-128k-b64", n_q_heads=32, n_kv_heads=8,
+                                      head_dim=128, seq_len=131072, block_size=64, stride=4,
+                                      n_groups=1, gamma=0.9, min_budget_tokens=0, seed=0,
+                                      preset="llama-128k"),
+    "llama3.2-1b-attn-128k": dict(name="llama3.2-1b-attn-128k", n_q_heads=32, n_kv_heads=8,
+                                  head_dim=64, seq_len=131072, block_size=128, stride=4,
+                                  n_groups=1, gamma=0.9, min_budget_tokens=0, seed=0,
+                                  preset="llama-128k"),
 }
 L2_FLUSH_BYTES = 256 << 20
 # kernels per step: estimate = pool, proxy lse, lse combine, -inf fill, proxy max-pool, budget
@@ -529,7 +539,7 @@ def run_ours(args):
                      "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
                      "traffic": traffic,
                      "peak_source": pk["_source"] + " bf16_tflops_sustained",
-                     "algorithmic": "4*b^2*d FLOP per executed (head,row,block) = 8.39 MFLOP"},
+                     "algorithmic": f"4*b^2*d FLOP per executed (head,row,block) = {4 * b * b * d / 1e6:.2f} MFLOP"},
         "work_share": [x / total_blocks for x in per_rank_blocks],
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -537,7 +547,8 @@ def run_ours(args):
         # the rows it flagged (an empty list at these inputs)
         # estimate: 9 kernels (4 of them Alg. 1); a row-range estimate adds 5 per extra range
         "gpu_launches": (ESTIMATE_KERNELS + 5 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
-                         + len(my_rows) * (2 if kname == "attn_tc8_kernel" else 1)) * args.steps,
+                         + len(my_rows) * ((2 if kname == "attn_tc8_kernel" else 1)
+                                           + (1 if b == 64 else 0))) * args.steps,   # + pair union
         "clocks": clocks,
         # the paper's own numbers, other hardware and workloads: context only
         "paper_context": {"attention_speedup_vs_flashattention": "up to 10.3x at 256K, H800 (P:586)",

@@ -59,8 +59,10 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
         if (c->head_dim % 32 || c->head_dim > 128)
             return fail(PROXYATTN_E_UNSUPPORTED, "FP32_DEBUG needs head_dim %% 32 == 0 and <= 128");
     } else {
-        if (c->head_dim != 128) return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs head_dim == 128");
-        if (c->block_size != 128) return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs block_size == 128");
+        if (c->head_dim != 64 && c->head_dim != 128)
+            return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs head_dim 64 or 128");
+        if (c->block_size != 64 && c->block_size != 128)
+            return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs block_size 64 or 128");
     }
     if (c->seq_len / c->block_size > (1 << 20)) return fail(PROXYATTN_E_UNSUPPORTED, "too many blocks");
     D.Hq = c->n_q_heads;
@@ -298,10 +300,14 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
     } else {
         int variant = pa::attn_variant(block_cnt == nullptr);
-        if (D.tok) {   // only the persistent kernel reads token-major tensors (3-D TMA maps)
+        // only the persistent kernel reads token-major tensors (3-D TMA maps) and has the
+        // d = 64 / b = 64 instantiations
+        const bool only8 = D.tok || D.d != 128 || D.b != 128;
+        if (only8) {
             if (block_cnt == nullptr) variant = 8;
             if (variant != 8)
-                return fail(PROXYATTN_E_UNSUPPORTED, "PROXYATTN_FLAG_TOKEN_MAJOR needs attention variant 8");
+                return fail(PROXYATTN_E_UNSUPPORTED,
+                            "token-major layouts and head_dim / block_size 64 need attention variant 8");
         }
         if ((variant == 4 || variant == 5) && (D.N % D.b || D.rb != 0 || D.re != D.M))
             return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0 and all rows");

@@ -21,8 +21,20 @@
 //   warps 4-7   epilogue: O (TMEM) * 1/l -> bf16 -> global; releases O for the next row
 //   warps 8-11  softmax of stream 0, warps 12-15 of stream 1 (thread = row = TMEM lane)
 // TMEM (512 columns): O [0,128)  S_0 [128,256)  S_1 [256,384)  P_0 [384,448)  P_1 [448,512).
+//
+// Shapes (template <kEmu, kD, kB>): head_dim kD in {64, 128}, block kB in {64, 128}.  The
+// 128 query rows of a work unit are the 128 TMEM lanes.  kB = 128: one (head, block row).
+// kB = 64: a PAIR of query heads of the same KV head on the same 64-row block row (lanes
+// 0-63 head 2p, 64-127 head 2p+1), so every S = Q K^T tile is still M = 128 (an M = 64
+// tcgen05.mma costs the issue slot of an M = 128 one).  The pair walks the UNION of its two
+// ascending lists (the selection's lists of one group are nested, so the union is the
+// longer list); a block that is not in a half's list gets P = 0 for that half.  The fixed
+// reference of a half is the max over its member blocks among the two first blocks, else
+// (neither is a member) the raw max of those blocks; rows whose sum would then underflow
+// (l < 2^-60) or overflow are re-run by the exact launch, as for kB = 128.
 #include <cuda_bf16.h>
 
+#include <climits>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -38,7 +50,7 @@ namespace {
 
 constexpr int kTileRows = 128;
 constexpr int kBox = kTileRows * 64 * 2;   // 16 KB: [128 rows][64 bf16] SW128 box
-constexpr int kTile = 2 * kBox;            // 32 KB: a 128 x 128 bf16 tile
+constexpr float kUnderflow = -60.0f;       // log2 floor of a row sum under a non-attained reference
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 constexpr int kItemSlots = 4;
@@ -69,11 +81,20 @@ struct __align__(8) Bars8 {
     Item items[kItemSlots];
     uint32_t tmem_base;
     float red[2][128];       // first-block / true row max exchange between the streams
+    float red_u[2][128];     // kB = 64: the same without the membership mask
     float lsum[2][2][128];   // [item parity][stream][row] row sums for the epilogue
 };
 
-constexpr size_t kSmemBytes = 1024 + kTile * (1 + kKStages + kVStages) + sizeof(Bars8);
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+template <int kD, int kB>
+struct Shape {
+    static constexpr int kQTile = (kD / 64) * kBox;      // Q: 128 rows x kD (64-col boxes at kBox)
+    static constexpr int kKBox = kB * 128;               // K / V: [kB rows][64 bf16] box
+    static constexpr int kKTile = (kD / 64) * kKBox;
+    static constexpr int kChunks = kB / 32;               // 32-column S chunks per block
+    static constexpr int kHalves = kB / 64;               // P halves (4 PV MMAs of K = 16 each)
+    static constexpr size_t kSmem = 1024 + kQTile + kKTile * (kKStages + kVStages) + sizeof(Bars8);
+    static_assert(kSmem <= 232448, "shared memory budget");
+};
 
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
@@ -83,25 +104,50 @@ struct Sched {        // device-side scheduler state of one launch pair (zeroed 
     int pad;
 };
 
-template <int kEmu>   // of every 8 key-column pairs, kEmu use the FMA-pipe exp2 (ex2_poly2)
+// Block-list walk of a kB = 64 work unit: the ascending union of the pair's two lists, with
+// each element's membership (bit 0: head A = lanes 0-63, bit 1: head B = lanes 64-127).
+struct PairWalk {
+    const int* a;
+    const int* b;
+    int ca, cb, pa, pb, j;
+    bool dense;
+    __device__ __forceinline__ int next(int& mem) {
+        if (dense) {
+            mem = cb > 0 ? 3 : 1;
+            return j++;
+        }
+        const int x = pa < ca ? __ldg(a + pa) : INT_MAX;
+        const int y = pb < cb ? __ldg(b + pb) : INT_MAX;
+        const int n = min(x, y);
+        mem = (x == n ? 1 : 0) | (y == n ? 2 : 0);
+        pa += (x == n);
+        pb += (y == n);
+        return n;
+    }
+};
+
+template <int kEmu, int kD, int kB>   // kEmu: of every 8 key-column pairs, kEmu use the FMA-pipe exp2
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
-                int* flagged, int exact, long long o_hs, long long o_ts) {
+                int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt) {
+    using Sh = Shape<kD, kB>;
+    constexpr bool kPair = (kB == 64);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sQ = smem;
-    uint8_t* sK = smem + kTile;
-    uint8_t* sV = smem + kTile * (1 + kKStages);
-    Bars8* bars = reinterpret_cast<Bars8*>(smem + kTile * (1 + kKStages + kVStages));
+    uint8_t* sK = smem + Sh::kQTile;
+    uint8_t* sV = sK + Sh::kKTile * kKStages;
+    Bars8* bars = reinterpret_cast<Bars8*>(sV + Sh::kKTile * kVStages);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nrows = row_hi - row_lo;
-    const int per_kv = r * nrows;
+    const int npairs = kPair ? (r + 1) >> 1 : r;       // work units per (kv head, block row)
+    const int per_kv = npairs * nrows;
     const int n_items = exact ? sched->n_flagged : n_total;
     const bool dense = (block_cnt == nullptr);
     const int passes = exact ? 2 : 1;   // exact: max sweep, then the fixed pass
@@ -139,12 +185,20 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
 
-    // item decode (same order as attn_tc7's grid: kv-head major, heavy rows first)
-    auto decode = [&](int item, int& hl, int& m, int& kvl) {
+    // item decode (kv-head major, heavy rows first): kB = 128 -> head h0 (h1 = -1);
+    // kB = 64 -> the pair (h0, h1), h1 = -1 when r is odd and the pair is the last one
+    auto decode = [&](int item, int& h0, int& h1, int& m, int& kvl) {
         kvl = item / per_kv;
         const int rem = item % per_kv;
-        m = row_hi - 1 - rem / r;
-        hl = kvl * r + rem % r;
+        m = row_hi - 1 - rem / npairs;
+        if (kPair) {
+            const int p = rem % npairs;
+            h0 = kvl * r + 2 * p;
+            h1 = (2 * p + 1 < r) ? h0 + 1 : -1;
+        } else {
+            h0 = kvl * r + rem % r;
+            h1 = -1;
+        }
     };
     auto get_item = [&](int it) -> Item {         // consumers: wait for slot, read, release
         const int slot = it % kItemSlots;
@@ -156,6 +210,16 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     };
     auto list_of = [&](int hl, int m) -> const int* {
         return dense ? nullptr : block_idx + (static_cast<long long>(hl) * M + m) * M;
+    };
+    auto walk_of = [&](int h0, int h1, int m) -> PairWalk {
+        PairWalk w;
+        w.dense = dense;
+        w.a = list_of(h0, m);
+        w.b = h1 >= 0 ? list_of(h1, m) : nullptr;
+        w.ca = dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(h0) * M + m);
+        w.cb = h1 < 0 ? 0 : dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(h1) * M + m);
+        w.pa = w.pb = w.j = 0;
+        return w;
     };
 
     if (warp < 4) {
@@ -173,28 +237,45 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     Item x{-1, 0};
                     if (k < n_items) {
                         x.item = exact ? flagged[k] : k;
-                        int hl, m, kvl;
-                        decode(x.item, hl, m, kvl);
-                        x.cnt = dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(hl) * M + m);
+                        int h0, h1, m, kvl;
+                        decode(x.item, h0, h1, m, kvl);
+                        x.cnt = dense ? m + 1
+                              : kPair ? __ldg(ucnt + x.item)
+                                      : __ldg(block_cnt + static_cast<long long>(h0) * M + m);
                     }
                     bars->items[slot] = x;
                     mbar_arrive(&bars->item_full[slot]);   // release semantics publish x
                     if (x.item < 0) break;
-                    int hl, m, kvl;
-                    decode(x.item, hl, m, kvl);
-                    const int* list = list_of(hl, m);
+                    int h0, h1, m, kvl;
+                    decode(x.item, h0, h1, m, kvl);
                     if (it > 0) mbar_wait(&bars->q_empty, (it - 1) & 1);   // last S of it-1 done
-                    mbar_expect_tx(&bars->q_full, kTile);
-                    tma_load_3d(sQ, &tmQ, &bars->q_full, 0, m * kTileRows, hl);
-                    tma_load_3d(sQ + kBox, &tmQ, &bars->q_full, 64, m * kTileRows, hl);
+                    if (kPair) {   // two 64-row head slices stacked in the 128-row tile
+                        mbar_expect_tx(&bars->q_full, (h1 >= 0 ? 2 : 1) * (kD / 64) * (kBox / 2));
+#pragma unroll
+                        for (int ch = 0; ch < kD / 64; ++ch) {
+                            tma_load_3d(sQ + ch * kBox, &tmQ, &bars->q_full, ch * 64, m * kB, h0);
+                            if (h1 >= 0)
+                                tma_load_3d(sQ + ch * kBox + kBox / 2, &tmQ, &bars->q_full, ch * 64, m * kB, h1);
+                        }
+                    } else {
+                        mbar_expect_tx(&bars->q_full, Sh::kQTile);
+#pragma unroll
+                        for (int ch = 0; ch < kD / 64; ++ch)
+                            tma_load_3d(sQ + ch * kBox, &tmQ, &bars->q_full, ch * 64, m * kTileRows, h0);
+                    }
+                    const int* list = list_of(h0, m);
                     for (int pass = 0; pass < passes; ++pass) {
+                        PairWalk w = walk_of(h0, h1, m);
                         for (int j = 0; j < x.cnt; ++j, ++gk) {
                             const int st = gk % kKStages;
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
-                            const int n = dense ? j : __ldg(list + j);
-                            mbar_expect_tx(&bars->k_full[st], kTile);
-                            tma_load_3d(sK + st * kTile, &tmK, &bars->k_full[st], 0, n * kTileRows, kvl);
-                            tma_load_3d(sK + st * kTile + kBox, &tmK, &bars->k_full[st], 64, n * kTileRows, kvl);
+                            int mem;
+                            const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                            mbar_expect_tx(&bars->k_full[st], Sh::kKTile);
+#pragma unroll
+                            for (int ch = 0; ch < kD / 64; ++ch)
+                                tma_load_3d(sK + st * Sh::kKTile + ch * Sh::kKBox, &tmK, &bars->k_full[st],
+                                            ch * 64, n * kB, kvl);
                         }
                     }
                 }
@@ -207,23 +288,27 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const Item x = get_item(it);
                 if (x.item < 0) break;
                 if (lane == 0) {
-                    int hl, m, kvl;
-                    decode(x.item, hl, m, kvl);
-                    const int* list = list_of(hl, m);
+                    int h0, h1, m, kvl;
+                    decode(x.item, h0, h1, m, kvl);
+                    const int* list = list_of(h0, m);
+                    PairWalk w = walk_of(h0, h1, m);
                     for (int j = 0; j < x.cnt; ++j, ++gv) {
                         const int st = gv % kVStages;
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
-                        const int n = dense ? j : __ldg(list + j);
-                        mbar_expect_tx(&bars->v_full[st], kTile);
-                        tma_load_3d(sV + st * kTile, &tmV, &bars->v_full[st], 0, n * kTileRows, kvl);
-                        tma_load_3d(sV + st * kTile + kBox, &tmV, &bars->v_full[st], 64, n * kTileRows, kvl);
+                        int mem;
+                        const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                        mbar_expect_tx(&bars->v_full[st], Sh::kKTile);
+#pragma unroll
+                        for (int ch = 0; ch < kD / 64; ++ch)
+                            tma_load_3d(sV + st * Sh::kKTile + ch * Sh::kKBox, &tmV, &bars->v_full[st],
+                                        ch * 64, n * kB, kvl);
                     }
                 }
                 __syncwarp();
             }
         } else if (warp == 1) {
             // -------------------------------------------------------- S issuer --
-            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+            constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kB, 0, 0);
             const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
             const bool leader = elect_one();
@@ -241,11 +326,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         mbar_wait(&bars->k_full[st], (gk / kKStages) & 1);
                         tc_fence_after();
                         if (leader) {
-                            const uint64_t b0 = dk + (st * kTile >> 4);
+                            const uint64_t b0 = dk + (st * Sh::kKTile >> 4);
 #pragma unroll
-                            for (int kk = 0; kk < 8; ++kk) {
-                                const uint32_t off = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
-                                umma_ss(tbase + kColS + s * 128, dq + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
+                            for (int kk = 0; kk < kD / 16; ++kk) {
+                                const uint32_t offq = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
+                                const uint32_t offk = ((kk >> 2) * Sh::kKBox + (kk & 3) * 32) >> 4;
+                                umma_ss(tbase + kColS + s * 128, dq + offq, b0 + offk, idesc_qk, kk > 0 ? 1u : 0u);
                             }
                             tc_commit(&bars->k_empty[st]);
                             tc_commit(&bars->s_full[s]);
@@ -258,8 +344,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             }
         } else {
             // ------------------------------------------------------- PV issuer --
-            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-            const uint64_t dv = sdesc_sw128(smem_u32(sV), kBox, 1024);
+            constexpr uint32_t idesc_pv = idesc_bf16_f32(128, kD, 0, 1);
+            const uint64_t dv = sdesc_sw128(smem_u32(sV), Sh::kKBox, 1024);
             const bool leader = elect_one();
             int gv = 0, gp[2] = {0, 0};
             for (int it = 0;; ++it) {
@@ -271,11 +357,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     mbar_wait(&bars->v_full[st], (gv / kVStages) & 1);
                     if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);   // O read out
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
+                    for (int half = 0; half < Sh::kHalves; ++half) {
                         mbar_wait(&bars->p_full[s][half], gp[s] & 1);
                         tc_fence_after();
                         if (leader) {
-                            const uint64_t b0 = dv + (st * kTile >> 4);
+                            const uint64_t b0 = dv + (st * Sh::kKTile >> 4);
 #pragma unroll
                             for (int k4 = 0; k4 < 4; ++k4) {
                                 const int kk = half * 4 + k4;
@@ -305,28 +391,30 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         for (int it = 0;; ++it) {
             const Item x = get_item(it);
             if (x.item < 0) break;
-            int hl, m, kvl;
-            decode(x.item, hl, m, kvl);
+            int h0, h1, m, kvl;
+            decode(x.item, h0, h1, m, kvl);
+            const int hl = (kPair && rr >= 64) ? h1 : h0;         // the row's head (-1: none)
+            const long long pos = static_cast<long long>(m) * kB + (rr & (kB - 1));
             mbar_wait(&bars->l_ready[it & 1], (it >> 1) & 1);
             const float l0 = bars->lsum[it & 1][0][rr], l1 = bars->lsum[it & 1][1][rr];
             const float inv = 1.f / (l0 + l1);
             if (!exact) {   // a row whose P exceeded the bound (l = +inf marker): exact re-run
-                const bool bad = !(l0 + l1 <= 2.f * exp2f(kOverflow));
+                bool bad = !(l0 + l1 <= 2.f * exp2f(kOverflow));
+                if (kPair) bad = bad || (hl >= 0 && l0 + l1 < exp2f(kUnderflow));
                 if (__any_sync(0xffffffffu, bad) && lane == 0)
                     flagged[atomicAdd(&sched->n_flagged, 1)] = x.item;   // <= 4 duplicates, benign
             }
             mbar_wait(&bars->o_final, it & 1);
             tc_fence_after();
-            const bool row_valid = static_cast<long long>(m) * kTileRows + rr < N;
-            uint4* dst = reinterpret_cast<uint4*>(
-                O + static_cast<long long>(hl) * o_hs + (static_cast<long long>(m) * kTileRows + rr) * o_ts);
+            const bool row_valid = hl >= 0 && pos < N;
+            uint4* dst = reinterpret_cast<uint4*>(O + static_cast<long long>(hl < 0 ? 0 : hl) * o_hs + pos * o_ts);
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
+            for (int h2 = 0; h2 < kD / 64; ++h2) {
                 uint32_t o[2][32];
                 tmem_ld32(tO + h2 * 64, o[0]);
                 tmem_ld32(tO + h2 * 64 + 32, o[1]);
                 tmem_ld_wait();
-                if (h2 == 1) {
+                if (h2 == kD / 64 - 1) {
                     tc_fence_before();
                     mbar_arrive(&bars->o_free);           // the next row's PV may overwrite O
                 }
@@ -352,6 +440,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const int s = (warp - 8) >> 2;                  // stream
         const int quarter = warp & 3;
         const int rr = quarter * 32 + lane;
+        const int qrow = rr & (kB - 1);                 // query row within the block
+        const int hp = kPair ? (quarter >> 1) : 0;      // kB = 64: this warp's head of the pair
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const uint32_t tS = tbase + lane_off + kColS + s * 128;
         const uint32_t tP = tbase + lane_off + kColP + s * 64;
@@ -390,7 +480,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         auto mask_chunk = [&](uint32_t (&x)[32], int c) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-                if (c * 32 + e > rr) x[e] = 0xff800000u;
+                if (c * 32 + e > qrow) x[e] = 0xff800000u;
         };
         auto release_p = [&](int half) {
             tmem_st_wait();
@@ -413,106 +503,144 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             mbar_arrive(&bars->s_free[s]);
         };
         // P of the block in S_s (already landed), with the reference known: chunked TMEM
-        // loads overlapped with the exp2s; S released once its last chunk is in registers
-        auto block_exps = [&](float m_ref, bool diag) -> float {
+        // loads overlapped with the exp2s; S released once its last chunk is in registers.
+        // A block outside this half's list (kB = 64 pairs) contributes P = 0.
+        auto block_exps = [&](float m_ref, bool diag, bool mine) -> float {
+            if (kPair && !mine) {
+                release_s();
+                if (gp > 0) {
+                    mbar_wait(&bars->p_free[s], (gp - 1) & 1);
+                    tc_fence_after();
+                }
+                uint32_t z[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) z[e] = 0u;
+#pragma unroll
+                for (int c = 0; c < Sh::kChunks; ++c) tmem_st16(tP + c * 16, z);
+#pragma unroll
+                for (int h = 0; h < Sh::kHalves; ++h) release_p(h);
+                ++gp;
+                return 0.f;
+            }
             const uint64_t nm2 = f2_pack(-m_ref, -m_ref);
             uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
-            uint32_t xa[32], xb[32];
-            tmem_ld32(tS, xa);
-            tmem_ld_wait_regs(xa);
-            tmem_ld32(tS + 32, xb);
-            if (diag) mask_chunk(xa, 0);
-            p_chunk(xa, nm2, ls, tP, true);
-            tmem_ld_wait_regs(xb);
-            tmem_ld32(tS + 64, xa);
-            if (diag) mask_chunk(xb, 1);
-            p_chunk(xb, nm2, ls, tP + 16, false);
-            release_p(0);
-            tmem_ld_wait_regs(xa);
-            tmem_ld32(tS + 96, xb);
-            if (diag) mask_chunk(xa, 2);
-            p_chunk(xa, nm2, ls, tP + 32, false);
-            tmem_ld_wait_regs(xb);
-            release_s();
-            if (diag) mask_chunk(xb, 3);
-            p_chunk(xb, nm2, ls, tP + 48, false);
-            release_p(1);
+            uint32_t xb[2][32];
+            tmem_ld32(tS, xb[0]);
+#pragma unroll
+            for (int c = 0; c < Sh::kChunks; ++c) {
+                tmem_ld_wait_regs(xb[c & 1]);
+                if (c + 1 < Sh::kChunks) tmem_ld32(tS + 32 * (c + 1), xb[(c + 1) & 1]);
+                else release_s();
+                if (diag) mask_chunk(xb[c & 1], c);
+                p_chunk(xb[c & 1], nm2, ls, tP + 16 * c, c == 0);
+                if (c & 1) release_p(c >> 1);
+            }
             ++gp;
             return sum_ls(ls);
         };
         // row max of the block in S_s (raw logits), chunked; S stays in TMEM
         auto block_max = [&](bool diag) -> float {
             float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            uint32_t xa[32], xb[32];
+            uint32_t xb[2][32];
             auto fold = [&](uint32_t (&x)[32], int c) {
                 if (diag) mask_chunk(x, c);
 #pragma unroll
                 for (int e = 0; e < 32; e += 2)
                     mx[(e >> 1) & 3] = fmaxf(mx[(e >> 1) & 3], fmaxf(__uint_as_float(x[e]), __uint_as_float(x[e + 1])));
             };
-            tmem_ld32(tS, xa);
-            tmem_ld_wait_regs(xa);
-            tmem_ld32(tS + 32, xb);
-            fold(xa, 0);
-            tmem_ld_wait_regs(xb);
-            tmem_ld32(tS + 64, xa);
-            fold(xb, 1);
-            tmem_ld_wait_regs(xa);
-            tmem_ld32(tS + 96, xb);
-            fold(xa, 2);
-            tmem_ld_wait_regs(xb);
-            fold(xb, 3);
+            tmem_ld32(tS, xb[0]);
+#pragma unroll
+            for (int c = 0; c < Sh::kChunks; ++c) {
+                tmem_ld_wait_regs(xb[c & 1]);
+                if (c + 1 < Sh::kChunks) tmem_ld32(tS + 32 * (c + 1), xb[(c + 1) & 1]);
+                fold(xb[c & 1], c);
+            }
             return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         };
-        auto exchange_max = [&](float v) {
-            bars->red[s][rr] = v;
+        // the two streams' maxima -> the shared reference (log2 units); kB = 64: the max over
+        // member blocks `vm`, else (no member among the first blocks) the raw max `vu`
+        auto exchange_max = [&](float vm, float vu) {
+            bars->red[s][rr] = vm;
+            if (kPair) bars->red_u[s][rr] = vu;
             softmax_bar();
-            const float r2 = fmaxf(bars->red[0][rr], bars->red[1][rr]) * scale_log2;
+            float r2 = fmaxf(bars->red[0][rr], bars->red[1][rr]);
+            if (kPair && r2 == -INFINITY) r2 = fmaxf(bars->red_u[0][rr], bars->red_u[1][rr]);
             softmax_bar();
-            return r2;
+            return r2 * scale_log2;
         };
 
         for (int it = 0;; ++it) {
             const Item x = get_item(it);
             if (x.item < 0) break;
-            int hl, m, kvl;
-            decode(x.item, hl, m, kvl);
-            const int* list = list_of(hl, m);
+            int h0, h1, m, kvl;
+            decode(x.item, h0, h1, m, kvl);
+            const int* list = list_of(h0, m);
             const int my_cnt = (x.cnt - s + 1) >> 1;   // blocks j = s, s + 2, ...
+            // kB = 64: this stream's positions of the pair's union walk, with membership
+            PairWalk w = walk_of(h0, h1, m);
+            int dummy;
+            auto next_mine = [&](bool& mine) -> int {
+                int mem;
+                const int n = w.next(mem);
+                w.next(dummy);                          // the other stream's position
+                mine = (mem >> hp) & 1;
+                return n;
+            };
+            if (kPair && s == 1) w.next(dummy);
             auto block_n = [&](int js) { return dense ? 2 * js + s : __ldg(list + 2 * js + s); };
             float l = 0.f;
             float m_ref;
             if (!exact) {
                 // reference = max of the two streams' first blocks (read twice from TMEM)
-                float rmax = -INFINITY;
-                const bool diag0 = (my_cnt > 0) && block_n(0) == m;
+                float rmax = -INFINITY, rmax_u = -INFINITY;
+                bool mine0 = true;
+                int n0 = -1;
                 if (my_cnt > 0) {
+                    n0 = kPair ? next_mine(mine0) : block_n(0);
                     wait_s();
-                    rmax = block_max(diag0);
+                    rmax_u = block_max(n0 == m);
+                    rmax = mine0 ? rmax_u : -INFINITY;
                 }
-                m_ref = exchange_max(rmax);
+                m_ref = exchange_max(rmax, rmax_u);
                 xhi = -INFINITY;
-                if (my_cnt > 0) l = block_exps(m_ref, diag0);
-                int n_next = (my_cnt > 1) ? block_n(1) : 0;
-                for (int js = 1; js < my_cnt; ++js) {
-                    const int n = n_next;
-                    if (js + 1 < my_cnt) n_next = block_n(js + 1);
-                    wait_s();
-                    l += block_exps(m_ref, n == m);
+                if (my_cnt > 0) l = block_exps(m_ref, n0 == m, mine0);
+                if (kPair) {
+                    for (int js = 1; js < my_cnt; ++js) {
+                        bool mine;
+                        const int n = next_mine(mine);
+                        wait_s();
+                        l += block_exps(m_ref, n == m, mine);
+                    }
+                } else {
+                    int n_next = (my_cnt > 1) ? block_n(1) : 0;
+                    for (int js = 1; js < my_cnt; ++js) {
+                        const int n = n_next;
+                        if (js + 1 < my_cnt) n_next = block_n(js + 1);
+                        wait_s();
+                        l += block_exps(m_ref, n == m, true);
+                    }
                 }
                 if (!(l <= exp2f(kOverflow)) || xhi > kOverflow) l = INFINITY;   // flag the row
             } else {
-                // exact: the row's true max first (S only), then the fixed pass
+                // exact: the row's true max over its own blocks first (S only), then the fixed pass
                 float tmax = -INFINITY;
                 for (int js = 0; js < my_cnt; ++js) {
+                    bool mine = true;
+                    const int n = kPair ? next_mine(mine) : block_n(js);
                     wait_s();
-                    tmax = fmaxf(tmax, block_max(block_n(js) == m));
+                    if (mine) tmax = fmaxf(tmax, block_max(n == m));
                     release_s();
                 }
-                m_ref = exchange_max(tmax);
+                m_ref = exchange_max(tmax, tmax);
+                if (kPair) {
+                    w = walk_of(h0, h1, m);
+                    if (s == 1) w.next(dummy);
+                }
                 for (int js = 0; js < my_cnt; ++js) {
+                    bool mine = true;
+                    const int n = kPair ? next_mine(mine) : block_n(js);
                     wait_s();
-                    l += block_exps(m_ref, block_n(js) == m);
+                    l += block_exps(m_ref, n == m, mine);
                 }
             }
             bars->lsum[it & 1][s][rr] = l;
@@ -528,10 +656,47 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     }
 }
 
-// Per-stream scheduler state + flagged-row list (grown on demand, never freed).
+// kB = 64: union size of each pair's two lists, |A| + |B| - |A n B| (a warp per work unit;
+// the elements of A are searched in the ascending B).  Same item order as the kernel.
+__global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* __restrict__ block_idx,
+                                  int M, int r, int row_lo, int row_hi, int n_items, int* __restrict__ ucnt) {
+    const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (item >= n_items) return;
+    const int nrows = row_hi - row_lo, npairs = (r + 1) >> 1;
+    const int kvl = item / (npairs * nrows), rem = item % (npairs * nrows);
+    const int m = row_hi - 1 - rem / npairs, p = rem % npairs;
+    const int h0 = kvl * r + 2 * p;
+    const int ca = __ldg(block_cnt + static_cast<long long>(h0) * M + m);
+    if (2 * p + 1 >= r) {
+        if (lane == 0) ucnt[item] = ca;
+        return;
+    }
+    const int cb = __ldg(block_cnt + static_cast<long long>(h0 + 1) * M + m);
+    const int* A = block_idx + (static_cast<long long>(h0) * M + m) * M;
+    const int* B = block_idx + (static_cast<long long>(h0 + 1) * M + m) * M;
+    int inter = 0;
+    for (int i = lane; i < ca; i += 32) {
+        const int v = __ldg(A + i);
+        int lo = 0, hi = cb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(B + mid) < v) lo = mid + 1;
+            else hi = mid;
+        }
+        inter += (lo < cb && __ldg(B + lo) == v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    if (lane == 0) ucnt[item] = ca + cb - inter;
+}
+
+// Per-stream scheduler state + flagged-row list + kB = 64 union counts (grown on demand,
+// never freed).
 struct SchedBuf {
     Sched* sched = nullptr;
     int* flagged = nullptr;
+    int* ucnt = nullptr;
     size_t cap = 0;
 };
 
@@ -543,55 +708,88 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
     std::lock_guard<std::mutex> lock(mu);
     SchedBuf& b = bufs[{dev, st}];
     if (!b.sched && cudaMalloc(&b.sched, sizeof(Sched)) != cudaSuccess) return nullptr;
-    if (b.cap < 4 * n_items) {   // each row can be appended by up to 4 epilogue warps
+    if (b.cap < n_items) {   // each row can be appended by up to 4 epilogue warps
         if (b.flagged) cudaFree(b.flagged);
-        b.flagged = nullptr;
+        if (b.ucnt) cudaFree(b.ucnt);
+        b.flagged = b.ucnt = nullptr;
+        b.cap = 0;
         if (cudaMalloc(&b.flagged, 4 * n_items * sizeof(int)) != cudaSuccess) return nullptr;
-        b.cap = 4 * n_items;
+        if (cudaMalloc(&b.ucnt, n_items * sizeof(int)) != cudaSuccess) return nullptr;
+        b.cap = n_items;
     }
     return &b;
+}
+
+using AttnKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, __nv_bfloat16*,
+                            const int*, const int*, int, int, int, float, int, int, int, Sched*, int*,
+                            int, long long, long long, const int*);
+
+template <int kD, int kB, int kEmu>
+AttnKernel kernel_with_attr() {
+    static bool set = false;
+    if (!set) {
+        if (cudaFuncSetAttribute(attn_tc8_kernel<kEmu, kD, kB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Shape<kD, kB>::kSmem)) != cudaSuccess)
+            return nullptr;
+        set = true;
+    }
+    return attn_tc8_kernel<kEmu, kD, kB>;
 }
 
 }  // namespace
 
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
+    if (!((D.d == 64 || D.d == 128) && (D.b == 64 || D.b == 128))) return cudaErrorInvalidValue;
     CUtensorMap mq, mk, mv;
-    if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128) ||
-        !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128) ||
-        !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128))
+    if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, D.b, D.d) ||
+        !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d) ||
+        !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d))
         return cudaErrorInvalidValue;
     static int emu = -1;
-    if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe
+    if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe (d = b = 128)
         const char* e = getenv("PROXYATTN_EXP_EMU");
         emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
     }
-    auto kern = emu == 0 ? attn_tc8_kernel<0> : emu == 1 ? attn_tc8_kernel<1>
-              : emu == 2 ? attn_tc8_kernel<2> : emu == 3 ? attn_tc8_kernel<3> : attn_tc8_kernel<4>;
-    static bool attr_set[5] = {false, false, false, false, false};
-    if (!attr_set[emu]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBytes));
-        if (e != cudaSuccess) return e;
-        attr_set[emu] = true;
+    AttnKernel kern = nullptr;
+    if (D.d == 128 && D.b == 128) {
+        kern = emu == 0 ? kernel_with_attr<128, 128, 0>() : emu == 1 ? kernel_with_attr<128, 128, 1>()
+             : emu == 2 ? kernel_with_attr<128, 128, 2>() : emu == 3 ? kernel_with_attr<128, 128, 3>()
+                                                          : kernel_with_attr<128, 128, 4>();
+    } else if (D.d == 128) {
+        kern = kernel_with_attr<128, 64, 2>();
+    } else if (D.b == 128) {   // d = 64: half the tensor work per exp2 -> more of them on the FMA pipe
+        kern = kernel_with_attr<64, 128, 4>();
+    } else {
+        kern = kernel_with_attr<64, 64, 4>();
     }
+    if (!kern) return cudaErrorInvalidValue;
     int dev = 0, n_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    const size_t n_items = static_cast<size_t>(D.Hl) * static_cast<size_t>(D.re - D.rb);
+    const bool pair = D.b == 64;
+    const int units = pair ? D.Hkvl * ((D.r + 1) / 2) : D.Hl;   // work units per block row
+    const size_t n_items = static_cast<size_t>(units) * static_cast<size_t>(D.re - D.rb);
     SchedBuf* sb = sched_for(st, n_items);
     if (!sb) return cudaErrorMemoryAllocation;
     cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);
     if (e != cudaSuccess) return e;
+    if (pair && block_cnt) {
+        pair_union_kernel<<<static_cast<unsigned>((n_items * 32 + 255) / 256), 256, 0, st>>>(
+            block_cnt, block_idx, D.M, D.r, D.rb, D.re, static_cast<int>(n_items), sb->ucnt);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
+    const size_t smem = D.d == 128 ? (D.b == 128 ? Shape<128, 128>::kSmem : Shape<128, 64>::kSmem)
+                                   : (D.b == 128 ? Shape<64, 128>::kSmem : Shape<64, 64>::kSmem);
     // fast launch over every row, then the exact launch over the rows it flagged (usually
     // none: its CTAs find an empty list and exit)
     for (int exact = 0; exact < 2; ++exact) {
         const int grid = exact ? n_sm : static_cast<int>(n_items < static_cast<size_t>(n_sm) ? n_items : n_sm);
-        kern<<<grid, kThreads, kSmemBytes, st>>>(
+        kern<<<grid, kThreads, smem, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
             D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
-            D.q_hs, D.q_ts);
+            D.q_hs, D.q_ts, sb->ucnt);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -1,4 +1,5 @@
-// score_tc.cu — tcgen05 score kernels of the estimation (bf16 build, b = 128, d = 128):
+// score_tc.cu — tcgen05 score kernels of the estimation (bf16 build, b in {64, 128},
+// d in {64, 128}, b/s in {16, 32, 64, 128}):
 //
 //   A2  proxy_lse     Eq. 1 softmax normaliser of the proxy logits over the sampled causal
 //                     keys (Z4): per (sampled row, key chunk) online (max, sum) in
@@ -6,13 +7,15 @@
 //   A3  proxy_maxpool Eq. 1 max-pool (Z6): L[c][m][n] = max over the 32 x 32
 //                     sampled window of z_ij - lse_i (b/s = 32 rows = one warp's TMEM lanes,
 //                     so the row-window max is a warp reduction).
-//   A4  budget        Alg. 1 line 1-2 (Z7, Z8): per head, last block's 128 queries
+//   A4  budget        Alg. 1 line 1-2 (Z7, Z8): per head, last block's b queries
 //                     against every key block: per (row t, block n) max m_tn and
-//                     s_tn = sum_k exp2(x_tk - m_tn); combined + sorted afterwards.
+//                     s_tn = sum_k exp2(x_tk - m_tn); combined + sorted afterwards.  With
+//                     b = 64 the A tile's rows 64-127 are padding and each 128-key tile
+//                     holds two key blocks (one partial per 64-column half).
 //
 // All three share one warp-specialised tile engine (192 threads):
 //   warp 0 TMA producer (A tile once, then 128-key B tiles into a 2-stage ring),
-//   warp 1 TMEM allocator + single-thread tcgen05.mma issuer (S = A B^T, K = d = 128,
+//   warp 1 TMEM allocator + single-thread tcgen05.mma issuer (S = A B^T, K = d,
 //          SS operands K-major SWIZZLE_128B, fp32 accumulators double-buffered in TMEM),
 //   warps 2-5 epilogue: thread = tile row (TMEM lane), tcgen05.ld 128 columns, mode math.
 #include <cuda_bf16.h>
@@ -56,6 +59,9 @@ struct ScoreParams {
     int n_chunks;    // chunks per tile row (proxy) / per head (budget)
     int r;           // budget: GQA ratio (local head -> local kv head)
     int bs;          // proxy: sampled rows (= keys) per block, b / s
+    int d;           // head dim (64 or 128): K of the MMAs, 64-column boxes per tile
+    int b;           // budget: block size (64 or 128); key tiles hold 128 / b blocks
+    int n_kt;        // budget: 128-key tiles
     float sc2;       // logit scale in log2 units
     float* part_m;   // LSE: [gl][Ns][n_chunks]; BUDGET: [Hl][M][128]
     float* part_s;
@@ -65,7 +71,9 @@ struct ScoreParams {
                         // bs sampled keys of block n (causal mask applied)
 };
 
-template <int kEmu>   // of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4)
+// kEmu: of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4); kB64: budget pass
+// with b = 64 (two key blocks per 128-key tile)
+template <int kEmu, bool kB64>
 __global__ void __launch_bounds__(kThreads, 2)
 score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 ScoreParams p) {
@@ -77,12 +85,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         prob = blockIdx.x / p.n_chunks;
         const int k = blockIdx.x % p.n_chunks;
         u_begin = k * p.chunk;
-        u_end = min(u_begin + p.chunk, p.M);
-        a_row = (p.M - 1) * 128;                   // the last block's query rows (Alg. 1)
+        u_end = min(u_begin + p.chunk, p.n_kt);
+        a_row = (p.M - 1) * p.b;                   // the last block's query rows (Alg. 1)
         a_head = prob;
         b_row0 = 0;
         b_head = prob / p.r;
-        diag_u = p.M - 1;
+        diag_u = p.n_kt - 1;
     } else {
         const int per_group = (p.tr_hi - p.tr_lo) * p.n_chunks;
         prob = blockIdx.x / per_group;
@@ -132,16 +140,16 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (p.mode == kBudget) tma_load_3d(dst, map, bar, col, row, head);
                 else tma_load_2d(dst, map, bar, col, row);
             };
-            mbar_expect_tx(&bars->a_full, kTile);
-            load(sA, &tmA, &bars->a_full, 0, a_row, a_head);
-            load(sA + kBox, &tmA, &bars->a_full, 64, a_row, a_head);
+            const int nbox = p.d / 64;
+            mbar_expect_tx(&bars->a_full, nbox * kBox);
+            for (int ch = 0; ch < nbox; ++ch) load(sA + ch * kBox, &tmA, &bars->a_full, ch * 64, a_row, a_head);
             for (int j = 0; j < nt; ++j) {
                 const int s = j % kStages;
                 if (j >= kStages) mbar_wait(&bars->b_empty[s], ((j / kStages) - 1) & 1);
                 const int brow = b_row0 + (u_begin + j) * 128;
-                mbar_expect_tx(&bars->b_full[s], kTile);
-                load(sB + s * kTile, &tmB, &bars->b_full[s], 0, brow, b_head);
-                load(sB + s * kTile + kBox, &tmB, &bars->b_full[s], 64, brow, b_head);
+                mbar_expect_tx(&bars->b_full[s], nbox * kBox);
+                for (int ch = 0; ch < nbox; ++ch)
+                    load(sB + s * kTile + ch * kBox, &tmB, &bars->b_full[s], ch * 64, brow, b_head);
             }
         }
     } else if (warp == 1) {
@@ -155,8 +163,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (j >= 2) mbar_wait(&bars->s_empty[j & 1], ((j >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t tS = tbase + (j & 1) * 128;
+                const int nkk = p.d / 16;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
+                    if (kk >= nkk) break;
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
                     umma_ss(tS, sdesc_sw128(a_addr + off, 16, 1024),
                             sdesc_sw128(b_addr + s * kTile + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
@@ -172,7 +182,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         float m_run = -INFINITY, s_run = 0.f;
         float lse_row = 0.f;
         // rows past the end (partial last tile / block): padded, excluded from every output
-        const bool row_ok = (p.mode == kBudget) ? ((p.M - 1) * 128 + rr < p.N) : (tr * 128 + rr < p.Ns);
+        const bool row_ok = (p.mode == kBudget) ? (rr < p.b && a_row + rr < p.N) : (tr * 128 + rr < p.Ns);
         if (p.mode == kMaxpool)
             lse_row = row_ok ? p.lse2[static_cast<long long>(prob) * p.Ns + tr * 128 + rr] : INFINITY;
         for (int j = 0; j < nt; ++j) {
@@ -253,13 +263,56 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
             } else {
-                // raw logits; causal mask inside the diagonal tile; 8 independent max chains
+                // raw logits; causal mask inside the diagonal tile (key position > query
+                // position); 8 independent max chains
                 if (diag) {
+                    const int thr = (p.mode == kBudget) ? a_row + rr - u * 128 : rr;
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
                         for (int e = 0; e < 32; ++e)
-                            if (c * 32 + e > rr) raw[c][e] = 0xff800000u;  // -inf
+                            if (c * 32 + e > thr) raw[c][e] = 0xff800000u;  // -inf
+                }
+                if (kB64 && p.mode == kBudget) {
+                    // two key blocks per tile: (max, sum) of each 64-column half
+#pragma unroll
+                    for (int hb = 0; hb < 2; ++hb) {
+                        float mx[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) mx[k] = __uint_as_float(raw[2 * hb][k]);
+#pragma unroll
+                        for (int c = 2 * hb; c < 2 * hb + 2; ++c)
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(raw[c][e]));
+                        const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.sc2;
+                        float acc = 0.f;
+                        if (tmax > -INFINITY) {
+                            const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
+                            const uint64_t nref = f2_pack(-tmax, -tmax);
+                            uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) {
+                                const int e0 = 64 * hb + 2 * c;
+                                const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
+                                                                   __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
+                                                           sc2, nref);
+                                float x0, x1;
+                                f2_unpack(x2, x0, x1);
+                                acc2[c & 3] = f2_add(acc2[c & 3], f2_pack(ex2(x0), ex2(x1)));
+                            }
+                            float a0, a1;
+                            f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
+                            acc = a0 + a1;
+                        }
+                        const int n = 2 * u + hb;
+                        if (n < p.M) {
+                            const long long o = (static_cast<long long>(prob) * p.M + n) * 128 + rr;
+                            const bool ok = row_ok && tmax > -INFINITY;
+                            p.part_m[o] = ok ? tmax : -INFINITY;   // padded rows carry no mass
+                            p.part_s[o] = ok ? acc : 0.f;
+                        }
+                    }
+                    continue;
                 }
                 float mx[8];
 #pragma unroll
@@ -505,16 +558,19 @@ bool maxpool_pass() {
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
 
-ScoreKernel score_kernel() {
+ScoreKernel score_kernel(bool b64 = false) {
+    if (b64) return score_tc_kernel<0, true>;
     const int e = score_emu();
-    return e == 0 ? score_tc_kernel<0> : e == 1 ? score_tc_kernel<1> : e == 2 ? score_tc_kernel<2>
-                                                                      : score_tc_kernel<3>;
+    return e == 0 ? score_tc_kernel<0, false> : e == 1 ? score_tc_kernel<1, false>
+         : e == 2 ? score_tc_kernel<2, false> : score_tc_kernel<3, false>;
 }
 
 bool set_smem_attr() {
     static bool done = false;
     if (!done) {
         if (cudaFuncSetAttribute(score_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmem)) != cudaSuccess ||
+            cudaFuncSetAttribute(score_kernel(true), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmem)) != cudaSuccess)
             return false;
         done = true;
@@ -525,7 +581,8 @@ bool set_smem_attr() {
 }  // namespace
 
 bool score_tc_supported(const Dims& D) {
-    return !D.fp32 && D.d == 128 && D.b == 128 && (D.s == 1 || D.s == 2 || D.s == 4 || D.s == 8);
+    return !D.fp32 && (D.d == 64 || D.d == 128) && (D.b == 64 || D.b == 128) &&
+           (D.bs == 16 || D.bs == 32 || D.bs == 64 || D.bs == 128);
 }
 
 size_t score_tc_scratch_bytes(const Dims& D) {
@@ -547,9 +604,11 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     if (!set_smem_attr()) return cudaErrorInvalidValue;
     CUtensorMap ma, mb;
     const uint64_t rows = static_cast<uint64_t>(D.gl) * D.Ns;
-    if (!make_map_bf16_sw128(&ma, Pq, rows, 128, 128) || !make_map_bf16_sw128(&mb, Pk, rows, 128, 128))
+    if (!make_map_bf16_sw128(&ma, Pq, rows, D.d, 128) || !make_map_bf16_sw128(&mb, Pk, rows, D.d, 128))
         return cudaErrorInvalidValue;
     ScoreParams p{};
+    p.d = D.d;
+    p.b = D.b;
     p.Ns = static_cast<int>(D.Ns);
     p.M = D.M;
     p.n_tr = static_cast<int>((D.Ns + 127) / 128);
@@ -598,21 +657,24 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
                              float* bmass, cudaStream_t st) {
     if (!set_smem_attr()) return cudaErrorInvalidValue;
     CUtensorMap ma, mb;
-    if (!make_map_bf16_sw128_3d(&ma, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128) ||
-        !make_map_bf16_sw128_3d(&mb, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128))
+    if (!make_map_bf16_sw128_3d(&ma, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128, D.d) ||
+        !make_map_bf16_sw128_3d(&mb, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, 128, D.d))
         return cudaErrorInvalidValue;
     ScoreParams p{};
     p.mode = kBudget;
+    p.d = D.d;
+    p.b = D.b;
     p.N = static_cast<int>(D.N);
     p.M = D.M;
     p.r = D.r;
+    p.n_kt = static_cast<int>((static_cast<long long>(D.M) * D.b + 127) / 128);
     p.chunk = score_chunk();
-    p.n_chunks = (D.M + p.chunk - 1) / p.chunk;
+    p.n_chunks = (p.n_kt + p.chunk - 1) / p.chunk;
     p.sc2 = kLog2e / sqrtf(static_cast<float>(D.d));
     p.part_m = scratch;
     p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
     const unsigned grid = static_cast<unsigned>(D.Hl) * p.n_chunks;
-    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.b == 64)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int n_comb = (D.M + kCombChunk - 1) / kCombChunk;

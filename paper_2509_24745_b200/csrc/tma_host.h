@@ -38,15 +38,16 @@ inline bool make_map_bf16_sw128(CUtensorMap* map, const void* base, uint64_t row
     return r == CUDA_SUCCESS;
 }
 
-// 3-D bf16 view [heads][rows][128] of a per-head 2-D matrix with arbitrary row and head
-// strides (elements): head-major tensors (row stride 128, head stride N*128) and token-major
-// ones (row stride = token stride, head stride 128) alike.  Box [1][box_rows][64], SWIZZLE_128B;
-// rows past `rows` are out of bounds and read as zeros.
+// 3-D bf16 view [heads][rows][cols] of a per-head 2-D matrix with arbitrary row and head
+// strides (elements): head-major tensors (row stride d, head stride N*d) and token-major
+// ones (row stride = token stride, head stride d) alike; cols = head_dim (64 or 128).
+// Box [1][box_rows][64], SWIZZLE_128B; rows past `rows` are out of bounds and read as zeros.
 inline bool make_map_bf16_sw128_3d(CUtensorMap* map, const void* base, uint64_t heads, uint64_t rows,
-                                   uint64_t row_stride, uint64_t head_stride, uint32_t box_rows) {
+                                   uint64_t row_stride, uint64_t head_stride, uint32_t box_rows,
+                                   uint64_t cols = 128) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    cuuint64_t dims[3] = {128, rows, heads};
+    cuuint64_t dims[3] = {cols, rows, heads};
     cuuint64_t strides[2] = {row_stride * 2, head_stride * 2};
     cuuint32_t box[3] = {64, box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};

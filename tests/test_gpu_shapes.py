@@ -1,0 +1,162 @@
+"""GPU parity of the bf16 tensor-core path at head_dim 64 and block size 64 (SURVEY §8(b):
+v1 supports d in {64, 128}, b in {64, 128}) against the fp64 CPU oracle, with the staged
+protocol of SURVEY §8(c).5 (budgets on margin-qualified heads, block lists on
+margin-qualified rows, O with the GPU mask injected into the oracle's O10).
+
+b = 64 runs the pair kernel (two query heads of one KV head per 128-lane tile, walking the
+union of their lists), so it is also checked on arbitrary, non-nested injected lists, on odd
+GQA ratios (a pair with one head), and on inputs that force its exact second launch.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2509_24745_b200 as pa
+import workloads
+from test_gpu_parity import DEV, MARGIN, check_masks, check_out, np32, ocfg_of, to_dev
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(64, 64), (64, 128), (128, 64)]
+
+
+def cfg_of(d, b, N, heads=(8, 2), g=1, gamma=0.9, stride=4, min_budget=0):
+    return pa.Config(n_q_heads=heads[0], n_kv_heads=heads[1], head_dim=d, seq_len=N, block_size=b,
+                     stride=stride, n_groups=g, gamma=gamma, min_budget_tokens=min_budget)
+
+
+def run_staged(cfg, Q, K, V, min_checked=0.9):
+    oc = ocfg_of(cfg)
+    Qf, Kf, Vf = np32(Q), np32(K), np32(V)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    est = oracle.estimate(oc, Qf, Kf)
+    ks = kstar.cpu().numpy()
+    ok = est["budget_margin"] > MARGIN
+    assert np.array_equal(ks[ok], est["kstar"][ok]), (ks, est["kstar"], est["budget_margin"])
+    checked, skipped = check_masks(oc, est["L"], ks, cnt, idx)
+    assert checked >= min_checked * (checked + skipped)
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    check_out(O, oracle.attention(oc, Qf, Kf, Vf, cnt.cpu().numpy(), idx.cpu().numpy()), fp32=False)
+    Od = pa.dense_prefill(cfg, Qd, Kd, Vd)
+    check_out(Od, oracle.dense(oc, Qf, Kf, Vf), fp32=False)
+    return cnt, idx
+
+
+@pytest.mark.parametrize("gamma", [0.5, 0.7, 0.9, 0.95, 1.0])
+def test_config_a_shape_bf16(gamma):
+    # config A's shape (8/2 heads, d = 64, N = 1024, b = 64, g = 2, s = 4) on the bf16
+    # tensor-core path, i.i.d. inputs (the AC4 gamma grid)
+    cfg = cfg_of(64, 64, 1024, g=2, gamma=gamma)
+    Q, K, V = workloads.iid(8, 2, 1024, 64, seed=int(gamma * 100))
+    run_staged(cfg, Q.bfloat16(), K.bfloat16(), V.bfloat16())
+
+
+@pytest.mark.parametrize("d,b", SHAPES)
+@pytest.mark.parametrize("case", [
+    dict(N=2048, heads=(8, 2), g=1, seed=0),
+    dict(N=2048, heads=(8, 2), g=2, seed=1, gamma=0.95),
+    dict(N=2048, heads=(7, 1), g=1, seed=2, min_budget=256),     # r = 7: a pair with one head
+    dict(N=1000, heads=(6, 2), g=2, seed=3, stride=2),           # ragged N, r = 3
+    dict(N=3001, heads=(4, 4), g=2, seed=4, gamma=0.7),          # ragged, r = 1 (no pairs)
+], ids=["llama-like", "g2", "qwen-like-r7", "ragged-r3", "ragged-r1"])
+def test_structured_staged(d, b, case):
+    case = dict(case)
+    seed = case.pop("seed")
+    cfg = cfg_of(d, b, **case)
+    Q, K, V, _ = workloads.structured(cfg.n_q_heads, cfg.n_kv_heads, cfg.seq_len, d, seed=seed)
+    run_staged(cfg, Q, K, V)
+
+
+def random_lists(Hq, M, seed, frac=0.3):
+    """Arbitrary valid lists (ascending, diagonal included), independent per head, so the
+    two heads of a b = 64 pair are NOT nested."""
+    rng = np.random.default_rng(seed)
+    cnt = np.zeros((Hq, M), np.int32)
+    idx = np.zeros((Hq, M, M), np.int32)
+    for h in range(Hq):
+        for m in range(M):
+            others = np.flatnonzero(rng.random(m) < frac)
+            lst = np.concatenate([others, [m]]).astype(np.int32)
+            cnt[h, m] = len(lst)
+            idx[h, m, :len(lst)] = lst
+    return cnt, idx
+
+
+@pytest.mark.parametrize("d,b", SHAPES + [(128, 128)])
+def test_injected_non_nested_lists(d, b):
+    cfg = cfg_of(d, b, 2048, heads=(6, 2))
+    Q, K, V, _ = workloads.structured(6, 2, 2048, d, seed=30)
+    cnt, idx = random_lists(6, cfg.M, seed=31)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    O = pa.prefill(cfg, Qd, Kd, Vd, torch.from_numpy(cnt).to(DEV), torch.from_numpy(idx).to(DEV))
+    ref = oracle.attention(ocfg_of(cfg), np32(Q), np32(K), np32(V), cnt, idx)
+    check_out(O, ref, fp32=False)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_pair_reference_fallback_and_exact_rerun(d):
+    # b = 64 pair: head 1's blocks are never among the union's first two blocks, and those
+    # blocks score ~+150 log2 units above everything head 1 keeps, so the non-member
+    # reference underflows head 1's row sums; the exact launch must recompute those rows.
+    N, b = 1024, 64
+    cfg = cfg_of(d, b, N, heads=(2, 1))
+    g = torch.Generator().manual_seed(40)
+    Q = torch.randn(2, N, d, generator=g) * 0.5
+    K = torch.randn(1, N, d, generator=g) * 0.5
+    V = torch.randn(1, N, d, generator=g)
+    u = torch.randn(d, generator=g)
+    u = u / u.norm()
+    Q[1] += 4.0 * u                                           # head 1 aligned with u ...
+    K[0, :2 * b] += 12.0 * u                                  # ... as are blocks 0 and 1
+    Q, K, V = Q.bfloat16(), K.bfloat16(), V.bfloat16()
+    M = N // b
+    cnt = np.zeros((2, M), np.int32)
+    idx = np.zeros((2, M, M), np.int32)
+    for m in range(M):
+        a = sorted(set(range(min(m + 1, 2))) | {m})           # head 0: blocks 0, 1 and m
+        c = sorted({m // 2, m})                               # head 1: never blocks 0/1 (m >= 2)
+        if m < 2:
+            c = [m]
+        cnt[0, m], cnt[1, m] = len(a), len(c)
+        idx[0, m, :len(a)], idx[1, m, :len(c)] = a, c
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    O = pa.prefill(cfg, Qd, Kd, Vd, torch.from_numpy(cnt).to(DEV), torch.from_numpy(idx).to(DEV))
+    assert torch.isfinite(O.float()).all()
+    ref = oracle.attention(ocfg_of(cfg), np32(Q), np32(K), np32(V), cnt, idx)
+    check_out(O, ref, fp32=False)
+
+
+@pytest.mark.parametrize("d,b", SHAPES)
+def test_token_major_and_row_range_bitwise(d, b):
+    from paper_2509_24745_b200 import shard
+    cfg = cfg_of(d, b, 2048, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, 2048, d, seed=50)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    full = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    # token-major [N][H][d] views of the same tensors: identical lists and outputs
+    tcfg = cfg.replace(token_major=True)
+    Qt, Kt, Vt = (x.transpose(0, 1).contiguous() for x in (Qd, Kd, Vd))
+    k2, _, c2, i2 = pa.estimate(tcfg, Qt, Kt)
+    assert torch.equal(k2, kstar) and torch.equal(c2, cnt)
+    Ot = pa.prefill(tcfg, Qt, Kt, Vt, c2, i2)
+    assert torch.equal(Ot.transpose(0, 1), full)
+    # zig-zag row shards reassemble the full output bit for bit
+    O = torch.zeros_like(full)
+    for rank in range(3):
+        shard.prefill_rows(cfg, Qd, Kd, Vd, cnt, idx, O, shard.zigzag_rows(cfg.M, 3, rank))
+    assert torch.equal(O, full)
+
+
+def test_determinism_pair_kernel():
+    cfg = cfg_of(128, 64, 4096, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, 4096, 128, seed=60)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    a = pa.estimate(cfg, Qd, Kd)
+    Oa = pa.prefill(cfg, Qd, Kd, Vd, a[2], a[3])
+    b = pa.estimate(cfg, Qd, Kd)
+    Ob = pa.prefill(cfg, Qd, Kd, Vd, b[2], b[3])
+    valid = torch.arange(cfg.M, device=DEV)[None, None, :] < a[2][:, :, None]   # first cnt entries
+    assert torch.equal(a[2], b[2]) and torch.equal(a[3][valid], b[3][valid]) and torch.equal(Oa, Ob)

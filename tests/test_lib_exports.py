@@ -63,8 +63,8 @@ def test_loads_and_validates_configs_on_host(so):
         "Hq % Hkv": (good.replace(n_q_heads=30), pa._lib.E_CONFIG),
         "Hkv % g": (good.replace(n_groups=3), pa._lib.E_CONFIG),
         "b % s": (good.replace(stride=3), pa._lib.E_CONFIG),
-        "d = 64 in bf16": (good.replace(head_dim=64), pa._lib.E_UNSUPPORTED),
-        "b = 64 in bf16": (good.replace(block_size=64), pa._lib.E_UNSUPPORTED),
+        "d = 96 in bf16": (good.replace(head_dim=96), pa._lib.E_UNSUPPORTED),
+        "b = 256 in bf16": (good.replace(block_size=256), pa._lib.E_UNSUPPORTED),
         "shard not kv-aligned": (good.replace(q_head_begin=2, q_head_end=8), pa._lib.E_CONFIG),
     }
     for name, (cfg, code) in bad.items():
@@ -76,6 +76,9 @@ def test_loads_and_validates_configs_on_host(so):
     # FP32_DEBUG accepts the small config A shape (d=64, b=64)
     a = pa.Config(8, 2, 64, 1024, 64, 4, 2, 0.9, fp32_debug=True)
     assert pa.workspace_bytes(a) > 0
+    # ... and so does the bf16 build (d in {64, 128}, b in {64, 128})
+    for d, b in ((64, 64), (64, 128), (128, 64)):
+        assert pa.workspace_bytes(pa.Config(8, 2, d, 1024, b, 4, 2, 0.9)) > 0
 
 
 def test_shard_group_arithmetic():
