@@ -21,17 +21,20 @@
 //   warps 4-7   epilogue: O (TMEM) * 1/l -> bf16 -> global; releases O for the next row
 //   warps 8-11  softmax of stream 0, warps 12-15 of stream 1 (thread = row = TMEM lane)
 // TMEM (512 columns): O [0,128)  S_0 [128,256)  S_1 [256,384)  P_0 [384,448)  P_1 [448,512).
+// (kB = 64: each stream's S and P regions hold two buffers, so a stream's next S and P
+// never wait for its previous block's PV.)
 //
 // Shapes (template <kEmu, kD, kB>): head_dim kD in {64, 128}, block kB in {64, 128}.  The
 // 128 query rows of a work unit are the 128 TMEM lanes.  kB = 128: one (head, block row).
-// kB = 64: a PAIR of query heads of the same KV head on the same 64-row block row (lanes
-// 0-63 head 2p, 64-127 head 2p+1), so every S = Q K^T tile is still M = 128 (an M = 64
-// tcgen05.mma costs the issue slot of an M = 128 one).  The pair walks the UNION of its two
-// ascending lists (the selection's lists of one group are nested, so the union is the
-// longer list); a block that is not in a half's list gets P = 0 for that half.  The fixed
-// reference of a half is the max over its member blocks among the two first blocks, else
-// (neither is a member) the raw max of those blocks; rows whose sum would then underflow
-// (l < 2^-60) or overflow are re-run by the exact launch, as for kB = 128.
+// kB = 64: a PAIR of adjacent 64-row block rows (2q, 2q+1) of one head (lanes 0-63 row 2q,
+// 64-127 row 2q+1), so every S = Q K^T tile is still M = 128 (an M = 64 tcgen05.mma costs
+// the issue slot of an M = 128 one).  The pair walks the UNION of its two ascending lists
+// (1.12x the mean list at the 128K bench inputs; pairing two heads of one KV head instead
+// measured 1.41x, scripts/pair_union_stats.py); a block that is not in a half's list gets
+// P = 0 for that half.  The fixed reference of a half is the max over its member blocks
+// among the two first blocks, else (neither is a member) the raw max of those blocks; rows
+// whose sum would then underflow (l < 2^-60) or overflow are re-run by the exact launch,
+// as for kB = 128.
 #include <cuda_bf16.h>
 
 #include <climits>
@@ -70,10 +73,10 @@ struct __align__(8) Bars8 {
     uint64_t k_empty[kKStages];
     uint64_t v_full[kVStages];
     uint64_t v_empty[kVStages];
-    uint64_t s_full[2];
-    uint64_t s_free[2];
-    uint64_t p_full[2][2];   // [stream][half]
-    uint64_t p_free[2];
+    uint64_t s_full[2][2];   // [stream][buffer] (kB = 64: two 64-column S buffers per stream)
+    uint64_t s_free[2][2];
+    uint64_t p_full[2][2];   // kB = 128: [stream][half]; kB = 64: [stream][buffer]
+    uint64_t p_free[2][2];   // [stream][buffer]
     uint64_t o_final, o_free;
     uint64_t l_ready[2];     // per item parity: both streams' row sums written
     uint64_t item_full[kItemSlots];
@@ -105,15 +108,15 @@ struct Sched {        // device-side scheduler state of one launch pair (zeroed 
 };
 
 // Block-list walk of a kB = 64 work unit: the ascending union of the pair's two lists, with
-// each element's membership (bit 0: head A = lanes 0-63, bit 1: head B = lanes 64-127).
+// each element's membership (bit 0: row A = lanes 0-63, bit 1: row B = lanes 64-127).
 struct PairWalk {
     const int* a;
     const int* b;
     int ca, cb, pa, pb, j;
     bool dense;
     __device__ __forceinline__ int next(int& mem) {
-        if (dense) {
-            mem = cb > 0 ? 3 : 1;
+        if (dense) {   // lists 0..ca-1 and 0..cb-1
+            mem = (j < ca ? 1 : 0) | (j < cb ? 2 : 0);
             return j++;
         }
         const int x = pa < ca ? __ldg(a + pa) : INT_MAX;
@@ -135,6 +138,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt) {
     using Sh = Shape<kD, kB>;
     constexpr bool kPair = (kB == 64);
+    constexpr int kNB = kPair ? 2 : 1;   // S / P buffers per stream (a 64-key S is 64 columns)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -146,8 +150,9 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nrows = row_hi - row_lo;
-    const int npairs = kPair ? (r + 1) >> 1 : r;       // work units per (kv head, block row)
-    const int per_kv = npairs * nrows;
+    // kB = 64: row pairs q in [q_lo, q_hi) cover the block rows [row_lo, row_hi)
+    const int q_lo = row_lo >> 1, q_hi = (row_hi + 1) >> 1;
+    const int per_kv = r * (kPair ? q_hi - q_lo : nrows);   // work units per kv head
     const int n_items = exact ? sched->n_flagged : n_total;
     const bool dense = (block_cnt == nullptr);
     const int passes = exact ? 2 : 1;   // exact: max sweep, then the fixed pass
@@ -164,11 +169,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             mbar_init(&bars->v_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars->s_full[s], 1);
-            mbar_init(&bars->s_free[s], 128);
-            mbar_init(&bars->p_full[s][0], 128);
-            mbar_init(&bars->p_full[s][1], 128);
-            mbar_init(&bars->p_free[s], 1);
+            for (int k = 0; k < 2; ++k) {
+                mbar_init(&bars->s_full[s][k], 1);
+                mbar_init(&bars->s_free[s][k], 128);
+                mbar_init(&bars->p_full[s][k], 128);
+                mbar_init(&bars->p_free[s][k], 1);
+            }
             mbar_init(&bars->l_ready[s], 256);
         }
         mbar_init(&bars->o_final, 1);
@@ -185,19 +191,19 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
 
-    // item decode (kv-head major, heavy rows first): kB = 128 -> head h0 (h1 = -1);
-    // kB = 64 -> the pair (h0, h1), h1 = -1 when r is odd and the pair is the last one
-    auto decode = [&](int item, int& h0, int& h1, int& m, int& kvl) {
+    // item decode (kv-head major, heavy rows first): head hl, its block row mA (kB = 128), or
+    // its row pair (mA, mB) = (2q, 2q+1) (kB = 64; -1 for a row outside [row_lo, row_hi))
+    auto decode = [&](int item, int& hl, int& mA, int& mB, int& kvl) {
         kvl = item / per_kv;
         const int rem = item % per_kv;
-        m = row_hi - 1 - rem / npairs;
+        hl = kvl * r + rem % r;
         if (kPair) {
-            const int p = rem % npairs;
-            h0 = kvl * r + 2 * p;
-            h1 = (2 * p + 1 < r) ? h0 + 1 : -1;
+            const int q = q_hi - 1 - rem / r;
+            mA = (2 * q >= row_lo) ? 2 * q : -1;
+            mB = (2 * q + 1 < row_hi) ? 2 * q + 1 : -1;
         } else {
-            h0 = kvl * r + rem % r;
-            h1 = -1;
+            mA = row_hi - 1 - rem / r;
+            mB = -1;
         }
     };
     auto get_item = [&](int it) -> Item {         // consumers: wait for slot, read, release
@@ -211,13 +217,16 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     auto list_of = [&](int hl, int m) -> const int* {
         return dense ? nullptr : block_idx + (static_cast<long long>(hl) * M + m) * M;
     };
-    auto walk_of = [&](int h0, int h1, int m) -> PairWalk {
+    auto count_of = [&](int hl, int m) -> int {
+        return m < 0 ? 0 : dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(hl) * M + m);
+    };
+    auto walk_of = [&](int hl, int mA, int mB) -> PairWalk {
         PairWalk w;
         w.dense = dense;
-        w.a = list_of(h0, m);
-        w.b = h1 >= 0 ? list_of(h1, m) : nullptr;
-        w.ca = dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(h0) * M + m);
-        w.cb = h1 < 0 ? 0 : dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(h1) * M + m);
+        w.a = mA >= 0 ? list_of(hl, mA) : nullptr;
+        w.b = mB >= 0 ? list_of(hl, mB) : nullptr;
+        w.ca = count_of(hl, mA);
+        w.cb = count_of(hl, mB);
         w.pa = w.pb = w.j = 0;
         return w;
     };
@@ -237,35 +246,26 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     Item x{-1, 0};
                     if (k < n_items) {
                         x.item = exact ? flagged[k] : k;
-                        int h0, h1, m, kvl;
-                        decode(x.item, h0, h1, m, kvl);
-                        x.cnt = dense ? m + 1
-                              : kPair ? __ldg(ucnt + x.item)
-                                      : __ldg(block_cnt + static_cast<long long>(h0) * M + m);
+                        int hl, mA, mB, kvl;
+                        decode(x.item, hl, mA, mB, kvl);
+                        x.cnt = !kPair ? count_of(hl, mA)
+                              : dense ? max(count_of(hl, mA), count_of(hl, mB)) : __ldg(ucnt + x.item);
                     }
                     bars->items[slot] = x;
                     mbar_arrive(&bars->item_full[slot]);   // release semantics publish x
                     if (x.item < 0) break;
-                    int h0, h1, m, kvl;
-                    decode(x.item, h0, h1, m, kvl);
+                    int hl, mA, mB, kvl;
+                    decode(x.item, hl, mA, mB, kvl);
                     if (it > 0) mbar_wait(&bars->q_empty, (it - 1) & 1);   // last S of it-1 done
-                    if (kPair) {   // two 64-row head slices stacked in the 128-row tile
-                        mbar_expect_tx(&bars->q_full, (h1 >= 0 ? 2 : 1) * (kD / 64) * (kBox / 2));
+                    // the unit's 128 query rows (kB = 64: rows 2q*64 .. 2q*64+127)
+                    const int q_row0 = kPair ? (mA >= 0 ? mA : mB - 1) * kB : mA * kTileRows;
+                    mbar_expect_tx(&bars->q_full, Sh::kQTile);
 #pragma unroll
-                        for (int ch = 0; ch < kD / 64; ++ch) {
-                            tma_load_3d(sQ + ch * kBox, &tmQ, &bars->q_full, ch * 64, m * kB, h0);
-                            if (h1 >= 0)
-                                tma_load_3d(sQ + ch * kBox + kBox / 2, &tmQ, &bars->q_full, ch * 64, m * kB, h1);
-                        }
-                    } else {
-                        mbar_expect_tx(&bars->q_full, Sh::kQTile);
-#pragma unroll
-                        for (int ch = 0; ch < kD / 64; ++ch)
-                            tma_load_3d(sQ + ch * kBox, &tmQ, &bars->q_full, ch * 64, m * kTileRows, h0);
-                    }
-                    const int* list = list_of(h0, m);
+                    for (int ch = 0; ch < kD / 64; ++ch)
+                        tma_load_3d(sQ + ch * kBox, &tmQ, &bars->q_full, ch * 64, q_row0, hl);
+                    const int* list = list_of(hl, mA);
                     for (int pass = 0; pass < passes; ++pass) {
-                        PairWalk w = walk_of(h0, h1, m);
+                        PairWalk w = walk_of(hl, mA, mB);
                         for (int j = 0; j < x.cnt; ++j, ++gk) {
                             const int st = gk % kKStages;
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
@@ -288,10 +288,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const Item x = get_item(it);
                 if (x.item < 0) break;
                 if (lane == 0) {
-                    int h0, h1, m, kvl;
-                    decode(x.item, h0, h1, m, kvl);
-                    const int* list = list_of(h0, m);
-                    PairWalk w = walk_of(h0, h1, m);
+                    int hl, mA, mB, kvl;
+                    decode(x.item, hl, mA, mB, kvl);
+                    const int* list = list_of(hl, mA);
+                    PairWalk w = walk_of(hl, mA, mB);
                     for (int j = 0; j < x.cnt; ++j, ++gv) {
                         const int st = gv % kVStages;
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
@@ -320,7 +320,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 for (int pass = 0; pass < passes; ++pass) {
                     for (int j = 0; j < x.cnt; ++j, ++gk) {
                         const int s = j & 1;
-                        if (gs[s] > 0) mbar_wait(&bars->s_free[s], (gs[s] - 1) & 1);
+                        const int sb = gs[s] % kNB;       // this stream's S buffer
+                        if (gs[s] >= kNB) mbar_wait(&bars->s_free[s][sb], ((gs[s] / kNB) - 1) & 1);
                         ++gs[s];
                         const int st = gk % kKStages;
                         mbar_wait(&bars->k_full[st], (gk / kKStages) & 1);
@@ -331,10 +332,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             for (int kk = 0; kk < kD / 16; ++kk) {
                                 const uint32_t offq = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
                                 const uint32_t offk = ((kk >> 2) * Sh::kKBox + (kk & 3) * 32) >> 4;
-                                umma_ss(tbase + kColS + s * 128, dq + offq, b0 + offk, idesc_qk, kk > 0 ? 1u : 0u);
+                                umma_ss(tbase + kColS + s * 128 + sb * 64, dq + offq, b0 + offk, idesc_qk,
+                                        kk > 0 ? 1u : 0u);
                             }
                             tc_commit(&bars->k_empty[st]);
-                            tc_commit(&bars->s_full[s]);
+                            tc_commit(&bars->s_full[s][sb]);
                         }
                         __syncwarp();
                     }
@@ -356,16 +358,17 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     const int st = gv % kVStages;
                     mbar_wait(&bars->v_full[st], (gv / kVStages) & 1);
                     if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);   // O read out
+                    const int pb = gp[s] % kNB;           // this stream's P buffer
 #pragma unroll
                     for (int half = 0; half < Sh::kHalves; ++half) {
-                        mbar_wait(&bars->p_full[s][half], gp[s] & 1);
+                        mbar_wait(&bars->p_full[s][kPair ? pb : half], (gp[s] / kNB) & 1);
                         tc_fence_after();
                         if (leader) {
                             const uint64_t b0 = dv + (st * Sh::kKTile >> 4);
 #pragma unroll
                             for (int k4 = 0; k4 < 4; ++k4) {
                                 const int kk = half * 4 + k4;
-                                umma_ts(tbase + kColO, tbase + kColP + s * 64 + kk * 8,
+                                umma_ts(tbase + kColO, tbase + kColP + s * 64 + pb * 32 + kk * 8,
                                         b0 + (kk * 2048 >> 4), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
                             }
                         }
@@ -374,7 +377,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     ++gp[s];
                     if (leader) {
                         tc_commit(&bars->v_empty[st]);
-                        tc_commit(&bars->p_free[s]);
+                        tc_commit(&bars->p_free[s][pb]);
                     }
                     __syncwarp();
                 }
@@ -391,23 +394,23 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         for (int it = 0;; ++it) {
             const Item x = get_item(it);
             if (x.item < 0) break;
-            int h0, h1, m, kvl;
-            decode(x.item, h0, h1, m, kvl);
-            const int hl = (kPair && rr >= 64) ? h1 : h0;         // the row's head (-1: none)
+            int hl, mA, mB, kvl;
+            decode(x.item, hl, mA, mB, kvl);
+            const int m = (kPair && rr >= 64) ? mB : mA;         // the row's block row (-1: none)
             const long long pos = static_cast<long long>(m) * kB + (rr & (kB - 1));
             mbar_wait(&bars->l_ready[it & 1], (it >> 1) & 1);
             const float l0 = bars->lsum[it & 1][0][rr], l1 = bars->lsum[it & 1][1][rr];
             const float inv = 1.f / (l0 + l1);
             if (!exact) {   // a row whose P exceeded the bound (l = +inf marker): exact re-run
                 bool bad = !(l0 + l1 <= 2.f * exp2f(kOverflow));
-                if (kPair) bad = bad || (hl >= 0 && l0 + l1 < exp2f(kUnderflow));
+                if (kPair) bad = bad || (m >= 0 && l0 + l1 < exp2f(kUnderflow));
                 if (__any_sync(0xffffffffu, bad) && lane == 0)
                     flagged[atomicAdd(&sched->n_flagged, 1)] = x.item;   // <= 4 duplicates, benign
             }
             mbar_wait(&bars->o_final, it & 1);
             tc_fence_after();
-            const bool row_valid = hl >= 0 && pos < N;
-            uint4* dst = reinterpret_cast<uint4*>(O + static_cast<long long>(hl < 0 ? 0 : hl) * o_hs + pos * o_ts);
+            const bool row_valid = m >= 0 && pos < N;
+            uint4* dst = reinterpret_cast<uint4*>(O + static_cast<long long>(hl) * o_hs + (m < 0 ? 0 : pos) * o_ts);
 #pragma unroll
             for (int h2 = 0; h2 < kD / 64; ++h2) {
                 uint32_t o[2][32];
@@ -441,12 +444,13 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const int quarter = warp & 3;
         const int rr = quarter * 32 + lane;
         const int qrow = rr & (kB - 1);                 // query row within the block
-        const int hp = kPair ? (quarter >> 1) : 0;      // kB = 64: this warp's head of the pair
+        const int hp = kPair ? (quarter >> 1) : 0;      // kB = 64: this warp's row of the pair
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const uint32_t tS = tbase + lane_off + kColS + s * 128;
         const uint32_t tP = tbase + lane_off + kColP + s * 64;
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
         int gs = 0, gp = 0;                             // this stream's S / P counters
+        int sb = 0;                                     // S buffer of the block being read
         float xhi = -INFINITY;
 
         auto p_chunk = [&](const uint32_t (&x)[32], uint64_t nm2, uint64_t (&ls)[4], uint32_t tdst,
@@ -471,8 +475,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
                 pk[p] = pack_bf16(p0, p1);
             }
-            if (wait_free && gp > 0) {                   // the previous PV has read P_s
-                mbar_wait(&bars->p_free[s], (gp - 1) & 1);
+            if (wait_free && gp >= kNB) {                // the PV kNB blocks back has read the buffer
+                mbar_wait(&bars->p_free[s][gp % kNB], ((gp / kNB) - 1) & 1);
                 tc_fence_after();
             }
             tmem_st16(tdst, pk);
@@ -485,7 +489,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         auto release_p = [&](int half) {
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&bars->p_full[s][half]);
+            mbar_arrive(&bars->p_full[s][kPair ? gp % kNB : half]);
         };
         auto sum_ls = [&](uint64_t (&ls)[4]) {
             const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
@@ -494,13 +498,14 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             return a + b;
         };
         auto wait_s = [&]() {
-            mbar_wait(&bars->s_full[s], gs & 1);
+            sb = gs % kNB;
+            mbar_wait(&bars->s_full[s][sb], (gs / kNB) & 1);
             ++gs;
             tc_fence_after();
         };
         auto release_s = [&]() {
             tc_fence_before();
-            mbar_arrive(&bars->s_free[s]);
+            mbar_arrive(&bars->s_free[s][sb]);
         };
         // P of the block in S_s (already landed), with the reference known: chunked TMEM
         // loads overlapped with the exp2s; S released once its last chunk is in registers.
@@ -508,15 +513,15 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         auto block_exps = [&](float m_ref, bool diag, bool mine) -> float {
             if (kPair && !mine) {
                 release_s();
-                if (gp > 0) {
-                    mbar_wait(&bars->p_free[s], (gp - 1) & 1);
+                if (gp >= kNB) {
+                    mbar_wait(&bars->p_free[s][gp % kNB], ((gp / kNB) - 1) & 1);
                     tc_fence_after();
                 }
                 uint32_t z[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) z[e] = 0u;
 #pragma unroll
-                for (int c = 0; c < Sh::kChunks; ++c) tmem_st16(tP + c * 16, z);
+                for (int c = 0; c < Sh::kChunks; ++c) tmem_st16(tP + (gp % kNB) * 32 + c * 16, z);
 #pragma unroll
                 for (int h = 0; h < Sh::kHalves; ++h) release_p(h);
                 ++gp;
@@ -525,14 +530,15 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const uint64_t nm2 = f2_pack(-m_ref, -m_ref);
             uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
             uint32_t xb[2][32];
-            tmem_ld32(tS, xb[0]);
+            const uint32_t tSb = tS + sb * 64, tPb = tP + (gp % kNB) * 32;
+            tmem_ld32(tSb, xb[0]);
 #pragma unroll
             for (int c = 0; c < Sh::kChunks; ++c) {
                 tmem_ld_wait_regs(xb[c & 1]);
-                if (c + 1 < Sh::kChunks) tmem_ld32(tS + 32 * (c + 1), xb[(c + 1) & 1]);
+                if (c + 1 < Sh::kChunks) tmem_ld32(tSb + 32 * (c + 1), xb[(c + 1) & 1]);
                 else release_s();
                 if (diag) mask_chunk(xb[c & 1], c);
-                p_chunk(xb[c & 1], nm2, ls, tP + 16 * c, c == 0);
+                p_chunk(xb[c & 1], nm2, ls, tPb + 16 * c, c == 0);
                 if (c & 1) release_p(c >> 1);
             }
             ++gp;
@@ -548,11 +554,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 for (int e = 0; e < 32; e += 2)
                     mx[(e >> 1) & 3] = fmaxf(mx[(e >> 1) & 3], fmaxf(__uint_as_float(x[e]), __uint_as_float(x[e + 1])));
             };
-            tmem_ld32(tS, xb[0]);
+            const uint32_t tSb = tS + sb * 64;
+            tmem_ld32(tSb, xb[0]);
 #pragma unroll
             for (int c = 0; c < Sh::kChunks; ++c) {
                 tmem_ld_wait_regs(xb[c & 1]);
-                if (c + 1 < Sh::kChunks) tmem_ld32(tS + 32 * (c + 1), xb[(c + 1) & 1]);
+                if (c + 1 < Sh::kChunks) tmem_ld32(tSb + 32 * (c + 1), xb[(c + 1) & 1]);
                 fold(xb[c & 1], c);
             }
             return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
@@ -572,12 +579,13 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         for (int it = 0;; ++it) {
             const Item x = get_item(it);
             if (x.item < 0) break;
-            int h0, h1, m, kvl;
-            decode(x.item, h0, h1, m, kvl);
-            const int* list = list_of(h0, m);
+            int hl, mA, mB, kvl;
+            decode(x.item, hl, mA, mB, kvl);
+            const int m = hp ? mB : mA;                 // this warp's block row (its diagonal block)
+            const int* list = list_of(hl, mA);
             const int my_cnt = (x.cnt - s + 1) >> 1;   // blocks j = s, s + 2, ...
             // kB = 64: this stream's positions of the pair's union walk, with membership
-            PairWalk w = walk_of(h0, h1, m);
+            PairWalk w = walk_of(hl, mA, mB);
             int dummy;
             auto next_mine = [&](bool& mine) -> int {
                 int mem;
@@ -633,7 +641,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 }
                 m_ref = exchange_max(tmax, tmax);
                 if (kPair) {
-                    w = walk_of(h0, h1, m);
+                    w = walk_of(hl, mA, mB);
                     if (s == 1) w.next(dummy);
                 }
                 for (int js = 0; js < my_cnt; ++js) {
@@ -656,38 +664,38 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     }
 }
 
-// kB = 64: union size of each pair's two lists, |A| + |B| - |A n B| (a warp per work unit;
-// the elements of A are searched in the ascending B).  Same item order as the kernel.
+// kB = 64: union size of each row pair's two lists, |A| + |B| - |A n B| (a warp per work
+// unit; the elements of A are searched in the ascending B).  Same item order as the kernel.
 __global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* __restrict__ block_idx,
                                   int M, int r, int row_lo, int row_hi, int n_items, int* __restrict__ ucnt) {
     const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (item >= n_items) return;
-    const int nrows = row_hi - row_lo, npairs = (r + 1) >> 1;
-    const int kvl = item / (npairs * nrows), rem = item % (npairs * nrows);
-    const int m = row_hi - 1 - rem / npairs, p = rem % npairs;
-    const int h0 = kvl * r + 2 * p;
-    const int ca = __ldg(block_cnt + static_cast<long long>(h0) * M + m);
-    if (2 * p + 1 >= r) {
-        if (lane == 0) ucnt[item] = ca;
-        return;
-    }
-    const int cb = __ldg(block_cnt + static_cast<long long>(h0 + 1) * M + m);
-    const int* A = block_idx + (static_cast<long long>(h0) * M + m) * M;
-    const int* B = block_idx + (static_cast<long long>(h0 + 1) * M + m) * M;
+    const int q_lo = row_lo >> 1, q_hi = (row_hi + 1) >> 1;
+    const int per_kv = r * (q_hi - q_lo);
+    const int rem = item % per_kv;
+    const int hl = (item / per_kv) * r + rem % r;
+    const int q = q_hi - 1 - rem / r;
+    const int mA = (2 * q >= row_lo) ? 2 * q : -1, mB = (2 * q + 1 < row_hi) ? 2 * q + 1 : -1;
+    const int ca = mA < 0 ? 0 : __ldg(block_cnt + static_cast<long long>(hl) * M + mA);
+    const int cb = mB < 0 ? 0 : __ldg(block_cnt + static_cast<long long>(hl) * M + mB);
     int inter = 0;
-    for (int i = lane; i < ca; i += 32) {
-        const int v = __ldg(A + i);
-        int lo = 0, hi = cb;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (__ldg(B + mid) < v) lo = mid + 1;
-            else hi = mid;
+    if (ca > 0 && cb > 0) {
+        const int* A = block_idx + (static_cast<long long>(hl) * M + mA) * M;
+        const int* B = block_idx + (static_cast<long long>(hl) * M + mB) * M;
+        for (int i = lane; i < ca; i += 32) {
+            const int v = __ldg(A + i);
+            int lo = 0, hi = cb;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(B + mid) < v) lo = mid + 1;
+                else hi = mid;
+            }
+            inter += (lo < cb && __ldg(B + lo) == v);
         }
-        inter += (lo < cb && __ldg(B + lo) == v);
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+        for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    }
     if (lane == 0) ucnt[item] = ca + cb - inter;
 }
 
@@ -742,7 +750,7 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
     if (!((D.d == 64 || D.d == 128) && (D.b == 64 || D.b == 128))) return cudaErrorInvalidValue;
     CUtensorMap mq, mk, mv;
-    if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, D.b, D.d) ||
+    if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128, D.d) ||
         !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d) ||
         !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d))
         return cudaErrorInvalidValue;
@@ -768,8 +776,9 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const bool pair = D.b == 64;
-    const int units = pair ? D.Hkvl * ((D.r + 1) / 2) : D.Hl;   // work units per block row
-    const size_t n_items = static_cast<size_t>(units) * static_cast<size_t>(D.re - D.rb);
+    // work units: (head, block row), or (head, row pair) for b = 64
+    const int nrows = pair ? (D.re + 1) / 2 - D.rb / 2 : D.re - D.rb;
+    const size_t n_items = static_cast<size_t>(D.Hl) * static_cast<size_t>(nrows);
     SchedBuf* sb = sched_for(st, n_items);
     if (!sb) return cudaErrorMemoryAllocation;
     cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);

@@ -114,12 +114,21 @@ def work_share(block_cnt_full: torch.Tensor, n_kv_heads: int, world: int) -> lis
     return out
 
 
-def zigzag_rows(M: int, world: int, rank: int) -> list[tuple[int, int]]:
+def row_align(cfg) -> int:
+    """Block rows per attention work unit: 2 for block size 64 (the kernel packs the row pair
+    (2q, 2q+1) of one head into its 128 lanes), else 1.  Row ranges aligned to it give
+    outputs bit-identical to the unsharded launch."""
+    return 2 if cfg.block_size == 64 else 1
+
+
+def zigzag_rows(M: int, world: int, rank: int, align: int = 1) -> list[tuple[int, int]]:
     """Block-row ranges of `rank` under zig-zag sharding: chunks p and 2P-1-p of 2P
-    near-equal chunks of [0, M) (empty ranges dropped)."""
-    if world < 1 or not (0 <= rank < world):
-        raise ValueError("bad world/rank")
-    edges = [(M * k) // (2 * world) for k in range(2 * world + 1)]
+    near-equal chunks of [0, M) (empty ranges dropped), with inner edges on multiples of
+    `align` rows."""
+    if world < 1 or not (0 <= rank < world) or align < 1:
+        raise ValueError("bad world/rank/align")
+    Mu = (M + align - 1) // align
+    edges = [min(M, align * ((Mu * k) // (2 * world))) for k in range(2 * world + 1)]
     out = []
     for c in (rank, 2 * world - 1 - rank):
         b, e = edges[c], edges[c + 1]
@@ -152,10 +161,10 @@ def prefill_rows(cfg, Q, K, V, block_cnt, block_idx, O, ranges, prefill=None):
     return O
 
 
-def row_work_share(block_cnt_full: torch.Tensor, world: int) -> list[float]:
+def row_work_share(block_cnt_full: torch.Tensor, world: int, align: int = 1) -> list[float]:
     """Executed (head, row, block) units per rank under zig-zag row sharding, as fractions."""
     per_row = block_cnt_full.double().sum(dim=0)
     tot = float(per_row.sum())
     M = per_row.numel()
-    return [sum(float(per_row[b:e].sum()) for b, e in zigzag_rows(M, world, r)) / tot
+    return [sum(float(per_row[b:e].sum()) for b, e in zigzag_rows(M, world, r, align)) / tot
             for r in range(world)]

@@ -162,23 +162,25 @@ def test_work_share_sums_to_one():
 
 # ----------------------------------------------------------- zig-zag row sharding --
 def test_zigzag_rows_cover_exactly_once_and_balance_linear_rows():
-    for M in (16, 1000, 1024, 2048, 7):
-        for P in (1, 2, 4, 8):
-            if 2 * P > M:
-                continue
-            seen = np.zeros(M, int)
-            loads = []
-            for r in range(P):
-                rr = shard.zigzag_rows(M, P, r)
-                assert len(rr) <= 2
-                load = 0
-                for b, e in rr:
-                    seen[b:e] += 1
-                    load += sum(m + 1 for m in range(b, e))       # K_{h,m} ~ (m+1) (Z12)
-                loads.append(load)
-            assert np.all(seen == 1)
-            if M >= 64:
-                assert max(loads) / (sum(loads) / P) < 1.02, (M, P, loads)
+    for align in (1, 2):                 # 2: block size 64 (the kernel's row pairs)
+        for M in (16, 1000, 1024, 2048, 7, 2047):
+            for P in (1, 2, 4, 8):
+                if 2 * P * align > M:
+                    continue
+                seen = np.zeros(M, int)
+                loads = []
+                for r in range(P):
+                    rr = shard.zigzag_rows(M, P, r, align)
+                    assert len(rr) <= 2
+                    load = 0
+                    for b, e in rr:
+                        assert b % align == 0 and (e % align == 0 or e == M)
+                        seen[b:e] += 1
+                        load += sum(m + 1 for m in range(b, e))       # K_{h,m} ~ (m+1) (Z12)
+                    loads.append(load)
+                assert np.all(seen == 1)
+                if M >= 64:
+                    assert max(loads) / (sum(loads) / P) < 1.01 + 0.01 * align, (M, P, align, loads)
 
 
 def test_zigzag_balance_on_bimodal_budgets_vs_head_sharding():
