@@ -135,13 +135,16 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
-                int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt) {
+                int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt,
+                int diag_noload) {
     using Sh = Shape<kD, kB>;
     constexpr bool kPair = (kB == 64);
     constexpr int kNB = kPair ? 2 : 1;   // S / P buffers per stream (a 64-key S is 64 columns)
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B aligned base, derived from the __shared__ array by pointer arithmetic so that
+    // the compiler keeps the shared state space (LDS/STS, not generic loads, for the barriers
+    // and exchange arrays)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sQ = smem;
     uint8_t* sK = smem + Sh::kQTile;
     uint8_t* sV = sK + Sh::kKTile * kKStages;
@@ -271,6 +274,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             int mem;
                             const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                            if (diag_noload && gk >= kKStages) {   // diagnostics: stale tile, no L2 traffic
+                                mbar_arrive(&bars->k_full[st]);
+                                continue;
+                            }
                             mbar_expect_tx(&bars->k_full[st], Sh::kKTile);
 #pragma unroll
                             for (int ch = 0; ch < kD / 64; ++ch)
@@ -297,6 +304,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         int mem;
                         const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                        if (diag_noload && gv >= kVStages) {
+                            mbar_arrive(&bars->v_full[st]);
+                            continue;
+                        }
                         mbar_expect_tx(&bars->v_full[st], Sh::kKTile);
 #pragma unroll
                         for (int ch = 0; ch < kD / 64; ++ch)
@@ -312,7 +323,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t dk = sdesc_sw128(smem_u32(sK), 16, 1024);
             const bool leader = elect_one();
-            int gk = 0, gs[2] = {0, 0};
+            int gk = 0, gs0 = 0, gs1 = 0;   // per-stream S counts (scalars: no local-memory array)
             for (int it = 0;; ++it) {
                 const Item x = get_item(it);
                 if (x.item < 0) break;
@@ -320,9 +331,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 for (int pass = 0; pass < passes; ++pass) {
                     for (int j = 0; j < x.cnt; ++j, ++gk) {
                         const int s = j & 1;
-                        const int sb = gs[s] % kNB;       // this stream's S buffer
-                        if (gs[s] >= kNB) mbar_wait(&bars->s_free[s][sb], ((gs[s] / kNB) - 1) & 1);
-                        ++gs[s];
+                        const int gss = s ? gs1 : gs0;
+                        const int sb = gss % kNB;         // this stream's S buffer
+                        if (gss >= kNB) mbar_wait(&bars->s_free[s][sb], ((gss / kNB) - 1) & 1);
+                        if (s) ++gs1;
+                        else ++gs0;
                         const int st = gk % kKStages;
                         mbar_wait(&bars->k_full[st], (gk / kKStages) & 1);
                         tc_fence_after();
@@ -349,7 +362,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             constexpr uint32_t idesc_pv = idesc_bf16_f32(128, kD, 0, 1);
             const uint64_t dv = sdesc_sw128(smem_u32(sV), Sh::kKBox, 1024);
             const bool leader = elect_one();
-            int gv = 0, gp[2] = {0, 0};
+            int gv = 0, gp0 = 0, gp1 = 0;   // per-stream P counts
             for (int it = 0;; ++it) {
                 const Item x = get_item(it);
                 if (x.item < 0) break;
@@ -358,10 +371,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     const int st = gv % kVStages;
                     mbar_wait(&bars->v_full[st], (gv / kVStages) & 1);
                     if (j == 0 && it > 0) mbar_wait(&bars->o_free, (it - 1) & 1);   // O read out
-                    const int pb = gp[s] % kNB;           // this stream's P buffer
+                    const int gps = s ? gp1 : gp0;
+                    const int pb = gps % kNB;             // this stream's P buffer
 #pragma unroll
                     for (int half = 0; half < Sh::kHalves; ++half) {
-                        mbar_wait(&bars->p_full[s][kPair ? pb : half], (gp[s] / kNB) & 1);
+                        mbar_wait(&bars->p_full[s][kPair ? pb : half], (gps / kNB) & 1);
                         tc_fence_after();
                         if (leader) {
                             const uint64_t b0 = dv + (st * Sh::kKTile >> 4);
@@ -374,7 +388,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         }
                         __syncwarp();
                     }
-                    ++gp[s];
+                    if (s) ++gp1;
+                    else ++gp0;
                     if (leader) {
                         tc_commit(&bars->v_empty[st]);
                         tc_commit(&bars->p_free[s][pb]);
@@ -730,7 +745,7 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
 
 using AttnKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, __nv_bfloat16*,
                             const int*, const int*, int, int, int, float, int, int, int, Sched*, int*,
-                            int, long long, long long, const int*);
+                            int, long long, long long, const int*, int);
 
 template <int kD, int kB, int kEmu>
 AttnKernel kernel_with_attr() {
@@ -789,6 +804,13 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
+    // PROXYATTN_DIAG_NOLOAD=1 (diagnostics only, WRONG results): K/V TMA loads after the
+    // first ring fill are skipped, so the launch time excludes the L2 -> SMEM traffic
+    static int noload = -1;
+    if (noload < 0) {
+        const char* e = getenv("PROXYATTN_DIAG_NOLOAD");
+        noload = (e && e[0] == '1') ? 1 : 0;
+    }
     const size_t smem = D.d == 128 ? (D.b == 128 ? Shape<128, 128>::kSmem : Shape<128, 64>::kSmem)
                                    : (D.b == 128 ? Shape<64, 128>::kSmem : Shape<64, 64>::kSmem);
     // fast launch over every row, then the exact launch over the rows it flagged (usually
@@ -798,7 +820,7 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         kern<<<grid, kThreads, smem, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
             D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
-            D.q_hs, D.q_ts, sb->ucnt);
+            D.q_hs, D.q_ts, sb->ucnt, noload);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

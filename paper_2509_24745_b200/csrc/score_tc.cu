@@ -107,8 +107,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int nt = u_end - u_begin;
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B aligned base, derived from the __shared__ array by pointer arithmetic so that
+    // the compiler keeps the shared state space (LDS/STS, not generic loads, for the barriers
+    // and exchange arrays)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + kTile;
     SBars* bars = reinterpret_cast<SBars*>(smem + kTile * (1 + kStages));

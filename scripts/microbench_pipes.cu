@@ -34,6 +34,9 @@ __global__ void k(float* out, long long* cyc, float seed) {
             if (OP == 3) u[i] ^= f2bf(x[i], __uint_as_float(u[i]));
             if (OP == 4) x[i] = fmax3(x[i], x[(i + 1) & 7], seed);
             if (OP == 5) x[i] = ffma(x[i], seed, x[i]);
+            if (OP == 6) { x[i] = ex2(x[i]); u[i] ^= f2bf(x[(i + 4) & 7], __uint_as_float(u[i])); }   // MUFU + F2FP
+            if (OP == 7) { x[i] = ex2(x[i]); y[i] = ffma2(y[i], c2, y[i]); }                         // MUFU + FFMA2
+            if (OP == 8) { x[i] = ex2(x[i]); u[i] = (u[i] + 0x7fffu + ((u[i] >> 16) & 1u)) & 0xffff0000u; }  // MUFU + ALU bf16 RNE
         }
     }
     long long t1 = clock64();
@@ -46,12 +49,13 @@ __global__ void k(float* out, long long* cyc, float seed) {
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const char* names[] = {"MUFU.EX2", "FFMA2", "FADD2", "F2FP.BF16x2", "FMNMX3", "FFMA"};
+    const char* names[] = {"MUFU.EX2", "FFMA2", "FADD2", "F2FP.BF16x2", "FMNMX3", "FFMA",
+                           "EX2+F2FP", "EX2+FFMA2", "EX2+ALU-RNE"};
     float* out; long long* cyc;
     cudaMalloc(&out, sizeof(float) * sms * 1024);
     cudaMalloc(&cyc, sizeof(long long) * sms);
     for (int warps : {4, 8, 16, 32}) {
-        for (int op = 0; op < 6; ++op) {
+        for (int op = 0; op < 9; ++op) {
             auto run = [&]() {
                 switch (op) {
                     case 0: k<0><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
@@ -60,6 +64,9 @@ int main() {
                     case 3: k<3><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
                     case 4: k<4><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
                     case 5: k<5><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
+                    case 6: k<6><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
+                    case 7: k<7><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
+                    case 8: k<8><<<sms, warps * 32>>>(out, cyc, 0.5f); break;
                 }
             };
             run();
