@@ -344,9 +344,25 @@ def run_ours(args):
 
     my_rows = shard.zigzag_rows(M, ws, rank, shard.row_align(cfg)) if sharding == "rows" else [(0, M)]
 
+    def gather_kstar(dst, src):     # Alg. 1's K* of every head (Hq int32) from all ranks
+        import torch.distributed as dist
+
+        if same_dev:                 # gloo-only test mode: through host memory
+            parts = [torch.empty_like(src.cpu()) for _ in range(ws)]
+            dist.all_gather(parts, src.cpu())
+            dst.copy_(torch.cat(parts))
+        else:
+            dist.all_gather_into_tensor(dst, src)
+
+    alg1_sharded = sharding == "rows" and ws > 1 and args.alg1 == "sharded"
+
+    def alg1():                      # head-sharded Alg. 1 + all-gather of K* (eager: a collective)
+        shard.budgets_sharded(cfg, Ql, Kl, ws, rank, wsp, all_gather=gather_kstar, out=(kstar, budget))
+
     def estimate():
-        if sharding == "rows" and ws > 1:   # lists of this rank's rows only, no cross-GPU traffic
-            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx))
+        if sharding == "rows" and ws > 1:   # lists of this rank's rows only
+            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx),
+                                kstar_given=alg1_sharded)
         elif sharding == "rows":
             pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
         else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums
@@ -378,6 +394,8 @@ def run_ours(args):
     with torch.cuda.stream(st):
         for _ in range(args.warmup):
             flush.zero_()
+            if alg1_sharded:
+                alg1()
             estimate()
             prefill()
         barrier()
@@ -397,6 +415,8 @@ def run_ours(args):
             for i in range(args.steps):
                 flush.zero_()                    # L2 flush, outside the events
                 ev[i][0].record(st)
+                if alg1_sharded:
+                    alg1()
                 run_est()
                 ev[i][1].record(st)
                 run_pre()
@@ -522,8 +542,9 @@ def run_ours(args):
                    "head_dim": d, "seq_len": w["seq_len"], "block": b, "stride": w["stride"],
                    "proxy_groups": w["n_groups"], "gamma": w["gamma"],
                    "min_budget_tokens": w["min_budget_tokens"],
-                   "parallelism": (f"zig-zag block rows x{ws}" if sharding == "rows" else
-                                   f"kv-head groups x{ws}") if ws > 1 else "single GPU",
+                   "parallelism": (f"zig-zag block rows x{ws}" + (", Alg. 1 head-sharded + all-gather of K*"
+                                                                  if alg1_sharded else "")
+                                   if sharding == "rows" else f"kv-head groups x{ws}") if ws > 1 else "single GPU",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "launch": "CUDA graphs (estimate, prefill)" if use_graph else "eager"},
         "speedup_vs_dense": dense_m / layer_ms,
@@ -607,6 +628,9 @@ def main():
     ap.add_argument("--shard", default="rows", choices=["rows", "heads"],
                     help="N > 1: zig-zag query-block-row sharding (balanced, no traffic) or "
                          "KV-head-group sharding (all-reduce of pooled sums when g < N)")
+    ap.add_argument("--alg1", default="sharded", choices=["sharded", "replicated"],
+                    help="N > 1 with row sharding: Alg. 1 per head on its head shard + all-gather "
+                         "of K* (default), or replicated on every rank")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--no-lib-dense", action="store_true",

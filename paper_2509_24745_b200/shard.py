@@ -14,7 +14,8 @@
   scores and selection of its rows only; Alg. 1 replicated) and the attention of two row
   chunks p and 2P-1-p; since K_{h,m} grows ~linearly in m for every head (reading Z12), the
   pair sums to the same work on every rank regardless of how budgets differ between heads,
-  with no cross-GPU traffic at all.
+  with no cross-GPU traffic at all.  Alg. 1 (per head, needed by every rank) is either
+  replicated or sharded by heads with an all-gather of the Hq K* values (budgets_sharded).
 
 The ops are the C-ABI calls of paper_2509_24745_b200 by default; tests inject other ops
 with the same signatures to check the orchestration on CPU with the gloo backend.
@@ -137,17 +138,54 @@ def zigzag_rows(M: int, world: int, rank: int, align: int = 1) -> list[tuple[int
     return sorted(out)
 
 
-def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None):
+def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, kstar_given=False):
     """A1-A6 for the block-row ranges only (zig-zag row sharding): the first call computes
-    Alg. 1's kstar for every head, the others reuse it (KSTAR_GIVEN); block lists are
-    written for the rows of the ranges only.  Returns (kstar, budget, block_cnt, block_idx)."""
+    Alg. 1's kstar for every head, the others reuse it (KSTAR_GIVEN); with kstar_given the
+    caller has filled out[0] already (budgets_sharded) and every call reuses it.  Block lists
+    are written for the rows of the ranges only.  Returns (kstar, budget, block_cnt, block_idx)."""
     if estimate is None:
         from . import _lib
 
         estimate = _lib.estimate
     for k, (b, e) in enumerate(ranges):
-        out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=k > 0), Q, K, workspace, out)
+        out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=kstar_given or k > 0), Q, K,
+                       workspace, out)
     return out
+
+
+def budgets_sharded(cfg, Q, K, world: int, rank: int, workspace=None, budgets=None,
+                    all_gather=None, out=None):
+    """Alg. 1 (A4) sharded by KV-aligned head ranges under zig-zag row sharding: rank p runs
+    it for its heads only and the per-head K* (Hq int32, 4 B each) are all-gathered, so the
+    per-rank estimate no longer repeats Alg. 1 for every head (~0.3 ms at 128K).  K* of a
+    head depends on that head's Q and K only, so the gathered vector equals the
+    replicated one bit for bit.  Q/K are the full head-major tensors.  Returns (kstar, budget)
+    for all heads; falls back to the replicated call when the KV heads do not split evenly."""
+    if budgets is None:
+        from . import _lib
+
+        budgets = _lib.budgets
+    Hq, Hkv = cfg.n_q_heads, cfg.n_kv_heads
+    if world == 1 or Hkv % world:
+        ks, bu = budgets(cfg, Q, K, workspace)
+        if out is None:
+            return ks, bu
+        out[0].copy_(ks)
+        out[1].copy_(bu)
+        return out[0], out[1]
+    if all_gather is None:
+        import torch.distributed as dist
+
+        all_gather = dist.all_gather_into_tensor
+    b, e = head_shard(Hq, Hkv, world, rank)
+    r = Hq // Hkv
+    loc = cfg.replace(q_head_begin=b, q_head_end=e, row_begin=0, row_end=0)
+    ks_loc, _ = budgets(loc, Q[b:e], K[b // r:e // r], workspace)
+    kstar = out[0] if out is not None else torch.empty(Hq, dtype=torch.int32, device=ks_loc.device)
+    all_gather(kstar, ks_loc.contiguous())
+    budget = out[1] if out is not None else torch.empty(Hq, dtype=torch.float32, device=ks_loc.device)
+    torch.div(kstar.float(), float(cfg.M), out=budget)       # b_h = K*_h / M (Alg. 1 line 4)
+    return kstar, budget
 
 
 def prefill_rows(cfg, Q, K, V, block_cnt, block_idx, O, ranges, prefill=None):

@@ -237,3 +237,52 @@ def test_zigzag_sharded_attention_equals_unsharded_oracle():
     Q, K, V, _ = workloads.structured(4, 2, 1024, 16, seed=5, dtype=torch.bfloat16)
     ref = oracle.pipeline(oc, Q.float().numpy(), K.float().numpy(), V.float().numpy())["O"]
     assert np.max(np.abs(O - ref)) == 0.0
+
+
+# ----------------------------------------------- head-sharded Alg. 1 + K* all-gather --
+def _alg1_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oc = oracle.Cfg(8, 4, 16, 1024, 64, 4, 1, 0.9, round_bf16=True)
+        Q, K, V, _ = workloads.structured(8, 4, 1024, 16, seed=9, dtype=torch.bfloat16)
+        Qf, Kf = Q.float().numpy(), K.float().numpy()
+        calls = []
+
+        def budgets(cfg, Q_, K_, workspace=None):          # oracle op on the shard's heads
+            b, e = cfg.q_head_begin, cfg.q_head_end
+            calls.append((b, e))
+            assert Q_.shape[0] == e - b and K_.shape[0] == (e - b) // 2
+            ks, bu, _, _ = oracle.budgets(oc, Qf, Kf, heads=list(range(b, e)))
+            return (torch.tensor(ks[b:e], dtype=torch.int32), torch.tensor(bu[b:e], dtype=torch.float32))
+
+        def all_gather(dst, src):
+            parts = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(parts, src)
+            dst.copy_(torch.cat(parts))
+
+        cfg = Config(8, 4, 16, 1024, 64, 4, 1, 0.9)
+        ks, bu = shard.budgets_sharded(cfg, Q, K, world, rank, budgets=budgets, all_gather=all_gather)
+        assert len(calls) == 1 and calls[0] == shard.head_shard(8, 4, world, rank)
+        if rank == 0:
+            q.put((ks.numpy(), bu.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_sharded_alg1_gathers_the_replicated_kstar():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_alg1_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ks, bu = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    oc = oracle.Cfg(8, 4, 16, 1024, 64, 4, 1, 0.9, round_bf16=True)
+    Q, K, V, _ = workloads.structured(8, 4, 1024, 16, seed=9, dtype=torch.bfloat16)
+    ref, _, _, _ = oracle.budgets(oc, Q.float().numpy(), K.float().numpy())
+    assert np.array_equal(ks, ref)                           # every head, bit for bit
+    assert np.allclose(bu, ref / oc.M)

@@ -167,3 +167,21 @@ def test_determinism_pair_kernel():
     Ob = pa.prefill(cfg, Qd, Kd, Vd, b[2], b[3])
     valid = torch.arange(cfg.M, device=DEV)[None, None, :] < a[2][:, :, None]   # first cnt entries
     assert torch.equal(a[2], b[2]) and torch.equal(a[3][valid], b[3][valid]) and torch.equal(Oa, Ob)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_head_sharded_budgets_concat_equal_full(world):
+    # shard.budgets_sharded's building block: Alg. 1 on each KV-aligned head shard (the
+    # local Q / K slices through the C-ABI), concatenated = the all-head call, bit for bit
+    from paper_2509_24745_b200 import shard
+    cfg = cfg_of(128, 128, 4096, heads=(8, 4))
+    Q, K, V, _ = workloads.structured(8, 4, 4096, 128, seed=70)
+    Qd, Kd, _ = to_dev(Q, K, V)
+    full, _ = pa.budgets(cfg, Qd, Kd)
+    parts = []
+    for rank in range(world):
+        def gather(dst, src, rank=rank):
+            parts.append(src.clone())
+            dst.zero_()
+        shard.budgets_sharded(cfg, Qd, Kd, world, rank, all_gather=gather)
+    assert torch.equal(torch.cat(parts), full)
