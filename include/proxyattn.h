@@ -18,7 +18,10 @@
  *  - Element type: bf16 (__nv_bfloat16) by default; fp32 when PROXYATTN_FLAG_FP32_DEBUG.
  *  - Per-head outputs (kstar, budget, block_cnt, block_idx) are indexed by local head.
  *  - All work is enqueued on `stream` (a cudaStream_t, passed as void*); no call
- *    synchronises the host except proxyattn_forward_host.
+ *    synchronises the host except proxyattn_forward_host.  proxyattn_estimate forks
+ *    Alg. 1 onto a library-owned per-device stream and joins it back to `stream` by
+ *    events before returning, so its completion is still ordered on `stream` (and the
+ *    call is capturable in a CUDA graph); PROXYATTN_SERIAL_ESTIMATE=1 disables the fork.
  *  - The library allocates no device memory: scratch comes from the caller's workspace.
  *  - Return codes: PROXYATTN_OK or one of the negative PROXYATTN_E_* codes; a
  *    human-readable reason is available from proxyattn_last_error() (thread-local).

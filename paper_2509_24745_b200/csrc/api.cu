@@ -169,12 +169,54 @@ int run_budgets(const pa::Dims& D, const void* Q, const void* K, void* ws, const
         return PROXYATTN_OK;
     }
     if (pa::score_tc_supported(D)) {
-        PA_CUDA(pa::launch_budget_tc(D, Q, K, at<float>(ws, W.scratch), bmass, st), "budget_tc");
+        PA_CUDA(pa::launch_budget_tc(D, Q, K, at<float>(ws, W.scratch_b), bmass, st), "budget_tc");
     } else {
         PA_CUDA(pa::launch_budget_lse(D, Q, K, blse, st), "budget_lse");
         PA_CUDA(pa::launch_budget_mass(D, Q, K, blse, bmass, st), "budget_mass");
     }
     PA_CUDA(pa::launch_budget_finalize(D, bmass, kstar, budget, st), "budget_finalize");
+    return PROXYATTN_OK;
+}
+
+// Per-device auxiliary stream of proxyattn_estimate (non-blocking, created once): Alg. 1
+// runs on it concurrently with A1-A3 (fork / join by events, so the pair stays capturable
+// in a CUDA graph).  PROXYATTN_SERIAL_ESTIMATE=1 keeps everything on the caller's stream.
+struct AuxEvents {
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+// fork / join events of the calling thread on the current device (reused: record -> wait
+// pairs are ordered on the host, and nothing is created or destroyed inside a capture)
+int estimate_events(AuxEvents* out) {
+    thread_local std::map<int, AuxEvents> per_dev;
+    int dev = 0;
+    PA_CUDA(cudaGetDevice(&dev), "get device");
+    AuxEvents& e = per_dev[dev];
+    if (!e.fork) {
+        PA_CUDA(cudaEventCreateWithFlags(&e.fork, cudaEventDisableTiming), "event create");
+        PA_CUDA(cudaEventCreateWithFlags(&e.join, cudaEventDisableTiming), "event create");
+    }
+    *out = e;
+    return PROXYATTN_OK;
+}
+
+int estimate_aux(cudaStream_t* aux) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> per_dev;
+    static int serial = -1;
+    if (serial < 0) {
+        const char* e = getenv("PROXYATTN_SERIAL_ESTIMATE");
+        serial = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (serial) {
+        *aux = nullptr;
+        return PROXYATTN_OK;
+    }
+    int dev = 0;
+    PA_CUDA(cudaGetDevice(&dev), "get device");
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& s = per_dev[dev];
+    if (!s) PA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    *aux = s;
     return PROXYATTN_OK;
 }
 
@@ -267,10 +309,29 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
         tr1 = static_cast<int>((i_end + 127) / 128);
         q_i0 = static_cast<long long>(tr0) * 128;
     }
+    // Alg. 1 (A4) depends on Q and K only: fork it onto the auxiliary stream so it overlaps
+    // A1-A3 (their kernels are MUFU- / latency-bound with tails; the pool is HBM-bound),
+    // join before A5-A6.  Separate scratch regions (W.scratch vs W.scratch_b).
+    const bool alg1 = !(D.flags & PROXYATTN_FLAG_KSTAR_GIVEN);
+    cudaStream_t aux = nullptr;
+    if (alg1 && pa::score_tc_supported(D) && D.static_kstar == 0) {
+        if ((rc = estimate_aux(&aux))) return rc;
+    }
+    AuxEvents ev{};
+    if (aux) {
+        if ((rc = estimate_events(&ev))) return rc;
+        PA_CUDA(cudaEventRecord(ev.fork, st), "record");
+        PA_CUDA(cudaStreamWaitEvent(aux, ev.fork, 0), "wait");
+        rc = run_budgets(D, Q, K, ws, W, kstar, budget, aux);
+        if (rc) return rc;
+        PA_CUDA(cudaEventRecord(ev.join, aux), "record");
+    }
     PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st, q_i0, i_end), "pool");
     rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st, tr0, tr1);
     if (rc) return rc;
-    if (!(D.flags & PROXYATTN_FLAG_KSTAR_GIVEN)) {
+    if (aux) {
+        PA_CUDA(cudaStreamWaitEvent(st, ev.join, 0), "wait");
+    } else if (alg1) {
         rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
         if (rc) return rc;
     }

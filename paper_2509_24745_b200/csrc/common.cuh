@@ -97,9 +97,10 @@ constexpr float kLn2 = 0.6931471805599453f;
 
 // Workspace carve-up of proxyattn_estimate (all offsets 256-B aligned).
 struct Workspace {
-    size_t pq, pk, lse, L, blse, bmass, scratch, total;
+    size_t pq, pk, lse, L, blse, bmass, scratch, scratch_b, total;
 };
 size_t score_tc_scratch_bytes(const Dims& D);
+size_t score_tc_budget_scratch_bytes(const Dims& D);
 bool score_tc_supported(const Dims& D);
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline Workspace workspace_layout(const Dims& D) {
@@ -113,6 +114,8 @@ inline Workspace workspace_layout(const Dims& D) {
     w.blse = off;  off = align256(off + (size_t)D.Hl * D.b * 4);
     w.bmass = off; off = align256(off + (size_t)D.Hl * D.M * 4);
     w.scratch = off; off = align256(off + (score_tc_supported(D) ? score_tc_scratch_bytes(D) : 0));
+    // Alg. 1's partials get their own region: the budget pass runs concurrently with A1-A3
+    w.scratch_b = off; off = align256(off + (score_tc_supported(D) ? score_tc_budget_scratch_bytes(D) : 0));
     w.total = off;
     return w;
 }

@@ -590,13 +590,16 @@ bool score_tc_supported(const Dims& D) {
 size_t score_tc_scratch_bytes(const Dims& D) {
     const int n_tr = static_cast<int>((D.Ns + 127) / 128);
     const int n_chunks = (n_tr + kChunk - 1) / kChunk;
-    // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]; A4: (m, s) partials + the
-    // combine's chunk partials.  The two passes run one after the other and share it.
-    const size_t lse_parts = 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 +
-                             static_cast<size_t>(D.gl) * D.Ns * D.M * 4;
+    // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]
+    return 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 +
+           static_cast<size_t>(D.gl) * D.Ns * D.M * 4;
+}
+
+size_t score_tc_budget_scratch_bytes(const Dims& D) {
+    // A4: (m, s) partials [Hl][M][128] + the combine's chunk partials (own region: the
+    // budget pass may run concurrently with A2/A3)
     const size_t n_comb = (D.M + kCombChunk - 1) / kCombChunk;
-    const size_t bud_parts = 2ull * D.Hl * D.M * 128 * 4 + 2ull * D.Hl * n_comb * 128 * 4;
-    return lse_parts > bud_parts ? lse_parts : bud_parts;
+    return 2ull * D.Hl * D.M * 128 * 4 + 2ull * D.Hl * n_comb * 128 * 4;
 }
 
 // A2 + A3 on tcgen05.  scratch: score_tc_scratch_bytes(D); lse_nat (may be null) receives
