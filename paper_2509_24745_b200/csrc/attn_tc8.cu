@@ -781,10 +781,16 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
                                                           : kernel_with_attr<128, 128, 4>();
     } else if (D.d == 128) {
         kern = kernel_with_attr<128, 64, 2>();
-    } else if (D.b == 128) {   // d = 64: half the tensor work per exp2 -> more of them on the FMA pipe
-        kern = kernel_with_attr<64, 128, 4>();
+    } else if (D.b == 128) {   // d = 64 (exp-bound: half the tensor work per exp2)
+        static int emu64 = -1;   // PROXYATTN_EXP_EMU64=2..4; 2/8 measured best at 128K
+        if (emu64 < 0) {         // (13.2-13.3 ms vs 13.4-13.6 at 3/8 and 13.8 at 4/8)
+            const char* e = getenv("PROXYATTN_EXP_EMU64");
+            emu64 = (e && e[0] >= '2' && e[0] <= '4') ? e[0] - '0' : 2;
+        }
+        kern = emu64 == 2 ? kernel_with_attr<64, 128, 2>() : emu64 == 3 ? kernel_with_attr<64, 128, 3>()
+                                                                           : kernel_with_attr<64, 128, 4>();
     } else {
-        kern = kernel_with_attr<64, 64, 4>();
+        kern = kernel_with_attr<64, 64, 2>();
     }
     if (!kern) return cudaErrorInvalidValue;
     int dev = 0, n_sm = 0;
