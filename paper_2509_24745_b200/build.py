@@ -36,6 +36,8 @@ def _flags(verbose: bool) -> list[str]:
                 "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         f += ["-Xptxas", "-v"]
+    # experiments only: extra -D defines (e.g. PROXYATTN_NVCC_DEFINES="-DPA_S_EARLY")
+    f += os.environ.get("PROXYATTN_NVCC_DEFINES", "").split()
     return f
 
 
