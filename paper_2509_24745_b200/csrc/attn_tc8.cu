@@ -136,7 +136,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
                 int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt,
-                int diag_noload) {
+                int diag_noload, const int* __restrict__ kvperm) {
     using Sh = Shape<kD, kB>;
     constexpr bool kPair = (kB == 64);
     constexpr int kNB = kPair ? 2 : 1;   // S / P buffers per stream (a 64-key S is 64 columns)
@@ -194,10 +194,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
 
-    // item decode (kv-head major, heavy rows first): head hl, its block row mA (kB = 128), or
+    // item decode (kv-head major — KV heads in decreasing total work when kvperm is given, so
+    // the last heads scheduled are the lightest — heavy rows first): head hl, its block row mA (kB = 128), or
     // its row pair (mA, mB) = (2q, 2q+1) (kB = 64; -1 for a row outside [row_lo, row_hi))
     auto decode = [&](int item, int& hl, int& mA, int& mB, int& kvl) {
-        kvl = item / per_kv;
+        kvl = kvperm ? __ldg(kvperm + item / per_kv) : item / per_kv;
         const int rem = item % per_kv;
         hl = kvl * r + rem % r;
         if (kPair) {
@@ -251,8 +252,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         x.item = exact ? flagged[k] : k;
                         int hl, mA, mB, kvl;
                         decode(x.item, hl, mA, mB, kvl);
+                        // ucnt is indexed by the natural (unpermuted) kv-head-major item
                         x.cnt = !kPair ? count_of(hl, mA)
-                              : dense ? max(count_of(hl, mA), count_of(hl, mB)) : __ldg(ucnt + x.item);
+                              : dense ? max(count_of(hl, mA), count_of(hl, mB))
+                                      : __ldg(ucnt + kvl * per_kv + x.item % per_kv);
                     }
                     bars->items[slot] = x;
                     mbar_arrive(&bars->item_full[slot]);   // release semantics publish x
@@ -714,12 +717,46 @@ __global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* 
     if (lane == 0) ucnt[item] = ca + cb - inter;
 }
 
+// KV-head order of the persistent schedule: decreasing total selected blocks over the launch's
+// rows (stable), one CTA.  Items stay KV-head-major (a KV head's K/V stay hot in L2) while the
+// heaviest rows of the launch are no longer left to the end when they belong to a late KV head
+// (the tail that limited row-sharded launches at 8 ranks).
+__global__ void __launch_bounds__(256) kv_order_kernel(const int* __restrict__ block_cnt, int M, int r,
+                                                       int row_lo, int row_hi, int n_kv,
+                                                       int* __restrict__ kvperm) {
+    __shared__ long long tot[64];
+    __shared__ long long part[256];
+    for (int kv = 0; kv < n_kv; ++kv) {
+        long long acc = 0;
+        const int n = r * (row_hi - row_lo);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int h = kv * r + i / (row_hi - row_lo), m = row_lo + i % (row_hi - row_lo);
+            acc += __ldg(block_cnt + static_cast<long long>(h) * M + m);
+        }
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) tot[kv] = part[0];
+        __syncthreads();
+    }
+    if (threadIdx.x < n_kv) {
+        const int me = threadIdx.x;
+        int rank = 0;
+        for (int j = 0; j < n_kv; ++j) rank += (tot[j] > tot[me]) || (tot[j] == tot[me] && j < me);
+        kvperm[rank] = me;
+    }
+}
+
 // Per-stream scheduler state + flagged-row list + kB = 64 union counts (grown on demand,
 // never freed).
 struct SchedBuf {
     Sched* sched = nullptr;
     int* flagged = nullptr;
     int* ucnt = nullptr;
+    int* kvperm = nullptr;   // [64]
     size_t cap = 0;
 };
 
@@ -731,6 +768,7 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
     std::lock_guard<std::mutex> lock(mu);
     SchedBuf& b = bufs[{dev, st}];
     if (!b.sched && cudaMalloc(&b.sched, sizeof(Sched)) != cudaSuccess) return nullptr;
+    if (!b.kvperm && cudaMalloc(&b.kvperm, 64 * sizeof(int)) != cudaSuccess) return nullptr;
     if (b.cap < n_items) {   // each row can be appended by up to 4 epilogue warps
         if (b.flagged) cudaFree(b.flagged);
         if (b.ucnt) cudaFree(b.ucnt);
@@ -745,7 +783,7 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
 
 using AttnKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, __nv_bfloat16*,
                             const int*, const int*, int, int, int, float, int, int, int, Sched*, int*,
-                            int, long long, long long, const int*, int);
+                            int, long long, long long, const int*, int, const int*);
 
 template <int kD, int kB, int kEmu>
 AttnKernel kernel_with_attr() {
@@ -809,6 +847,13 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
             block_cnt, block_idx, D.M, D.r, D.rb, D.re, static_cast<int>(n_items), sb->ucnt);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
+    // KV heads in decreasing work (sparse launches with more than one local KV head, <= 64)
+    const int* kvperm = nullptr;
+    if (block_cnt && D.Hkvl > 1 && D.Hkvl <= 64) {
+        kv_order_kernel<<<1, 256, 0, st>>>(block_cnt, D.M, D.r, D.rb, D.re, D.Hkvl, sb->kvperm);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        kvperm = sb->kvperm;
+    }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
     // PROXYATTN_DIAG_NOLOAD=1 (diagnostics only, WRONG results): K/V TMA loads after the
     // first ring fill are skipped, so the launch time excludes the L2 -> SMEM traffic
@@ -826,7 +871,7 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         kern<<<grid, kThreads, smem, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
             D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
-            D.q_hs, D.q_ts, sb->ucnt, noload);
+            D.q_hs, D.q_ts, sb->ucnt, noload, kvperm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -1,0 +1,94 @@
+"""Per-rank step time of the zig-zag row-sharded layer at P ranks, emulated one rank at a time
+on ONE GPU (each rank's exact kernels: head-sharded Alg. 1, the row-range estimate of its two
+chunks, the row-range attention; the K* all-gather replaced by a device copy of the
+replicated K*).  A projection of the per-GPU time at P GPUs (each GPU alone on its share,
+same clocks), not a multi-GPU measurement.
+
+    python scripts/rank_emulation.py [P] [N] [--graph]"""
+import json
+import sys
+
+import torch
+
+import paper_2509_24745_b200 as pa
+from paper_2509_24745_b200 import shard
+import workloads
+
+P = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
+dev = torch.device("cuda:0")
+cfg = pa.Config(32, 8, 128, N, 128, 4, 1, 0.9, 0)
+Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=workloads.PRESETS["llama-128k"], device=dev)
+M = cfg.M
+wsp = pa.alloc_workspace(cfg, dev)
+kfull, _ = pa.budgets(cfg, Q, K, wsp)
+kstar = torch.empty(32, dtype=torch.int32, device=dev)
+budget = torch.empty(32, dtype=torch.float32, device=dev)
+cnt = torch.zeros(32, M, dtype=torch.int32, device=dev)
+idx = torch.empty(32, M, M, dtype=torch.int32, device=dev)
+O = torch.empty_like(Q)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+
+def timed(fn, it=5):
+    for _ in range(2):
+        fn()
+    ts = []
+    for _ in range(it):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        fn(e[1])
+        e[2].record()
+        torch.cuda.synchronize()
+        ts.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])))
+    ts.sort(key=lambda x: x[0] + x[1])
+    return ts[len(ts) // 2]
+
+
+out = []
+full_est, full_att = timed(lambda mid=None: (pa.estimate(cfg, Q, K, wsp, out=(kstar, budget, cnt, idx)),
+                                              mid.record() if mid else None,
+                                              pa.prefill(cfg, Q, K, V, cnt, idx, O)))
+graphs = "--graph" in sys.argv     # replay the row estimate and the attention from CUDA graphs, as bench.py
+for r in range(P):
+    rows = shard.zigzag_rows(M, P, r)
+
+    def alg1(r=r):
+        shard.budgets_sharded(cfg, Q, K, P, r, wsp, all_gather=lambda d, s: d.copy_(kfull), out=(kstar, budget))
+
+    def est_rows(rows=rows):
+        shard.estimate_rows(cfg, Q, K, rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True)
+
+    def att_rows(rows=rows):
+        shard.prefill_rows(cfg, Q, K, V, cnt, idx, O, rows)
+
+    run_e, run_a = est_rows, att_rows
+    if graphs:
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            alg1(); est_rows(); att_rows()
+            torch.cuda.synchronize()
+            ge, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ge, stream=st):
+                est_rows()
+            with torch.cuda.graph(gp, stream=st):
+                att_rows()
+        torch.cuda.synchronize()
+        run_e, run_a = ge.replay, gp.replay
+
+    def step(mid=None):
+        alg1()
+        run_e()
+        if mid is not None:
+            mid.record()
+        run_a()
+
+    est, att = timed(step)
+    out.append({"rank": r, "rows": rows, "estimate_ms": round(est, 4), "attention_ms": round(att, 4),
+                "step_ms": round(est + att, 4)})
+worst = max(o["step_ms"] for o in out)
+print(json.dumps({"P": P, "N": N, "single_gpu_step_ms": round(full_est + full_att, 4),
+                  "max_rank_step_ms": worst, "projected_speedup": round((full_est + full_att) / worst, 2),
+                  "ranks": out}))
