@@ -185,3 +185,28 @@ def test_head_sharded_budgets_concat_equal_full(world):
             dst.zero_()
         shard.budgets_sharded(cfg, Qd, Kd, world, rank, all_gather=gather)
     assert torch.equal(torch.cat(parts), full)
+
+
+@pytest.mark.parametrize("d,b", SHAPES)
+def test_forward_host_matches_device_path(d, b):
+    # the host-buffer entry (pipelined per KV head: sub-shard prefills) at the new shapes
+    cfg = cfg_of(d, b, 2048, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, 2048, d, seed=80)
+    Qh, Kh, Vh = Q.pin_memory(), K.pin_memory(), V.pin_memory()
+    Oh = torch.empty_like(Qh).pin_memory()
+    ks = torch.empty(8, dtype=torch.int32).pin_memory()
+    ws = torch.empty(pa.forward_host_workspace_bytes(cfg), dtype=torch.uint8, device=DEV)
+    pa.forward_host(cfg, Qh, Kh, Vh, Oh, ws, ks)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    torch.cuda.synchronize()
+    assert torch.equal(ks, kstar.cpu()) and torch.equal(Oh, O.cpu())
+
+
+@pytest.mark.parametrize("variant", [dict(force_sink=True), dict(static_kstar=5), dict(constant_k=True)],
+                         ids=["sink", "static5", "constantK"])
+def test_method_variants_block64(variant):
+    cfg = cfg_of(128, 64, 2048, heads=(8, 2)).replace(**variant)
+    Q, K, V, _ = workloads.structured(8, 2, 2048, 128, seed=81)
+    run_staged(cfg, Q, K, V)
