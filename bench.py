@@ -555,6 +555,9 @@ def run_ours(args):
                           if lib_dense else None),
         "estimate_ms": est_m,
         "prefill_ms": att_m,
+        # estimation cost relative to the same-run dense attention (the paper's "< 10 %",
+        # P:614-615; cost model g/(n s^2) = 0.20 % here, Alg. 1 adds about as much, Z22)
+        "estimate_over_dense": est_m / dense_m,
         "sparsity": sparsity,
         "tflops_exec": achieved,
         "roofline": {"bound": "tensor", "kernel": f"{kname} (A7)", "achieved": achieved,
