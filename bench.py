@@ -359,10 +359,14 @@ def run_ours(args):
     def alg1():                      # head-sharded Alg. 1 + all-gather of K* (eager: a collective)
         shard.budgets_sharded(cfg, Ql, Kl, ws, rank, wsp, all_gather=gather_kstar, out=(kstar, budget))
 
+    # the rank's two row chunks are estimated concurrently (own workspace and stream each)
+    est_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if alg1_sharded else None
+    est_ws = [wsp, pa.alloc_workspace(cfg, dev)] if alg1_sharded else None
+
     def estimate():
         if sharding == "rows" and ws > 1:   # lists of this rank's rows only
             shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx),
-                                kstar_given=alg1_sharded)
+                                kstar_given=alg1_sharded, streams=est_streams, workspaces=est_ws)
         elif sharding == "rows":
             pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
         else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums

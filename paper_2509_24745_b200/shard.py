@@ -138,15 +138,33 @@ def zigzag_rows(M: int, world: int, rank: int, align: int = 1) -> list[tuple[int
     return sorted(out)
 
 
-def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, kstar_given=False):
+def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, kstar_given=False,
+                  streams=None, workspaces=None):
     """A1-A6 for the block-row ranges only (zig-zag row sharding): the first call computes
     Alg. 1's kstar for every head, the others reuse it (KSTAR_GIVEN); with kstar_given the
     caller has filled out[0] already (budgets_sharded) and every call reuses it.  Block lists
-    are written for the rows of the ranges only.  Returns (kstar, budget, block_cnt, block_idx)."""
+    are written for the rows of the ranges only.  Returns (kstar, budget, block_cnt, block_idx).
+
+    With kstar_given, `streams` and one workspace per range, the ranges' estimates run
+    concurrently (each is a short chain of small, latency-bound kernels; they write disjoint
+    rows of the outputs), forked from and joined back to the current stream."""
     if estimate is None:
         from . import _lib
 
         estimate = _lib.estimate
+    if kstar_given and streams and workspaces and len(ranges) > 1 and out is not None:
+        cur = torch.cuda.current_stream()
+        used = []
+        for k, (b, e) in enumerate(ranges):
+            s = streams[k % len(streams)]
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=True), Q, K,
+                         workspaces[k % len(workspaces)], out)
+            used.append(s)
+        for s in used:
+            cur.wait_stream(s)
+        return out
     for k, (b, e) in enumerate(ranges):
         out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=kstar_given or k > 0), Q, K,
                        workspace, out)

@@ -51,6 +51,8 @@ full_est, full_att = timed(lambda mid=None: (pa.estimate(cfg, Q, K, wsp, out=(ks
                                               mid.record() if mid else None,
                                               pa.prefill(cfg, Q, K, V, cnt, idx, O)))
 steps = []
+est_streams = [torch.cuda.Stream(), torch.cuda.Stream()]      # as bench.py: chunks in parallel
+est_ws = [wsp, pa.alloc_workspace(cfg, dev)]
 graphs = "--graph" in sys.argv     # replay the row estimate and the attention from CUDA graphs, as bench.py
 for r in range(P):
     rows = shard.zigzag_rows(M, P, r)
@@ -59,7 +61,8 @@ for r in range(P):
         shard.budgets_sharded(cfg, Q, K, P, r, wsp, all_gather=lambda d, s: d.copy_(kfull), out=(kstar, budget))
 
     def est_rows(rows=rows):
-        shard.estimate_rows(cfg, Q, K, rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True)
+        shard.estimate_rows(cfg, Q, K, rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True,
+                            streams=est_streams, workspaces=est_ws)
 
     def att_rows(rows=rows):
         shard.prefill_rows(cfg, Q, K, V, cnt, idx, O, rows)

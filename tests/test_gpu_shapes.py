@@ -210,3 +210,26 @@ def test_method_variants_block64(variant):
     cfg = cfg_of(128, 64, 2048, heads=(8, 2)).replace(**variant)
     Q, K, V, _ = workloads.structured(8, 2, 2048, 128, seed=81)
     run_staged(cfg, Q, K, V)
+
+
+def test_concurrent_row_range_estimates_match_sequential():
+    # bench.py's per-rank estimate at N > 1: K* given (head-sharded Alg. 1), the two zig-zag
+    # chunks estimated on two streams with their own workspaces == one after the other
+    from paper_2509_24745_b200 import shard
+    cfg = cfg_of(128, 128, 8192, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, 8192, 128, seed=90)
+    Qd, Kd, _ = to_dev(Q, K, V)
+    kstar, budget, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    rows = shard.zigzag_rows(cfg.M, 4, 1)
+    assert len(rows) == 2
+    outs = []
+    for conc in (False, True):
+        out = (kstar.clone(), budget.clone(), torch.zeros_like(cnt), torch.full_like(idx, -7))
+        kw = dict(streams=[torch.cuda.Stream(), torch.cuda.Stream()],
+                  workspaces=[pa.alloc_workspace(cfg, DEV), pa.alloc_workspace(cfg, DEV)]) if conc else {}
+        shard.estimate_rows(cfg, Qd, Kd, rows, out=out, kstar_given=True, **kw)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0][2], outs[1][2]) and torch.equal(outs[0][3], outs[1][3])
+    for b, e in rows:
+        assert torch.equal(outs[1][2][:, b:e], cnt[:, b:e])
