@@ -718,36 +718,47 @@ __global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* 
 }
 
 // KV-head order of the persistent schedule: decreasing total selected blocks over the launch's
-// rows (stable), one CTA.  Items stay KV-head-major (a KV head's K/V stay hot in L2) while the
+// rows (stable).  Items stay KV-head-major (a KV head's K/V stay hot in L2) while the
 // heaviest rows of the launch are no longer left to the end when they belong to a late KV head
-// (the tail that limited row-sharded launches at 8 ranks).
-__global__ void __launch_bounds__(256) kv_order_kernel(const int* __restrict__ block_cnt, int M, int r,
-                                                       int row_lo, int row_hi, int n_kv,
-                                                       int* __restrict__ kvperm) {
-    __shared__ long long tot[64];
-    __shared__ long long part[256];
-    for (int kv = 0; kv < n_kv; ++kv) {
-        long long acc = 0;
-        const int n = r * (row_hi - row_lo);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int h = kv * r + i / (row_hi - row_lo), m = row_lo + i % (row_hi - row_lo);
+// (the tail that limited row-sharded launches at 8 ranks).  One CTA per KV head sums its
+// counts; the last CTA to finish ranks the sums (kvsum / done live in the scheduler buffer,
+// `done` returns to 0 for the next launch).
+__global__ void __launch_bounds__(1024) kv_order_kernel(const int* __restrict__ block_cnt, int M, int r,
+                                                        int row_lo, int row_hi, int n_kv,
+                                                        long long* __restrict__ kvsum, int* __restrict__ done,
+                                                        int* __restrict__ kvperm) {
+    __shared__ long long warp_part[32];
+    __shared__ bool last;
+    const int kv = blockIdx.x;
+    long long acc = 0;
+    for (int h = kv * r; h < (kv + 1) * r; ++h)
+        for (int m = row_lo + threadIdx.x; m < row_hi; m += blockDim.x)
             acc += __ldg(block_cnt + static_cast<long long>(h) * M + m);
-        }
-        part[threadIdx.x] = acc;
-        __syncthreads();
-        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-            if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) tot[kv] = part[0];
-        __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += warp_part[w];
+        kvsum[kv] = t;
+        __threadfence();
+        last = atomicAdd(done, 1) == n_kv - 1;
     }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
     if (threadIdx.x < n_kv) {
         const int me = threadIdx.x;
+        const long long tm = *(volatile long long*)(kvsum + me);
         int rank = 0;
-        for (int j = 0; j < n_kv; ++j) rank += (tot[j] > tot[me]) || (tot[j] == tot[me] && j < me);
+        for (int j = 0; j < n_kv; ++j) {
+            const long long tj = *(volatile long long*)(kvsum + j);
+            rank += (tj > tm) || (tj == tm && j < me);
+        }
         kvperm[rank] = me;
     }
+    if (threadIdx.x == 0) *done = 0;
 }
 
 // Per-stream scheduler state + flagged-row list + kB = 64 union counts (grown on demand,
@@ -757,6 +768,8 @@ struct SchedBuf {
     int* flagged = nullptr;
     int* ucnt = nullptr;
     int* kvperm = nullptr;   // [64]
+    long long* kvsum = nullptr;   // [64]
+    int* kvdone = nullptr;
     size_t cap = 0;
 };
 
@@ -768,7 +781,12 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
     std::lock_guard<std::mutex> lock(mu);
     SchedBuf& b = bufs[{dev, st}];
     if (!b.sched && cudaMalloc(&b.sched, sizeof(Sched)) != cudaSuccess) return nullptr;
-    if (!b.kvperm && cudaMalloc(&b.kvperm, 64 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (!b.kvperm) {
+        if (cudaMalloc(&b.kvperm, 64 * sizeof(int)) != cudaSuccess) return nullptr;
+        if (cudaMalloc(&b.kvsum, 64 * sizeof(long long)) != cudaSuccess) return nullptr;
+        if (cudaMalloc(&b.kvdone, sizeof(int)) != cudaSuccess) return nullptr;
+        if (cudaMemset(b.kvdone, 0, sizeof(int)) != cudaSuccess) return nullptr;
+    }
     if (b.cap < n_items) {   // each row can be appended by up to 4 epilogue warps
         if (b.flagged) cudaFree(b.flagged);
         if (b.ucnt) cudaFree(b.ucnt);
@@ -850,7 +868,8 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     // KV heads in decreasing work (sparse launches with more than one local KV head, <= 64)
     const int* kvperm = nullptr;
     if (block_cnt && D.Hkvl > 1 && D.Hkvl <= 64) {
-        kv_order_kernel<<<1, 256, 0, st>>>(block_cnt, D.M, D.r, D.rb, D.re, D.Hkvl, sb->kvperm);
+        kv_order_kernel<<<D.Hkvl, 1024, 0, st>>>(block_cnt, D.M, D.r, D.rb, D.re, D.Hkvl, sb->kvsum,
+                                                 sb->kvdone, sb->kvperm);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         kvperm = sb->kvperm;
     }

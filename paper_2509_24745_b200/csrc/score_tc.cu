@@ -59,7 +59,7 @@ struct ScoreParams {
     int n_chunks;    // chunks per tile row (proxy) / per head (budget)
     int r;           // budget: GQA ratio (local head -> local kv head)
     int bs;          // proxy: sampled rows (= keys) per block, b / s
-    int d;           // head dim (64 or 128): K of the MMAs, 64-column boxes per tile
+    int d;           // head dim (64 or 128; the kernel's kD)
     int b;           // budget: block size (64 or 128); key tiles hold 128 / b blocks
     int n_kt;        // budget: 128-key tiles
     float sc2;       // logit scale in log2 units
@@ -72,8 +72,8 @@ struct ScoreParams {
 };
 
 // kEmu: of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4); kB64: budget pass
-// with b = 64 (two key blocks per 128-key tile)
-template <int kEmu, bool kB64>
+// with b = 64 (two key blocks per 128-key tile); kD: head dim (K of the MMAs)
+template <int kEmu, bool kB64, int kD>
 __global__ void __launch_bounds__(kThreads, 2)
 score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 ScoreParams p) {
@@ -142,7 +142,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (p.mode == kBudget) tma_load_3d(dst, map, bar, col, row, head);
                 else tma_load_2d(dst, map, bar, col, row);
             };
-            const int nbox = p.d / 64;
+            constexpr int nbox = kD / 64;
             mbar_expect_tx(&bars->a_full, nbox * kBox);
             for (int ch = 0; ch < nbox; ++ch) load(sA + ch * kBox, &tmA, &bars->a_full, ch * 64, a_row, a_head);
             for (int j = 0; j < nt; ++j) {
@@ -165,10 +165,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (j >= 2) mbar_wait(&bars->s_empty[j & 1], ((j >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t tS = tbase + (j & 1) * 128;
-                const int nkk = p.d / 16;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    if (kk >= nkk) break;
+                for (int kk = 0; kk < kD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
                     umma_ss(tS, sdesc_sw128(a_addr + off, 16, 1024),
                             sdesc_sw128(b_addr + s * kTile + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
@@ -182,6 +180,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int rr = quarter * 32 + lane;                  // tile row
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         float m_run = -INFINITY, s_run = 0.f;
+        // diagonal tile: key column c is masked when c > rr + diag_off (key position past the
+        // query's); 0 except in the b = 64 budget pass, where the last block can sit in the
+        // second half of its 128-key tile (diag_off = 64)
+        const int diag_off = kB64 && p.mode == kBudget ? a_row - diag_u * 128 : 0;
         float lse_row = 0.f;
         // rows past the end (partial last tile / block): padded, excluded from every output
         const bool row_ok = (p.mode == kBudget) ? (rr < p.b && a_row + rr < p.N) : (tr * 128 + rr < p.Ns);
@@ -268,7 +270,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 // raw logits; causal mask inside the diagonal tile (key position > query
                 // position); 8 independent max chains
                 if (diag) {
-                    const int thr = (p.mode == kBudget) ? a_row + rr - u * 128 : rr;
+                    const int thr = rr + diag_off;
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -560,21 +562,22 @@ bool maxpool_pass() {
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
 
-ScoreKernel score_kernel(bool b64 = false) {
-    if (b64) return score_tc_kernel<0, true>;
+ScoreKernel score_kernel(int d, bool b64 = false) {
+    if (d == 64) return b64 ? score_tc_kernel<0, true, 64> : score_tc_kernel<0, false, 64>;
+    if (b64) return score_tc_kernel<0, true, 128>;
     const int e = score_emu();
-    return e == 0 ? score_tc_kernel<0, false> : e == 1 ? score_tc_kernel<1, false>
-         : e == 2 ? score_tc_kernel<2, false> : score_tc_kernel<3, false>;
+    return e == 0 ? score_tc_kernel<0, false, 128> : e == 1 ? score_tc_kernel<1, false, 128>
+         : e == 2 ? score_tc_kernel<2, false, 128> : score_tc_kernel<3, false, 128>;
 }
 
 bool set_smem_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(score_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kSmem)) != cudaSuccess ||
-            cudaFuncSetAttribute(score_kernel(true), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kSmem)) != cudaSuccess)
-            return false;
+        for (int d : {64, 128})
+            for (bool b64 : {false, true})
+                if (cudaFuncSetAttribute(score_kernel(d, b64), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem)) != cudaSuccess)
+                    return false;
         done = true;
     }
     return true;
@@ -634,7 +637,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.W = maxpool_pass() ? nullptr : lse2 + static_cast<size_t>(D.gl) * D.Ns;
     const unsigned grid = static_cast<unsigned>(D.gl) * (p.tr_hi - p.tr_lo) * p.n_chunks;
     p.mode = kLse;
-    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int i0 = p.tr_lo * 128, i1 = static_cast<int>(p.tr_hi * 128 < D.Ns ? p.tr_hi * 128 : D.Ns);
@@ -653,7 +656,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.mode = kMaxpool;
     p.lse2 = lse2;
     p.L = L;
-    score_kernel()<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     return cudaGetLastError();
 }
 
@@ -679,7 +682,7 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
     p.part_m = scratch;
     p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
     const unsigned grid = static_cast<unsigned>(D.Hl) * p.n_chunks;
-    score_kernel(D.b == 64)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.d, D.b == 64)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int n_comb = (D.M + kCombChunk - 1) / kCombChunk;
