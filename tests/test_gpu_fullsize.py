@@ -1,5 +1,6 @@
-"""Full-size parity on the bench configuration (128K tokens, Llama-3.1-8B attention shape,
-the same launch configuration bench.py times), checked against the oracle on SAMPLED
+"""Full-size parity on bench.py's workloads (128K Llama-3.1-8B shape = the headline, its
+b = 64 variant, the d = 64 Llama-3.2-1B shape, Qwen2.5-7B at 64K with g = 4 and the 2048-token
+minimum budget; the same launch configuration bench.py times), checked against the oracle on SAMPLED
 outputs the oracle can compute one by one: L rows, Alg. 1 budgets of sampled heads,
 selected blocks on sampled rows (margin-gated), and O on sampled (head, row)
 items with the GPU mask injected.  Plus properties that hold at any size."""
@@ -16,19 +17,28 @@ pytestmark = pytest.mark.gpu
 MARGIN = 1e-4
 
 
-@pytest.fixture(scope="module")
-def layer():
+# bench.py's workloads at full size: (Hq, Hkv, d, N, b, g, min budget, preset)
+WORKLOADS = {
+    "llama3.1-8b-attn-128k": (32, 8, 128, 131072, 128, 1, 0, "llama-128k"),
+    "llama3.1-8b-attn-128k-b64": (32, 8, 128, 131072, 64, 1, 0, "llama-128k"),
+    "llama3.2-1b-attn-128k": (32, 8, 64, 131072, 128, 1, 0, "llama1b-128k"),
+    "qwen2.5-7b-attn-64k": (28, 4, 128, 65536, 128, 4, 2048, "qwen-64k"),
+}
+
+
+@pytest.fixture(scope="module", params=list(WORKLOADS))
+def layer(request):
     dev = torch.device("cuda:0")
-    N = 131072
-    cfg = pa.Config(32, 8, 128, N, 128, 4, 1, 0.9, 0)
-    Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=workloads.PRESETS["llama-128k"],
+    Hq, Hkv, d, N, b, g, mb, preset = WORKLOADS[request.param]
+    cfg = pa.Config(Hq, Hkv, d, N, b, 4, g, 0.9, mb)
+    Q, K, V, _ = workloads.structured(Hq, Hkv, N, d, seed=0, params=workloads.PRESETS[preset],
                                       device=dev)
     kstar, budget, cnt, idx = pa.estimate(cfg, Q, K)
     O = pa.prefill(cfg, Q, K, V, cnt, idx)
     qsum, ksum = pa.pool(cfg, Q, K)
     L = pa.proxy_scores(cfg, qsum, ksum)
     torch.cuda.synchronize()
-    oc = oracle.Cfg(32, 8, 128, N, 128, 4, 1, 0.9, 0, round_bf16=True)
+    oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, g, 0.9, mb, round_bf16=True)
     host = dict(Q=Q.float().cpu().numpy(), K=K.float().cpu().numpy(), V=V.float().cpu().numpy())
     return dict(cfg=cfg, oc=oc, kstar=kstar.cpu().numpy(), budget=budget.cpu().numpy(),
                 cnt=cnt.cpu().numpy(), idx=idx, O=O, L=L.cpu().numpy(), **host)
@@ -41,18 +51,20 @@ def test_fullsize_properties(layer):
     np.testing.assert_allclose(layer["budget"], ks / M, rtol=1e-6)
     # A5 closed form (Z12) on every (head, row)
     m = np.arange(M)[None, :]
-    K = np.minimum(m + 1, np.maximum((ks[:, None].astype(np.int64) * (m + 1) + M - 1) // M, 1))
+    F = -(-cfg.min_budget_tokens // cfg.block_size)
+    K = np.minimum(m + 1, np.maximum(np.maximum((ks[:, None].astype(np.int64) * (m + 1) + M - 1) // M, F), 1))
     assert np.array_equal(cnt, K)
-    # lists: ascending, causal, diagonal last, nested across heads of the group by budget
+    # lists: ascending, causal, diagonal last
     idx = layer["idx"]
-    for h in (0, 7, 19, 31):
+    H = cfg.n_q_heads
+    for h in (0, 7, 19, H - 1):
         for mm in (0, 1, M // 3, M - 1):
             lst = idx[h, mm, :cnt[h, mm]].cpu().numpy()
             assert lst[-1] == mm and np.all(np.diff(lst) > 0) and lst[0] >= 0
-    L = layer["L"][0]
-    assert np.all(np.isneginf(L[np.triu_indices(M, 1)]))
-    assert np.all(np.isfinite(L[np.tril_indices(M)]))
-    assert np.all(L[np.tril_indices(M)] <= 1e-6)            # log-probabilities
+    for L in layer["L"]:                                     # every proxy group
+        assert np.all(np.isneginf(L[np.triu_indices(M, 1)]))
+        assert np.all(np.isfinite(L[np.tril_indices(M)]))
+        assert np.all(L[np.tril_indices(M)] <= 1e-6)        # log-probabilities
     assert torch.isfinite(layer["O"]).all()
 
 
@@ -62,12 +74,15 @@ def test_fullsize_sampled_parity(layer):
     rows = [0, 1, M // 4, M // 2, 3 * M // 4, M - 1]
     Pq, Pk, scale = oracle.pool(oc, layer["Q"], layer["K"])
     _, Lref = oracle.proxy_scores(oc, Pq, Pk, scale, rows=rows)
-    for m in rows:
-        ref = Lref[0, m, :m + 1]
-        got = layer["L"][0, m, :m + 1].astype(np.float64)
-        assert np.max(np.abs(got - ref)) <= 1e-4, m
+    G = cfg.n_groups
+    for c in range(G):
+        for m in rows:
+            ref = Lref[c, m, :m + 1]
+            got = layer["L"][c, m, :m + 1].astype(np.float64)
+            assert np.max(np.abs(got - ref)) <= 1e-4, (c, m)
     # budgets of sampled heads (margin-gated)
-    heads = [0, 5, 17, 30]
+    H, b = cfg.n_q_heads, cfg.block_size
+    heads = [0, 5, 17, H - 2]
     ks_ref, _, bmg, _ = oracle.budgets(oc, layer["Q"], layer["K"], heads=heads)
     for h in heads:
         if bmg[h] > MARGIN:
@@ -75,8 +90,8 @@ def test_fullsize_sampled_parity(layer):
         else:
             assert abs(int(layer["kstar"][h]) - int(ks_ref[h])) <= 1
     # selection on sampled rows from the oracle's L with the GPU budgets injected
-    Lfull = np.full((1, M, M), -np.inf)
-    Lfull[0, rows] = Lref[0, rows]
+    Lfull = np.full((G, M, M), -np.inf)
+    Lfull[:, rows] = Lref[:, rows]
     ocnt, oidx, cmg = oracle.select(oc, Lfull, layer["kstar"], rows=rows)
     checked = 0
     idx = layer["idx"]
@@ -89,7 +104,7 @@ def test_fullsize_sampled_parity(layer):
                 checked += 1
     assert checked >= 0.9 * cfg.n_q_heads * len(rows)
     # O on sampled (head, row) items with the GPU mask injected
-    items = [(0, M - 1), (17, M - 1), (5, M // 2), (30, 1), (11, 0), (24, 3 * M // 4)]
+    items = [(0, M - 1), (17, M - 1), (5, M // 2), (H - 2, 1), (11, 0), (24, 3 * M // 4), (H - 1, M - 2)]
     cnt_h = layer["cnt"]
     idx_h = np.zeros((cfg.n_q_heads, M, M), np.int32)
     for h, m in items:
@@ -98,8 +113,8 @@ def test_fullsize_sampled_parity(layer):
                             items=np.array(items, np.int32).reshape(-1))
     O = layer["O"]
     for h, m in items:
-        got = O[h, m * 128:(m + 1) * 128].float().cpu().numpy()
-        err = np.abs(got - Oref[h, m * 128:(m + 1) * 128])
+        got = O[h, m * b:(m + 1) * b].float().cpu().numpy()
+        err = np.abs(got - Oref[h, m * b:(m + 1) * b])
         assert err.max() <= 2e-2 and err.mean() <= 2e-3, (h, m, err.max(), err.mean())
 
 
@@ -114,7 +129,8 @@ def test_fullsize_dense_sampled(layer):
     items = [(3, M - 1), (20, M // 3)]
     Oref = oracle.dense(oc, layer["Q"], layer["K"], layer["V"],
                         items=np.array(items, np.int32).reshape(-1))
+    b = cfg.block_size
     for h, m in items:
-        got = Od[h, m * 128:(m + 1) * 128].float().cpu().numpy()
-        err = np.abs(got - Oref[h, m * 128:(m + 1) * 128])
+        got = Od[h, m * b:(m + 1) * b].float().cpu().numpy()
+        err = np.abs(got - Oref[h, m * b:(m + 1) * b])
         assert err.max() <= 2e-2 and err.mean() <= 2e-3, (h, m, err.max(), err.mean())
