@@ -45,8 +45,10 @@ extern "C" {
  * 0 < gamma <= 1, min_budget_tokens >= 0.  N need not be a multiple of b: M = ceil(N/b)
  * blocks, the last one zero-padded with its padded keys masked and no output for padded
  * rows; sampled positions are i*s < N, N/s rounded up.
- * bf16 build supports d == 128, b == 128; FP32_DEBUG supports d % 32 == 0, d <= 128,
- * any b with b % s == 0 (SIMT kernels, for the 1e-4 parity contract). */
+ * bf16 build supports d in {64, 128} and b in {64, 128} (tcgen05 kernels; the estimation's
+ * tensor-core passes also need b/s in {16, 32, 64, 128}, else SIMT kernels run them);
+ * FP32_DEBUG supports d % 32 == 0, d <= 128, any b with b % s == 0 (SIMT kernels, for the
+ * 1e-4 parity contract). */
 typedef struct {
     int32_t  n_q_heads;          /* Hq (global) */
     int32_t  n_kv_heads;         /* Hkv (global) */
@@ -123,7 +125,9 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K,
  * Q[h][t]·K[kv(h)][k]/sqrt(d), times V.  Accepts ANY valid lists (non-empty, ascending,
  * in range, n <= m), so oracle masks can be injected.  With PROXYATTN_FLAG_CHECK the
  * lists are validated on the device first and E_SHAPE is returned on a violation
- * (this flag synchronises the stream). */
+ * (this flag synchronises the stream).  b = 64 works on row PAIRS (2q, 2q+1) of a head: a
+ * [row_begin, row_end) range aligned to even rows gives outputs bit-identical to the full
+ * launch; an unaligned one splits a pair (results within the bf16 tolerance, not bitwise). */
 int proxyattn_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
                       const int32_t* block_cnt, const int32_t* block_idx, void* O,
                       void* stream);
