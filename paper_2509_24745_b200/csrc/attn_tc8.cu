@@ -826,25 +826,29 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d))
         return cudaErrorInvalidValue;
     static int emu = -1;
-    if (emu < 0) {   // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe (d = b = 128)
+    // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe (d = b = 128).  Default 0:
+    // under the power cap all-MUFU measured best (128K prefill 18.84-18.94 ms vs 18.85-19.06 at
+    // 1/8 and 19.18-19.28 at 2/8, three alternating runs; 2/8 was best before the barrier fix)
+    if (emu < 0) {
         const char* e = getenv("PROXYATTN_EXP_EMU");
-        emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
+        emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 0;
     }
     AttnKernel kern = nullptr;
     if (D.d == 128 && D.b == 128) {
         kern = emu == 0 ? kernel_with_attr<128, 128, 0>() : emu == 1 ? kernel_with_attr<128, 128, 1>()
              : emu == 2 ? kernel_with_attr<128, 128, 2>() : emu == 3 ? kernel_with_attr<128, 128, 3>()
                                                           : kernel_with_attr<128, 128, 4>();
-    } else if (D.d == 128) {
-        kern = kernel_with_attr<128, 64, 2>();
+    } else if (D.d == 128) {   // b = 64: 0 or 2 (PROXYATTN_EXP_EMU)
+        kern = emu == 2 ? kernel_with_attr<128, 64, 2>() : kernel_with_attr<128, 64, 0>();
     } else if (D.b == 128) {   // d = 64 (exp-bound: half the tensor work per exp2)
         static int emu64 = -1;   // PROXYATTN_EXP_EMU64=2..4; 2/8 measured best at 128K
         if (emu64 < 0) {         // (13.2-13.3 ms vs 13.4-13.6 at 3/8 and 13.8 at 4/8)
             const char* e = getenv("PROXYATTN_EXP_EMU64");
-            emu64 = (e && e[0] >= '2' && e[0] <= '4') ? e[0] - '0' : 2;
+            emu64 = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
         }
-        kern = emu64 == 2 ? kernel_with_attr<64, 128, 2>() : emu64 == 3 ? kernel_with_attr<64, 128, 3>()
-                                                                           : kernel_with_attr<64, 128, 4>();
+        kern = emu64 == 0 ? kernel_with_attr<64, 128, 0>() : emu64 == 1 ? kernel_with_attr<64, 128, 1>()
+             : emu64 == 2 ? kernel_with_attr<64, 128, 2>() : emu64 == 3 ? kernel_with_attr<64, 128, 3>()
+                                                                         : kernel_with_attr<64, 128, 4>();
     } else {
         kern = kernel_with_attr<64, 64, 2>();
     }
