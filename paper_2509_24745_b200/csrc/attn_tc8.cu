@@ -54,8 +54,14 @@ namespace {
 constexpr int kTileRows = 128;
 constexpr int kBox = kTileRows * 64 * 2;   // 16 KB: [128 rows][64 bf16] SW128 box
 constexpr float kUnderflow = -60.0f;       // log2 floor of a row sum under a non-attained reference
-constexpr int kKStages = 3;
-constexpr int kVStages = 2;
+#ifndef PA_KSTAGES
+#define PA_KSTAGES 3
+#endif
+#ifndef PA_VSTAGES
+#define PA_VSTAGES 2
+#endif
+constexpr int kKStages = PA_KSTAGES;   // K ring (3) and V ring (2) stages of 32 KB tiles
+constexpr int kVStages = PA_VSTAGES;
 constexpr int kItemSlots = 4;
 constexpr int kThreads = 512;
 constexpr float kOverflow = 32.0f;         // log2 headroom of P over the fast reference
