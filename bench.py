@@ -577,6 +577,7 @@ def run_ours(args):
         # estimate: 9 kernels (4 of them Alg. 1); a row-range estimate adds 5 per extra range
         "gpu_launches": (ESTIMATE_KERNELS + 5 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
                          + len(my_rows) * ((2 if kname == "attn_tc8_kernel" else 1)
+                                           + (1 if kname == "attn_tc8_kernel" and cfg.Hl // cfg.r > 1 else 0)  # kv order
                                            + (1 if b == 64 else 0))) * args.steps,   # + pair union
         "clocks": clocks,
         # the paper's own numbers, other hardware and workloads: context only
