@@ -67,8 +67,10 @@ struct ScoreParams {
     float* part_s;
     const float* lse2;  // MAXPOOL: [gl][Ns] (log2 units)
     float* L;           // MAXPOOL: [gl][M][M] (natural log)
-    float* W;           // LSE (optional): [gl][Ns][M] raw-logit max of each row over the
-                        // bs sampled keys of block n (causal mask applied)
+    float* W;           // LSE (optional): [gl][n_tr][Ns][nwin] raw-logit max of each row over
+                        // the bs sampled keys of block n = u * nwin + w of key tile u (causal
+                        // mask applied); tile-major so a warp's store of its 32 rows' windows
+                        // is one contiguous 32 * nwin * 4-byte segment
 };
 
 // kEmu: of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4); kB64: budget pass
@@ -331,18 +333,25 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     // maxima of A3 are folds of it; the max-pool itself runs afterwards
                     // from W and lse (maxpool_from_windows_kernel), bit-identical to kMaxpool
                     const int nwin = 128 / p.bs;
-                    float* wrow = p.W + (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.M;
+                    float* wrow = p.W + ((static_cast<long long>(prob) * p.n_tr + u) * p.Ns + tr * 128 + rr) * nwin;
+                    float win[8];
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        if (c >= nwin) break;
-                        const float w = p.bs == 16 ? mx[c]
-                                      : p.bs == 32 ? fmaxf(mx[(2 * c) & 7], mx[(2 * c + 1) & 7])
-                                      : p.bs == 64 ? fmaxf(fmaxf(mx[(4 * c) & 7], mx[(4 * c + 1) & 7]),
-                                                           fmaxf(mx[(4 * c + 2) & 7], mx[(4 * c + 3) & 7]))
-                                                   : fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-                        const int n = u * nwin + c;
-                        if (n < p.M) wrow[n] = w;
+                    for (int c = 0; c < 8; ++c)
+                        win[c] = p.bs == 16 ? mx[c]
+                               : p.bs == 32 ? fmaxf(mx[(2 * c) & 7], mx[(2 * c + 1) & 7])
+                               : p.bs == 64 ? fmaxf(fmaxf(mx[(4 * c) & 7], mx[(4 * c + 1) & 7]),
+                                                    fmaxf(mx[(4 * c + 2) & 7], mx[(4 * c + 3) & 7]))
+                                            : fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                                    fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                    if (nwin == 8) {
+                        reinterpret_cast<float4*>(wrow)[0] = make_float4(win[0], win[1], win[2], win[3]);
+                        reinterpret_cast<float4*>(wrow)[1] = make_float4(win[4], win[5], win[6], win[7]);
+                    } else if (nwin == 4) {
+                        *reinterpret_cast<float4*>(wrow) = make_float4(win[0], win[1], win[2], win[3]);
+                    } else if (nwin == 2) {
+                        *reinterpret_cast<float2*>(wrow) = make_float2(win[0], win[1]);
+                    } else {
+                        *wrow = win[0];
                     }
                 }
                 const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
@@ -422,27 +431,53 @@ __global__ void lse_combine_kernel(int rows, int chunk, int Ns, int n_chunks, co
 // A3 from the window maxima of the lse pass: L[c][m][n] = ln2 * max over the block's valid
 // sampled rows i of (W[c][i][n] * sc2 - lse2[c][i]) for n <= m, -inf above the diagonal.
 // The operations of kMaxpool (window max of raw logits, scale, subtract lse, max over rows,
-// ln2) without its second GEMM pass; one CTA per (group, block row).
-__global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, float sc2,
+// ln2) without its second GEMM pass.  One CTA per (group, block row); a warp per key tile u
+// reads the block's rows' window vectors of that tile (contiguous in W's tile-major layout),
+// lanes over rows, then a max over lanes per window.
+__global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, int n_tr, float sc2,
                                                                    const float* __restrict__ W,
                                                                    const float* __restrict__ lse2,
                                                                    float* __restrict__ L, int rb, int re) {
-    __shared__ float lse_s[128];
     const int m = rb + blockIdx.x % (re - rb), c = blockIdx.x / (re - rb);   // block rows [rb, re)
     const int i0 = m * bs, i1 = min(i0 + bs, Ns);
-    for (int i = threadIdx.x; i < i1 - i0; i += blockDim.x)
-        lse_s[i] = lse2[static_cast<long long>(c) * Ns + i0 + i];
-    __syncthreads();
+    const int nwin = 128 / bs;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     float* Lrow = L + (static_cast<long long>(c) * M + m) * M;
-    const float* Wc = W + static_cast<long long>(c) * Ns * M;
-    for (int n = threadIdx.x; n < M; n += blockDim.x) {
-        float w = -INFINITY;
-        if (n <= m) {
-            for (int i = i0; i < i1; ++i)
-                w = fmaxf(w, fmaf(__ldg(Wc + static_cast<long long>(i) * M + n), sc2, -lse_s[i - i0]));
-            w *= kLn2;
+    for (int n = m + 1 + threadIdx.x; n < M; n += blockDim.x) Lrow[n] = -INFINITY;
+    const int u_max = m / nwin;                       // tiles holding blocks n <= m
+    for (int u = warp; u <= u_max; u += nwarps) {
+        const float* Wu = W + ((static_cast<long long>(c) * n_tr + u) * Ns) * nwin;
+        float best[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) best[w] = -INFINITY;
+        for (int i = i0 + lane; i < i1; i += 32) {
+            const float nl = -__ldg(lse2 + static_cast<long long>(c) * Ns + i);
+            const float* wi = Wu + static_cast<long long>(i) * nwin;
+            float v[8];
+            if (nwin == 8) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(wi));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(wi) + 1);
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            } else if (nwin == 4) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(wi));
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            } else if (nwin == 2) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(wi));
+                v[0] = a.x; v[1] = a.y;
+            } else {
+                v[0] = __ldg(wi);
+            }
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+                if (w < nwin) best[w] = fmaxf(best[w], fmaf(v[w], sc2, nl));
         }
-        Lrow[n] = w;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            if (w >= nwin) break;
+            const float x = warp_max(best[w]);
+            const int n = u * nwin + w;
+            if (lane == 0 && n <= m) Lrow[n] = x * kLn2;
+        }
     }
 }
 
@@ -594,8 +629,9 @@ size_t score_tc_scratch_bytes(const Dims& D) {
     const int n_tr = static_cast<int>((D.Ns + 127) / 128);
     const int n_chunks = (n_tr + kChunk - 1) / kChunk;
     // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]
-    return 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 +
-           static_cast<size_t>(D.gl) * D.Ns * D.M * 4;
+    const size_t nwin = 128 / (D.bs > 0 ? D.bs : 1);
+    return 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 + 32 +
+           static_cast<size_t>(D.gl) * n_tr * D.Ns * nwin * 4;   // W [gl][n_tr][Ns][nwin], aligned
 }
 
 size_t score_tc_budget_scratch_bytes(const Dims& D) {
@@ -634,7 +670,9 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     float* lse2 = part_s + static_cast<size_t>(D.gl) * D.Ns * p.n_chunks;
     p.part_m = part_m;
     p.part_s = part_s;
-    p.W = maxpool_pass() ? nullptr : lse2 + static_cast<size_t>(D.gl) * D.Ns;
+    // W: 32-byte aligned (its rows are stored as float4 / float2 vectors)
+    const uintptr_t w_addr = reinterpret_cast<uintptr_t>(lse2 + static_cast<size_t>(D.gl) * D.Ns);
+    p.W = maxpool_pass() ? nullptr : reinterpret_cast<float*>((w_addr + 31) & ~static_cast<uintptr_t>(31));
     const unsigned grid = static_cast<unsigned>(D.gl) * (p.tr_hi - p.tr_lo) * p.n_chunks;
     p.mode = kLse;
     score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
@@ -647,7 +685,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (!maxpool_pass()) {
         maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
-            D.M, p.Ns, p.bs, p.sc2, p.W, lse2, L, D.rb, D.re);
+            D.M, p.Ns, p.bs, p.n_tr, p.sc2, p.W, lse2, L, D.rb, D.re);
         return cudaGetLastError();
     }
     const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
