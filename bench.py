@@ -497,6 +497,45 @@ def run_ours(args):
         e2e = {"value": float(np.mean(ts)), "unit": "ms", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
         del dws
+    elif ws > 1 and not args.no_e2e and w["n_kv_heads"] % ws == 0:
+        # N > 1: each rank runs its KV-aligned head shard from pinned host buffers (only its
+        # heads cross PCIe; the pooled sums are all-reduced when a proxy group spans ranks),
+        # wall-clock between barriers, max over ranks
+        import torch.distributed as dist
+
+        hcfg = build_config(pa, rank, ws, w, "heads")
+        hb2, he2 = hcfg.local_heads
+        Qh = Q[hb2:he2].cpu().pin_memory()
+        Kh = K[hb2 // r:he2 // r].cpu().pin_memory()
+        Vh = V[hb2 // r:he2 // r].cpu().pin_memory()
+        Oh = torch.empty_like(Qh).pin_memory()
+        del wsp
+        torch.cuda.empty_cache()
+        hws = pa.alloc_workspace(hcfg, dev)
+
+        def ar(t):
+            if same_dev:            # gloo-only test mode: through host memory
+                c = t.cpu()
+                dist.all_reduce(c)
+                t.copy_(c)
+            else:
+                dist.all_reduce(t)
+
+        shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=ar)
+        ts = []
+        for _ in range(max(2, args.steps // 2)):
+            barrier()
+            t0 = time.perf_counter()
+            shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=ar)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        tv = torch.tensor([float(np.mean(ts))], dtype=torch.float64)
+        dist.all_reduce(tv, op=dist.ReduceOp.MAX, group=cpu_group)
+        h2d = (Qh.numel() + Kh.numel() + Vh.numel()) * 2 * ws
+        d2h = Oh.numel() * 2 * ws
+        e2e = {"value": float(tv.item()), "unit": "ms", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "path": "KV-head-group shards from pinned host buffers (all ranks' bytes), max over ranks"}
+        del hws
 
     if rank != 0:
         if ws > 1:

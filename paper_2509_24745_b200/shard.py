@@ -95,6 +95,25 @@ def estimate_sharded(cfg, Q_local, K_local, world: int, workspace=None, ops: Opt
     return kstar, budget, cnt, idx
 
 
+def forward_host_sharded(cfg_local, Qh, Kh, Vh, Oh, world: int, workspace=None, all_reduce=None):
+    """One ProxyAttn layer for this rank's KV-aligned head shard, end to end from pinned HOST
+    buffers (the e2e leg at N > 1): H2D of its query heads and their KV heads, A1-A6 with the
+    pooled sums all-reduced when a proxy group spans ranks, A7 on the local
+    heads, D2H of O into Oh.  Synchronises the current stream; returns the local K* (host)."""
+    from . import _lib
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Q = Qh.to(dev, non_blocking=True)
+    K = Kh.to(dev, non_blocking=True)
+    V = Vh.to(dev, non_blocking=True)
+    kstar, _, cnt, idx = estimate_sharded(cfg_local, Q, K, world, workspace, all_reduce=all_reduce)
+    O = _lib.prefill(cfg_local, Q, K, V, cnt, idx)
+    Oh.copy_(O, non_blocking=True)
+    ks = kstar.to("cpu", non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return ks
+
+
 def gather_heads(t_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """all_gather of a head-major local tensor into the full head dimension (verification)."""
     import torch.distributed as dist
