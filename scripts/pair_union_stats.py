@@ -11,8 +11,9 @@ import paper_2509_24745_b200 as pa
 import workloads
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 dev = torch.device("cuda:0")
-cfg = pa.Config(32, 8, 128, N, 64, 4, 1, 0.9, 0)
+cfg = pa.Config(32, 8, 128, N, b, 4, 1, 0.9, 0)
 Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=workloads.PRESETS["llama-128k"], device=dev)
 _, _, cnt, idx = pa.estimate(cfg, Q, K)
 M, H, r = cfg.M, 32, 4
@@ -35,5 +36,5 @@ for kv in range(8):
 # (b) adjacent rows of one head
 mb = mask[:, 0::2] | mask[:, 1::2] if M % 2 == 0 else None
 ub = float(mb.sum())
-print(json.dumps({"N": N, "M": M, "sum_cnt": tot, "head_pairs_by_count": ua / (tot / 2),
+print(json.dumps({"N": N, "b": b, "M": M, "sum_cnt": tot, "head_pairs_by_count": ua / (tot / 2),
                   "adjacent_rows": ub / (tot / 2)}))
