@@ -689,9 +689,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 }
 
 // kB = 64: union size of each row pair's two lists, |A| + |B| - |A n B| (a warp per work
-// unit; the elements of A are searched in the ascending B).  Same item order as the kernel.
+// unit; B marked in a per-warp bitmap and A tested, or A's elements binary-searched in the
+// ascending B when the bitmap does not fit).  Same item order as the kernel.
 __global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* __restrict__ block_idx,
-                                  int M, int r, int row_lo, int row_hi, int n_items, int* __restrict__ ucnt) {
+                                  int M, int r, int row_lo, int row_hi, int n_items, int* __restrict__ ucnt,
+                                  int use_bitmap) {
     const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (item >= n_items) return;
@@ -704,7 +706,28 @@ __global__ void pair_union_kernel(const int* __restrict__ block_cnt, const int* 
     const int ca = mA < 0 ? 0 : __ldg(block_cnt + static_cast<long long>(hl) * M + mA);
     const int cb = mB < 0 ? 0 : __ldg(block_cnt + static_cast<long long>(hl) * M + mB);
     int inter = 0;
-    if (ca > 0 && cb > 0) {
+    extern __shared__ unsigned pair_bits[];           // a (M+31)/32-word bitmap per warp, or none
+    const int words = (M + 31) >> 5;
+    if (ca > 0 && cb > 0 && use_bitmap) {
+        // |A n B| by marking B's columns in a bitmap and testing A's: coalesced, independent loads
+        const int* A = block_idx + (static_cast<long long>(hl) * M + mA) * M;
+        const int* B = block_idx + (static_cast<long long>(hl) * M + mB) * M;
+        unsigned* bm = pair_bits + (threadIdx.x >> 5) * words;
+        const int nw = (mB >> 5) + 1;                  // B's columns are <= mB
+        for (int w = lane; w < nw; w += 32) bm[w] = 0u;
+        __syncwarp();
+        for (int i = lane; i < cb; i += 32) {
+            const int v = __ldg(B + i);
+            atomicOr(bm + (v >> 5), 1u << (v & 31));
+        }
+        __syncwarp();
+        for (int i = lane; i < ca; i += 32) {
+            const int v = __ldg(A + i);
+            inter += (bm[v >> 5] >> (v & 31)) & 1u;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    } else if (ca > 0 && cb > 0) {
         const int* A = block_idx + (static_cast<long long>(hl) * M + mA) * M;
         const int* B = block_idx + (static_cast<long long>(hl) * M + mB) * M;
         for (int i = lane; i < ca; i += 32) {
@@ -871,8 +894,12 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);
     if (e != cudaSuccess) return e;
     if (pair && block_cnt) {
-        pair_union_kernel<<<static_cast<unsigned>((n_items * 32 + 255) / 256), 256, 0, st>>>(
-            block_cnt, block_idx, D.M, D.r, D.rb, D.re, static_cast<int>(n_items), sb->ucnt);
+        // bitmap intersection while 8 warps' bitmaps fit in 16 KB (M <= 16384), else binary search
+        const int words = (D.M + 31) / 32;
+        const bool bitmap = words * 8 * 4 <= 16384;
+        pair_union_kernel<<<static_cast<unsigned>((n_items * 32 + 255) / 256), 256,
+                            bitmap ? static_cast<size_t>(words) * 8 * 4 : 0, st>>>(
+            block_cnt, block_idx, D.M, D.r, D.rb, D.re, static_cast<int>(n_items), sb->ucnt, bitmap ? 1 : 0);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // KV heads in decreasing work (sparse launches with more than one local KV head, <= 64)
