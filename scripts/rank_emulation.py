@@ -4,7 +4,7 @@ chunks, the row-range attention; the K* all-gather replaced by a device copy of 
 replicated K*).  A projection of the per-GPU time at P GPUs (each GPU alone on its share,
 same clocks), not a multi-GPU measurement.
 
-    python scripts/rank_emulation.py [P] [N] [--graph]"""
+    python scripts/rank_emulation.py [P] [N] [--graph] [--qwen]"""
 import json
 import sys
 
@@ -16,16 +16,18 @@ import workloads
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
+qwen = "--qwen" in sys.argv      # Qwen2.5-7B shape (28/4 heads, g = 4, min budget 2048), 64K preset
 dev = torch.device("cuda:0")
-cfg = pa.Config(32, 8, 128, N, 128, 4, 1, 0.9, 0)
-Q, K, V, _ = workloads.structured(32, 8, N, 128, seed=0, params=workloads.PRESETS["llama-128k"], device=dev)
+Hq, Hkv, g, mb, preset = (28, 4, 4, 2048, "qwen-64k") if qwen else (32, 8, 1, 0, "llama-128k")
+cfg = pa.Config(Hq, Hkv, 128, N, 128, 4, g, 0.9, mb)
+Q, K, V, _ = workloads.structured(Hq, Hkv, N, 128, seed=0, params=workloads.PRESETS[preset], device=dev)
 M = cfg.M
 wsp = pa.alloc_workspace(cfg, dev)
 kfull, _ = pa.budgets(cfg, Q, K, wsp)
-kstar = torch.empty(32, dtype=torch.int32, device=dev)
-budget = torch.empty(32, dtype=torch.float32, device=dev)
-cnt = torch.zeros(32, M, dtype=torch.int32, device=dev)
-idx = torch.empty(32, M, M, dtype=torch.int32, device=dev)
+kstar = torch.empty(Hq, dtype=torch.int32, device=dev)
+budget = torch.empty(Hq, dtype=torch.float32, device=dev)
+cnt = torch.zeros(Hq, M, dtype=torch.int32, device=dev)
+idx = torch.empty(Hq, M, M, dtype=torch.int32, device=dev)
 O = torch.empty_like(Q)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -99,6 +101,6 @@ for pas in range(2):
         if pas == 0 or est + att < out[r]["step_ms"]:
             out[r].update(estimate_ms=round(est, 4), attention_ms=round(att, 4), step_ms=round(est + att, 4))
 worst = max(o["step_ms"] for o in out)
-print(json.dumps({"P": P, "N": N, "single_gpu_step_ms": round(full_est + full_att, 4),
+print(json.dumps({"P": P, "N": N, "workload": "qwen2.5-7b" if qwen else "llama3.1-8b", "single_gpu_step_ms": round(full_est + full_att, 4),
                   "max_rank_step_ms": worst, "projected_speedup": round((full_est + full_att) / worst, 2),
                   "ranks": out}))
