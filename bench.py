@@ -64,9 +64,11 @@ WORKLOADS = {
                                   preset="llama1b-128k"),
 }
 L2_FLUSH_BYTES = 256 << 20
-# kernels per step: estimate = pool, proxy lse, lse combine, -inf fill, proxy max-pool, budget
-# partials, budget combine, budget finalize, select (9); + one attention launch per row range
-ESTIMATE_KERNELS = 9
+# kernels per step: estimate = pool, proxy lse pass, max-pool (+ lse combine), budget pass,
+# budget partials, budget masses, budget finalize, select (8); a row-range estimate with K*
+# given = pool, lse pass, max-pool, select (4 per extra range); prefill = KV order + the fast
+# and exact attention launches (+ the pair union at b = 64)
+ESTIMATE_KERNELS = 8
 
 
 def peaks() -> dict:
@@ -613,8 +615,8 @@ def run_ours(args):
         "e2e": e2e,
         # attn_tc8 is two launches per prefill call: the fast pass and the exact re-run of
         # the rows it flagged (an empty list at these inputs)
-        # estimate: 9 kernels (4 of them Alg. 1); a row-range estimate adds 5 per extra range
-        "gpu_launches": (ESTIMATE_KERNELS + 5 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
+        # estimate: 8 kernels (4 of them Alg. 1); a row-range estimate adds 4 per extra range
+        "gpu_launches": (ESTIMATE_KERNELS + 4 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
                          + len(my_rows) * ((2 if kname == "attn_tc8_kernel" else 1)
                                            + (1 if kname == "attn_tc8_kernel" and cfg.Hl // cfg.r > 1 else 0)  # kv order
                                            + (1 if b == 64 else 0))) * args.steps,   # + pair union

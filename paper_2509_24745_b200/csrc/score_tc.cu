@@ -434,12 +434,32 @@ __global__ void lse_combine_kernel(int rows, int chunk, int Ns, int n_chunks, co
 // ln2) without its second GEMM pass.  One CTA per (group, block row); a warp per key tile u
 // reads the block's rows' window vectors of that tile (contiguous in W's tile-major layout),
 // lanes over rows, then a max over lanes per window.
+// The block's row lse (A2's normaliser) is combined here from the lse pass's per-chunk (max,
+// sum) partials (fixed chunk order), so no separate combine launch sits on the critical path.
 __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, int n_tr, float sc2,
                                                                    const float* __restrict__ W,
-                                                                   const float* __restrict__ lse2,
+                                                                   const float* __restrict__ part_m,
+                                                                   const float* __restrict__ part_s,
+                                                                   int chunk, int n_chunks,
+                                                                   float* __restrict__ lse_nat,
                                                                    float* __restrict__ L, int rb, int re) {
+    __shared__ float lse_s[128];
     const int m = rb + blockIdx.x % (re - rb), c = blockIdx.x / (re - rb);   // block rows [rb, re)
     const int i0 = m * bs, i1 = min(i0 + bs, Ns);
+    if (threadIdx.x < i1 - i0) {                       // lse2 of the block's rows (lse_combine's formula)
+        const long long i = static_cast<long long>(c) * Ns + i0 + threadIdx.x;
+        const int nk = ((i0 + static_cast<int>(threadIdx.x)) / 128 + chunk) / chunk;
+        const float* pm = part_m + i * n_chunks;
+        const float* ps = part_s + i * n_chunks;
+        float mx = -INFINITY;
+        for (int k = 0; k < nk; ++k) mx = fmaxf(mx, pm[k]);
+        float sum = 0.f;
+        for (int k = 0; k < nk; ++k) sum += ps[k] * ex2(pm[k] - mx);
+        const float l2 = mx + __log2f(sum);
+        lse_s[threadIdx.x] = l2;
+        if (lse_nat) lse_nat[i] = l2 * kLn2;
+    }
+    __syncthreads();
     const int nwin = 128 / bs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     float* Lrow = L + (static_cast<long long>(c) * M + m) * M;
@@ -451,7 +471,7 @@ __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns
 #pragma unroll
         for (int w = 0; w < 8; ++w) best[w] = -INFINITY;
         for (int i = i0 + lane; i < i1; i += 32) {
-            const float nl = -__ldg(lse2 + static_cast<long long>(c) * Ns + i);
+            const float nl = -lse_s[i - i0];
             const float* wi = Wu + static_cast<long long>(i) * nwin;
             float v[8];
             if (nwin == 8) {
@@ -678,16 +698,16 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (!maxpool_pass()) {   // lse combine fused into the max-pool (rows of the block rows)
+        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
+            D.M, p.Ns, p.bs, p.n_tr, p.sc2, p.W, part_m, part_s, p.chunk, p.n_chunks, lse_nat, L, D.rb, D.re);
+        return cudaGetLastError();
+    }
     const int i0 = p.tr_lo * 128, i1 = static_cast<int>(p.tr_hi * 128 < D.Ns ? p.tr_hi * 128 : D.Ns);
     const long long rws = static_cast<long long>(D.gl) * (i1 - i0);
     lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
         static_cast<int>(rws), p.chunk, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat, i0, i1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (!maxpool_pass()) {
-        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
-            D.M, p.Ns, p.bs, p.n_tr, p.sc2, p.W, lse2, L, D.rb, D.re);
-        return cudaGetLastError();
-    }
     const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
     fill_neg_inf_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(L, cells);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
