@@ -358,17 +358,41 @@ def run_ours(args):
 
     alg1_sharded = sharding == "rows" and ws > 1 and args.alg1 == "sharded"
 
+    # Alg. 1 has its own workspace: it runs concurrently with the chunks' score passes
+    alg1_ws = pa.alloc_workspace(cfg, dev) if alg1_sharded else None
+
     def alg1():                      # head-sharded Alg. 1 + all-gather of K* (eager: a collective)
-        shard.budgets_sharded(cfg, Ql, Kl, ws, rank, wsp, all_gather=gather_kstar, out=(kstar, budget))
+        shard.budgets_sharded(cfg, Ql, Kl, ws, rank, alg1_ws, all_gather=gather_kstar, out=(kstar, budget))
 
     # the rank's two row chunks are estimated concurrently (own workspace and stream each)
     est_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if alg1_sharded else None
     est_ws = [wsp, pa.alloc_workspace(cfg, dev)] if alg1_sharded else None
 
+    def scores():                    # alg1_sharded: the chunks' A1-A3, K* not needed yet
+        shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True,
+                            streams=est_streams, workspaces=est_ws, scores_only=True)
+
+    def select_lists():              # alg1_sharded: A5-A6 of the chunks once K* is gathered
+        shard.select_rows(cfg, my_rows, est_ws, kstar, (cnt, idx))
+
+    aux_st = torch.cuda.Stream(dev) if alg1_sharded else None
+
+    def estimate_overlapped(run_scores, run_select):
+        # the chunks' score passes on a side stream while this stream runs the head-sharded
+        # Alg. 1 and the K* all-gather; selection after both
+        cur = torch.cuda.current_stream(dev)
+        aux_st.wait_stream(cur)
+        with torch.cuda.stream(aux_st):
+            run_scores()
+        alg1()
+        cur.wait_stream(aux_st)
+        run_select()
+
     def estimate():
-        if sharding == "rows" and ws > 1:   # lists of this rank's rows only
-            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx),
-                                kstar_given=alg1_sharded, streams=est_streams, workspaces=est_ws)
+        if alg1_sharded:
+            estimate_overlapped(scores, select_lists)
+        elif sharding == "rows" and ws > 1:   # lists of this rank's rows only
+            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx))
         elif sharding == "rows":
             pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
         else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums
@@ -400,18 +424,25 @@ def run_ours(args):
     with torch.cuda.stream(st):
         for _ in range(args.warmup):
             flush.zero_()
-            if alg1_sharded:
-                alg1()
             estimate()
             prefill()
         barrier()
         if use_graph:
             g_est, g_pre = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_est, stream=st):
-                estimate()
+            if alg1_sharded:         # two graphs around the eager collective
+                g_sel = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_est, stream=st):
+                    scores()
+                with torch.cuda.graph(g_sel, stream=st):
+                    select_lists()
+            else:
+                with torch.cuda.graph(g_est, stream=st):
+                    estimate()
             with torch.cuda.graph(g_pre, stream=st):
                 prefill()
             run_est, run_pre = g_est.replay, g_pre.replay
+            if alg1_sharded:
+                run_est = lambda: estimate_overlapped(g_est.replay, g_sel.replay)  # noqa: E731
             run_est()
             run_pre()
             barrier()
@@ -421,8 +452,6 @@ def run_ours(args):
             for i in range(args.steps):
                 flush.zero_()                    # L2 flush, outside the events
                 ev[i][0].record(st)
-                if alg1_sharded:
-                    alg1()
                 run_est()
                 ev[i][1].record(st)
                 run_pre()

@@ -87,6 +87,10 @@ typedef struct {
 /* estimate only: kstar is an INPUT (from an earlier call over another row range of the same
  * layer); Alg. 1 is skipped and budget is left untouched. */
 #define PROXYATTN_FLAG_KSTAR_GIVEN 0x40u
+/* estimate only: run A1-A3 (and Alg. 1 unless KSTAR_GIVEN) but not the selection; the block
+ * scores L stay in the workspace for proxyattn_select_ws (block_cnt / block_idx may be NULL).
+ * Lets a caller overlap the scores with a K* exchange (multi-GPU) and select afterwards. */
+#define PROXYATTN_FLAG_SCORES_ONLY 0x80u
 
 #define PROXYATTN_OK               0
 #define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */
@@ -161,6 +165,11 @@ int proxyattn_budgets(const proxyattn_cfg* cfg, const void* Q, const void* K,
  * diagonal forced and counted, ties to the lower index (Z15, Z17), emitted ascending. */
 int proxyattn_select(const proxyattn_cfg* cfg, const float* L, const int32_t* kstar,
                      int32_t* block_cnt, int32_t* block_idx, void* stream);
+
+/* A5-A6 from the L a PROXYATTN_FLAG_SCORES_ONLY estimate left in `workspace` (same cfg,
+ * rows [row_begin, row_end)); kstar [Hl] is an input. */
+int proxyattn_select_ws(const proxyattn_cfg* cfg, const void* workspace, size_t workspace_bytes,
+                        const int32_t* kstar, int32_t* block_cnt, int32_t* block_idx, void* stream);
 
 /* -------------------------------------------------------------- host path -- */
 

@@ -23,6 +23,7 @@ from ._lib import (  # noqa: F401
     prefill,
     proxy_scores,
     select,
+    select_ws,
     varlen_workspace_bytes,
     with_strides,
     workspace_bytes,

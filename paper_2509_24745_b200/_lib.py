@@ -22,6 +22,7 @@ FLAG_CONSTANT_K = 0x8
 FLAG_DESIGNATED_HEAD = 0x10
 FLAG_TOKEN_MAJOR = 0x20
 FLAG_KSTAR_GIVEN = 0x40
+FLAG_SCORES_ONLY = 0x80
 
 OK = 0
 E_CONFIG = -1
@@ -83,6 +84,7 @@ class Config:
     row_begin: int = 0              # prefill row range (zig-zag row sharding); 0/0 = all rows
     row_end: int = 0
     kstar_given: bool = False       # estimate: kstar is an input (row-range calls after the first)
+    scores_only: bool = False       # estimate: stop before the selection (select_ws finishes)
     token_major: bool = False       # Q/K/V/O as [N][heads][d] with token strides (0 = packed)
     q_token_stride: int = 0
     kv_token_stride: int = 0
@@ -121,7 +123,8 @@ class Config:
                  | (FLAG_CONSTANT_K if self.constant_k else 0)
                  | (FLAG_DESIGNATED_HEAD if self.designated_head else 0)
                  | (FLAG_TOKEN_MAJOR if self.token_major else 0)
-                 | (FLAG_KSTAR_GIVEN if self.kstar_given else 0))
+                 | (FLAG_KSTAR_GIVEN if self.kstar_given else 0)
+                 | (FLAG_SCORES_ONLY if self.scores_only else 0))
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
                      self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,
@@ -142,6 +145,7 @@ _SIGS = {
     "proxyattn_proxy_scores": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P], ctypes.c_int),
     "proxyattn_budgets": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P, _P], ctypes.c_int),
     "proxyattn_select": ([_CP, _P, _P, _P, _P, _P], ctypes.c_int),
+    "proxyattn_select_ws": ([_CP, _P, ctypes.c_size_t, _P, _P, _P, _P], ctypes.c_int),
     "proxyattn_forward_host_workspace_bytes": ([_CP, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "proxyattn_forward_host": ([_CP, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], ctypes.c_int),
     "proxyattn_cost_ratio": ([_CP], ctypes.c_double),
@@ -308,6 +312,15 @@ def select(cfg: Config, L, kstar):
     idx = torch.empty(cfg.Hl, cfg.M, cfg.M, dtype=torch.int32, device=L.device)
     _check(lib().proxyattn_select(_cfg_ref(cfg), _ptr(L), _ptr(kstar), _ptr(cnt), _ptr(idx),
                                   _stream(L.device)))
+    return cnt, idx
+
+
+def select_ws(cfg: Config, workspace, kstar, out):
+    """proxyattn_select_ws: A5-A6 of rows [row_begin, row_end) from the L a scores_only
+    estimate left in `workspace`; writes out = (block_cnt, block_idx)."""
+    cnt, idx = out
+    _check(lib().proxyattn_select_ws(_cfg_ref(cfg), _ptr(workspace), workspace.numel(), _ptr(kstar),
+                                     _ptr(cnt), _ptr(idx), _stream(workspace.device)))
     return cnt, idx
 
 

@@ -291,7 +291,8 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
                     D.qb, D.qe, D.gq);
     const pa::Workspace W = pa::workspace_layout(D);
     if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
-    if (!Q || !K || !kstar || !budget || !block_cnt || !block_idx)
+    const bool scores_only = (D.flags & PROXYATTN_FLAG_SCORES_ONLY) != 0;
+    if (!Q || !K || !kstar || !budget || (!scores_only && (!block_cnt || !block_idx)))
         return fail(PROXYATTN_E_SHAPE, "NULL pointer");
     cudaStream_t st = S(stream);
     void* Pq = at<char>(ws, W.pq);
@@ -335,7 +336,21 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
         rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
         if (rc) return rc;
     }
+    if (scores_only) return PROXYATTN_OK;   // L stays in the workspace (proxyattn_select_ws)
     PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, st), "select");
+    return PROXYATTN_OK;
+}
+
+int proxyattn_select_ws(const proxyattn_cfg* cfg, const void* ws, size_t ws_bytes, const int32_t* kstar,
+                        int32_t* block_cnt, int32_t* block_idx, void* stream) {
+    pa::Dims D;
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    const pa::Workspace W = pa::workspace_layout(D);
+    if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
+    if (!kstar || !block_cnt || !block_idx) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    const float* L = reinterpret_cast<const float*>(static_cast<const char*>(ws) + W.L);
+    PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, S(stream)), "select");
     return PROXYATTN_OK;
 }
 

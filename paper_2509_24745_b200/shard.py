@@ -158,7 +158,7 @@ def zigzag_rows(M: int, world: int, rank: int, align: int = 1) -> list[tuple[int
 
 
 def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, kstar_given=False,
-                  streams=None, workspaces=None):
+                  streams=None, workspaces=None, scores_only=False):
     """A1-A6 for the block-row ranges only (zig-zag row sharding): the first call computes
     Alg. 1's kstar for every head, the others reuse it (KSTAR_GIVEN); with kstar_given the
     caller has filled out[0] already (budgets_sharded) and every call reuses it.  Block lists
@@ -166,7 +166,9 @@ def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, ks
 
     With kstar_given, `streams` and one workspace per range, the ranges' estimates run
     concurrently (each is a short chain of small, latency-bound kernels; they write disjoint
-    rows of the outputs), forked from and joined back to the current stream."""
+    rows of the outputs), forked from and joined back to the current stream.  With
+    scores_only the calls stop before the selection (select_rows finishes from each range's
+    workspace), so the K* exchange can overlap the score passes."""
     if estimate is None:
         from . import _lib
 
@@ -178,15 +180,27 @@ def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, ks
             s = streams[k % len(streams)]
             s.wait_stream(cur)
             with torch.cuda.stream(s):
-                estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=True), Q, K,
+                estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=True, scores_only=scores_only), Q, K,
                          workspaces[k % len(workspaces)], out)
             used.append(s)
         for s in used:
             cur.wait_stream(s)
         return out
+    assert not scores_only, "scores_only needs kstar_given, streams and one workspace per range"
     for k, (b, e) in enumerate(ranges):
         out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=kstar_given or k > 0), Q, K,
                        workspace, out)
+    return out
+
+
+def select_rows(cfg, ranges, workspaces, kstar, out, select_ws=None):
+    """A5-A6 of each row range from the L its scores_only estimate left in its workspace."""
+    if select_ws is None:
+        from . import _lib
+
+        select_ws = _lib.select_ws
+    for k, (b, e) in enumerate(ranges):
+        select_ws(cfg.replace(row_begin=b, row_end=e), workspaces[k % len(workspaces)], kstar, out)
     return out
 
 

@@ -55,38 +55,50 @@ full_est, full_att = timed(lambda mid=None: (pa.estimate(cfg, Q, K, wsp, out=(ks
 steps = []
 est_streams = [torch.cuda.Stream(), torch.cuda.Stream()]      # as bench.py: chunks in parallel
 est_ws = [wsp, pa.alloc_workspace(cfg, dev)]
+alg1_ws = pa.alloc_workspace(cfg, dev)
+aux = torch.cuda.Stream()
 graphs = "--graph" in sys.argv     # replay the row estimate and the attention from CUDA graphs, as bench.py
 for r in range(P):
     rows = shard.zigzag_rows(M, P, r)
 
     def alg1(r=r):
-        shard.budgets_sharded(cfg, Q, K, P, r, wsp, all_gather=lambda d, s: d.copy_(kfull), out=(kstar, budget))
+        shard.budgets_sharded(cfg, Q, K, P, r, alg1_ws, all_gather=lambda d, s: d.copy_(kfull), out=(kstar, budget))
 
-    def est_rows(rows=rows):
+    def est_rows(rows=rows):         # the chunks' score passes (K* not needed yet)
         shard.estimate_rows(cfg, Q, K, rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True,
-                            streams=est_streams, workspaces=est_ws)
+                            streams=est_streams, workspaces=est_ws, scores_only=True)
+
+    def sel_rows(rows=rows):
+        shard.select_rows(cfg, rows, est_ws, kstar, (cnt, idx))
 
     def att_rows(rows=rows):
         shard.prefill_rows(cfg, Q, K, V, cnt, idx, O, rows)
 
-    run_e, run_a = est_rows, att_rows
+    run_e, run_s, run_a = est_rows, sel_rows, att_rows
     if graphs:
         st = torch.cuda.Stream()
         st.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(st):
-            alg1(); est_rows(); att_rows()
+            alg1(); est_rows(); sel_rows(); att_rows()
             torch.cuda.synchronize()
-            ge, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            ge, gs, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(ge, stream=st):
                 est_rows()
+            with torch.cuda.graph(gs, stream=st):
+                sel_rows()
             with torch.cuda.graph(gp, stream=st):
                 att_rows()
         torch.cuda.synchronize()
-        run_e, run_a = ge.replay, gp.replay
+        run_e, run_s, run_a = ge.replay, gs.replay, gp.replay
 
-    def step(mid=None, alg1=alg1, run_e=run_e, run_a=run_a):
+    def step(mid=None, alg1=alg1, run_e=run_e, run_s=run_s, run_a=run_a):
+        cur = torch.cuda.current_stream()     # as bench.py: scores || (Alg. 1 + K* exchange)
+        aux.wait_stream(cur)
+        with torch.cuda.stream(aux):
+            run_e()
         alg1()
-        run_e()
+        cur.wait_stream(aux)
+        run_s()
         if mid is not None:
             mid.record()
         run_a()

@@ -233,3 +233,28 @@ def test_concurrent_row_range_estimates_match_sequential():
     assert torch.equal(outs[0][2], outs[1][2]) and torch.equal(outs[0][3], outs[1][3])
     for b, e in rows:
         assert torch.equal(outs[1][2][:, b:e], cnt[:, b:e])
+
+
+def test_scores_only_then_select_ws_equals_estimate():
+    # the overlapped multi-GPU estimate: A1-A3 without selection, then A5-A6 from the L left in
+    # the workspace == the one-call estimate (row ranges, K* given)
+    from paper_2509_24745_b200 import shard
+    cfg = cfg_of(128, 128, 8192, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, 8192, 128, seed=91)
+    Qd, Kd, _ = to_dev(Q, K, V)
+    kstar, budget, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    rows = shard.zigzag_rows(cfg.M, 4, 2)
+    wss = [pa.alloc_workspace(cfg, DEV), pa.alloc_workspace(cfg, DEV)]
+    out = (kstar.clone(), budget.clone(), torch.zeros_like(cnt), torch.full_like(idx, -7))
+    shard.estimate_rows(cfg, Qd, Kd, rows, out=out, kstar_given=True, scores_only=True,
+                        streams=[torch.cuda.Stream(), torch.cuda.Stream()], workspaces=wss)
+    torch.cuda.synchronize()
+    assert torch.all(out[2] == 0)                           # no selection yet
+    shard.select_rows(cfg, rows, wss, out[0], (out[2], out[3]))
+    torch.cuda.synchronize()
+    for b, e in rows:
+        assert torch.equal(out[2][:, b:e], cnt[:, b:e])
+        for h in range(8):
+            for m in range(b, e):
+                c = int(cnt[h, m])
+                assert torch.equal(out[3][h, m, :c], idx[h, m, :c])
