@@ -596,6 +596,23 @@ int score_emu() {
 // PROXYATTN_MAXPOOL_PASS=1: A3 as a second tcgen05 pass (kMaxpool) instead of from the
 // window maxima the lse pass stores (diagnostics / comparison only).
 // Key tiles per CTA of the score passes; PROXYATTN_SCORE_CHUNK=16/32/64 overrides.
+// Key tiles per CTA of the proxy (A2) pass: the default unless the causal grid of this
+// config would leave the GPU under-filled (short N), then the largest of 8 / 4 / 2 that gives
+// >= 2 CTAs per SM (128 / 64 / 32-row proxies at 16K: 48 CTAs at 16 tiles each otherwise).
+int proxy_chunk(const Dims& D, int base) {
+    int dev = 0, n_sm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const long long n_tr = (D.Ns + 127) / 128;
+    int c = base;
+    while (c > 2) {
+        long long ctas = 0;
+        for (long long tr = 0; tr < n_tr; ++tr) ctas += (tr + c) / c;
+        if (ctas * D.gl >= 2LL * n_sm) break;
+        c >>= 1;
+    }
+    return c;
+}
+
 int score_chunk() {
     static int v = -1;
     if (v < 0) {
@@ -647,7 +664,8 @@ bool score_tc_supported(const Dims& D) {
 
 size_t score_tc_scratch_bytes(const Dims& D) {
     const int n_tr = static_cast<int>((D.Ns + 127) / 128);
-    const int n_chunks = (n_tr + kChunk - 1) / kChunk;
+    const int chunk = proxy_chunk(D, score_chunk() < kChunk ? score_chunk() : kChunk);
+    const int n_chunks = (n_tr + chunk - 1) / chunk;
     // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]
     const size_t nwin = 128 / (D.bs > 0 ? D.bs : 1);
     return 2ull * D.gl * D.Ns * n_chunks * 4 + 2ull * D.gl * D.Ns * 4 + 32 +
@@ -676,7 +694,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.Ns = static_cast<int>(D.Ns);
     p.M = D.M;
     p.n_tr = static_cast<int>((D.Ns + 127) / 128);
-    p.chunk = score_chunk();
+    p.chunk = proxy_chunk(D, score_chunk());
     p.n_chunks = (p.n_tr + p.chunk - 1) / p.chunk;
     p.tr_lo = tr0;
     p.tr_hi = tr1 < 0 ? p.n_tr : tr1;
