@@ -258,3 +258,26 @@ def test_scores_only_then_select_ws_equals_estimate():
             for m in range(b, e):
                 c = int(cnt[h, m])
                 assert torch.equal(out[3][h, m, :c], idx[h, m, :c])
+
+
+@pytest.mark.parametrize("d,b", SHAPES)
+def test_varlen_packed_equals_one_call_per_sequence(d, b):
+    # packed token-major varlen at the new shapes, ragged lengths
+    def tok(t):
+        return t.transpose(0, 1).contiguous()
+    Hq, Hkv, lens = 8, 2, [1000, 0, 1536, 321]
+    seqs = [workloads.structured(Hq, Hkv, n, d, seed=100 + i, device=DEV) if n else None
+            for i, n in enumerate(lens)]
+    cu = np.concatenate([[0], np.cumsum(lens)]).tolist()
+    packed = [torch.cat([tok(s[j]) for s in seqs if s is not None], 0) for j in range(3)]
+    cfg = pa.Config(Hq, Hkv, d, 1, b, 4, 1, 0.9, token_major=True)
+    O, kstar = pa.forward_varlen(cfg, cu, *packed)
+    for i, n in enumerate(lens):
+        if n == 0:
+            continue
+        Q, K, V, _ = seqs[i]
+        c1 = pa.Config(Hq, Hkv, d, n, b, 4, 1, 0.9)
+        k1, _, cnt, idx = pa.estimate(c1, Q, K)
+        O1 = pa.prefill(c1, Q, K, V, cnt, idx)
+        assert torch.equal(kstar[i], k1)
+        assert torch.equal(O[cu[i]:cu[i + 1]], tok(O1))
