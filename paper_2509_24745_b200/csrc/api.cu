@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <map>
 #include <mutex>
@@ -540,17 +541,24 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
 }
 
 // ------------------------------------------------------------------ varlen --
-// One ProxyAttn layer per packed sequence: the cfg with seq_len = the sequence's length and
-// the pointers advanced by cu_seqlens[i] tokens; per-sequence outputs and estimate scratch
-// live in the caller's workspace (sized for the longest sequence) and are reused in stream order.
+// One ProxyAttn layer per packed sequence.  The estimate runs per sequence (the cfg with
+// seq_len = its length, pointers advanced by cu_seqlens[i] tokens, scratch reused in stream
+// order).  bf16 with b = 128: every sequence's block lists are kept (packed, each with its own
+// M) and ONE persistent attention launch covers all sequences (work items of the longest
+// sequences first); otherwise one prefill per sequence.
 struct VarlenLayout {
-    size_t kstar, budget, cnt, idx, ws, total;
+    size_t kstar, budget, cnt, idx, descs, ws, total;
+    bool packed;
 };
+static bool varlen_packed(const pa::Dims& D) {
+    return !D.fp32 && D.b == 128 && pa::attn_variant(false) == 8;
+}
 static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu, VarlenLayout& L,
                          int64_t& max_len) {
     if (!cfg || !(cfg->flags & PROXYATTN_FLAG_TOKEN_MAJOR))
         return fail(PROXYATTN_E_CONFIG, "varlen needs PROXYATTN_FLAG_TOKEN_MAJOR (packed [tokens][heads][d])");
     if (n < 0 || !cu || cu[0] != 0) return fail(PROXYATTN_E_CONFIG, "cu_seqlens must start at 0");
+    if (cfg->row_begin != 0 || cfg->row_end != 0) return fail(PROXYATTN_E_CONFIG, "varlen takes no row range");
     max_len = 0;
     for (int32_t i = 0; i < n; ++i) {
         if (cu[i + 1] < cu[i]) return fail(PROXYATTN_E_CONFIG, "cu_seqlens must be non-decreasing");
@@ -561,11 +569,22 @@ static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu,
     pa::Dims D;
     int rc = derive(&c, D);
     if (rc) return rc;
+    L.packed = varlen_packed(D);
+    size_t n_cnt = (size_t)D.Hl * D.M, n_idx = (size_t)D.Hl * D.M * D.M;
+    if (L.packed) {
+        n_cnt = n_idx = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            const size_t Mi = (size_t)((cu[i + 1] - cu[i] + D.b - 1) / D.b);
+            n_cnt += (size_t)D.Hl * Mi;
+            n_idx += (size_t)D.Hl * Mi * Mi;
+        }
+    }
     size_t off = 0;
     L.kstar = off;  off = pa::align256(off + (size_t)D.Hl * 4);
     L.budget = off; off = pa::align256(off + (size_t)D.Hl * 4);
-    L.cnt = off;    off = pa::align256(off + (size_t)D.Hl * D.M * 4);
-    L.idx = off;    off = pa::align256(off + (size_t)D.Hl * D.M * D.M * 4);
+    L.cnt = off;    off = pa::align256(off + n_cnt * 4);
+    L.idx = off;    off = pa::align256(off + n_idx * 4);
+    L.descs = off;  off = pa::align256(off + (L.packed ? (size_t)n * sizeof(pa::SeqDesc) : 0));
     L.ws = off;     off = pa::align256(off + pa::workspace_layout(D).total);
     L.total = off;
     return PROXYATTN_OK;
@@ -598,23 +617,73 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
     const size_t el = D0.fp32 ? 4 : 2;
     c.q_token_stride = D0.q_ts;      // pin the strides: the defaults depend on nothing per sequence,
     c.kv_token_stride = D0.kv_ts;    // but make it explicit
+    cudaStream_t st = S(stream);
+    std::vector<pa::SeqDesc> descs;
+    std::vector<size_t> cnt_off(n_seqs, 0), idx_off(n_seqs, 0);
+    if (L.packed) {
+        // list offsets in sequence order; work items longest sequence first (heavy rows early)
+        size_t oc = 0, oi = 0;
+        for (int32_t i = 0; i < n_seqs; ++i) {
+            const size_t Mi = (size_t)((cu[i + 1] - cu[i] + D0.b - 1) / D0.b);
+            cnt_off[i] = oc;
+            idx_off[i] = oi;
+            oc += (size_t)D0.Hl * Mi;
+            oi += (size_t)D0.Hl * Mi * Mi;
+        }
+        std::vector<int32_t> order;
+        for (int32_t i = 0; i < n_seqs; ++i)
+            if (cu[i + 1] > cu[i]) order.push_back(i);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t x, int32_t y) { return cu[x + 1] - cu[x] > cu[y + 1] - cu[y]; });
+        long long item0 = 0;
+        for (int32_t i : order) {
+            pa::SeqDesc sd{};
+            sd.tok0 = cu[i];
+            sd.cnt_off = (long long)cnt_off[i];
+            sd.idx_off = (long long)idx_off[i];
+            sd.N = static_cast<int>(cu[i + 1] - cu[i]);
+            sd.M = static_cast<int>((sd.N + D0.b - 1) / D0.b);
+            sd.item0 = static_cast<int>(item0);
+            item0 += (long long)D0.Hl * sd.M;
+            descs.push_back(sd);
+        }
+        if (item0 > INT32_MAX || cu[n_seqs] > INT32_MAX)
+            return fail(PROXYATTN_E_UNSUPPORTED, "varlen batch too large for one launch");
+        if (!descs.empty())   // before any kernel: a pageable copy synchronises the stream first
+            PA_CUDA(cudaMemcpyAsync(at<char>(ws, L.descs), descs.data(), descs.size() * sizeof(pa::SeqDesc),
+                                    cudaMemcpyHostToDevice, st), "varlen descriptors");
+    }
     for (int32_t i = 0; i < n_seqs; ++i) {
         const int64_t n = cu[i + 1] - cu[i];
         if (n == 0) continue;
         c.seq_len = n;
         const size_t qo = (size_t)cu[i] * D0.q_ts * el, ko = (size_t)cu[i] * D0.kv_ts * el;
         int32_t* ks = at<int32_t>(ws, L.kstar);
+        int32_t* cnt = at<int32_t>(ws, L.cnt) + cnt_off[i];
+        int32_t* idx = at<int32_t>(ws, L.idx) + idx_off[i];
         rc = proxyattn_estimate(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
-                                at<char>(ws, L.ws), ws_bytes - L.ws, ks, at<float>(ws, L.budget),
-                                at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), stream);
+                                at<char>(ws, L.ws), ws_bytes - L.ws, ks, at<float>(ws, L.budget), cnt, idx,
+                                stream);
         if (rc) return rc;
-        rc = proxyattn_prefill(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
-                               static_cast<const char*>(V) + ko, at<int32_t>(ws, L.cnt),
-                               at<int32_t>(ws, L.idx), static_cast<char*>(O) + qo, stream);
-        if (rc) return rc;
+        if (!L.packed) {
+            rc = proxyattn_prefill(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
+                                   static_cast<const char*>(V) + ko, cnt, idx, static_cast<char*>(O) + qo,
+                                   stream);
+            if (rc) return rc;
+        }
         if (kstar)
             PA_CUDA(cudaMemcpyAsync(kstar + (size_t)i * D0.Hl, ks, (size_t)D0.Hl * 4,
-                                    cudaMemcpyDeviceToDevice, S(stream)), "varlen kstar");
+                                    cudaMemcpyDeviceToDevice, st), "varlen kstar");
+    }
+    if (L.packed && !descs.empty()) {
+        c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
+        pa::Dims D;
+        if ((rc = derive(&c, D))) return rc;
+        const int n_items = descs.back().item0 + D.Hl * descs.back().M;
+        PA_CUDA(pa::launch_attn_tc8_varlen(D, Q, K, V, at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), O,
+                                           at<pa::SeqDesc>(ws, L.descs), static_cast<int>(descs.size()),
+                                           n_items, st),
+                "attn_tc8 varlen");
     }
     return PROXYATTN_OK;
 }

@@ -135,14 +135,16 @@ struct PairWalk {
     }
 };
 
-template <int kEmu, int kD, int kB>   // kEmu: of every 8 key-column pairs, kEmu use the FMA-pipe exp2
+// kEmu: of every 8 key-column pairs, kEmu use the FMA-pipe exp2; kVar: varlen (packed sequences)
+template <int kEmu, int kD, int kB, bool kVar = false>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
                 int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt,
-                int diag_noload, const int* __restrict__ kvperm) {
+                int diag_noload, const int* __restrict__ kvperm, const SeqDesc* __restrict__ seqs,
+                int n_seqs) {
     using Sh = Shape<kD, kB>;
     constexpr bool kPair = (kB == 64);
     constexpr int kNB = kPair ? 2 : 1;   // S / P buffers per stream (a 64-key S is 64 columns)
@@ -200,19 +202,43 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
 
+    // The current item's sequence (varlen: n_seqs > 0, one packed launch over all sequences;
+    // each role decodes every item it handles, so these are per-thread): token offset, length,
+    // block rows and the base of its block lists.
+    long long c_tok = 0;
+    int c_N = N, c_M = M;
+    const int* c_cnt = block_cnt;
+    const int* c_idx = block_idx;
     // item decode (kv-head major — KV heads in decreasing total work when kvperm is given, so
     // the last heads scheduled are the lightest — heavy rows first): head hl, its block row mA (kB = 128), or
     // its row pair (mA, mB) = (2q, 2q+1) (kB = 64; -1 for a row outside [row_lo, row_hi))
     auto decode = [&](int item, int& hl, int& mA, int& mB, int& kvl) {
-        kvl = kvperm ? __ldg(kvperm + item / per_kv) : item / per_kv;
-        const int rem = item % per_kv;
+        int pk = per_kv, rhi = row_hi;
+        if (kVar && n_seqs > 0) {  // varlen (kB = 128): sequence s holds items [item0_s, item0_{s+1})
+            int lo = 0, hi = n_seqs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(&seqs[mid].item0) <= item) lo = mid;
+                else hi = mid - 1;
+            }
+            c_tok = __ldg(&seqs[lo].tok0);
+            c_N = __ldg(&seqs[lo].N);
+            c_M = __ldg(&seqs[lo].M);
+            c_cnt = block_cnt + __ldg(&seqs[lo].cnt_off);
+            c_idx = block_idx + __ldg(&seqs[lo].idx_off);
+            item -= __ldg(&seqs[lo].item0);
+            pk = r * c_M;
+            rhi = c_M;
+        }
+        kvl = kvperm ? __ldg(kvperm + item / pk) : item / pk;
+        const int rem = item % pk;
         hl = kvl * r + rem % r;
         if (kPair) {
             const int q = q_hi - 1 - rem / r;
             mA = (2 * q >= row_lo) ? 2 * q : -1;
             mB = (2 * q + 1 < row_hi) ? 2 * q + 1 : -1;
         } else {
-            mA = row_hi - 1 - rem / r;
+            mA = rhi - 1 - rem / r;
             mB = -1;
         }
     };
@@ -225,10 +251,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         return x;
     };
     auto list_of = [&](int hl, int m) -> const int* {
-        return dense ? nullptr : block_idx + (static_cast<long long>(hl) * M + m) * M;
+        return dense ? nullptr : c_idx + (static_cast<long long>(hl) * c_M + m) * c_M;
     };
     auto count_of = [&](int hl, int m) -> int {
-        return m < 0 ? 0 : dense ? m + 1 : __ldg(block_cnt + static_cast<long long>(hl) * M + m);
+        return m < 0 ? 0 : dense ? m + 1 : __ldg(c_cnt + static_cast<long long>(hl) * c_M + m);
     };
     auto walk_of = [&](int hl, int mA, int mB) -> PairWalk {
         PairWalk w;
@@ -270,7 +296,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     decode(x.item, hl, mA, mB, kvl);
                     if (it > 0) mbar_wait(&bars->q_empty, (it - 1) & 1);   // last S of it-1 done
                     // the unit's 128 query rows (kB = 64: rows 2q*64 .. 2q*64+127)
-                    const int q_row0 = kPair ? (mA >= 0 ? mA : mB - 1) * kB : mA * kTileRows;
+                    const int q_row0 = static_cast<int>(c_tok) + (kPair ? (mA >= 0 ? mA : mB - 1) * kB : mA * kTileRows);
                     mbar_expect_tx(&bars->q_full, Sh::kQTile);
 #pragma unroll
                     for (int ch = 0; ch < kD / 64; ++ch)
@@ -291,7 +317,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
                             for (int ch = 0; ch < kD / 64; ++ch)
                                 tma_load_3d(sK + st * Sh::kKTile + ch * Sh::kKBox, &tmK, &bars->k_full[st],
-                                            ch * 64, n * kB, kvl);
+                                            ch * 64, static_cast<int>(c_tok) + n * kB, kvl);
                         }
                     }
                 }
@@ -321,7 +347,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
                         for (int ch = 0; ch < kD / 64; ++ch)
                             tma_load_3d(sV + st * Sh::kKTile + ch * Sh::kKBox, &tmV, &bars->v_full[st],
-                                        ch * 64, n * kB, kvl);
+                                        ch * 64, static_cast<int>(c_tok) + n * kB, kvl);
                     }
                 }
                 __syncwarp();
@@ -433,8 +459,8 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             }
             mbar_wait(&bars->o_final, it & 1);
             tc_fence_after();
-            const bool row_valid = m >= 0 && pos < N;
-            uint4* dst = reinterpret_cast<uint4*>(O + static_cast<long long>(hl) * o_hs + (m < 0 ? 0 : pos) * o_ts);
+            const bool row_valid = m >= 0 && pos < c_N;
+            uint4* dst = reinterpret_cast<uint4*>(O + static_cast<long long>(hl) * o_hs + (c_tok + (m < 0 ? 0 : pos)) * o_ts);
 #pragma unroll
             for (int h2 = 0; h2 < kD / 64; ++h2) {
                 uint32_t o[2][32];
@@ -830,25 +856,28 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
 
 using AttnKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, __nv_bfloat16*,
                             const int*, const int*, int, int, int, float, int, int, int, Sched*, int*,
-                            int, long long, long long, const int*, int, const int*);
+                            int, long long, long long, const int*, int, const int*, const SeqDesc*, int);
 
-template <int kD, int kB, int kEmu>
+template <int kD, int kB, int kEmu, bool kVar = false>
 AttnKernel kernel_with_attr() {
     static bool set = false;
     if (!set) {
-        if (cudaFuncSetAttribute(attn_tc8_kernel<kEmu, kD, kB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(attn_tc8_kernel<kEmu, kD, kB, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Shape<kD, kB>::kSmem)) != cudaSuccess)
             return nullptr;
         set = true;
     }
-    return attn_tc8_kernel<kEmu, kD, kB>;
+    return attn_tc8_kernel<kEmu, kD, kB, kVar>;
 }
 
 }  // namespace
 
-cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
-                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
+namespace {
+cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* V, const int* block_cnt,
+                       const int* block_idx, void* O, cudaStream_t st, const SeqDesc* seqs, int n_seqs,
+                       int varlen_items) {
     if (!((D.d == 64 || D.d == 128) && (D.b == 64 || D.b == 128))) return cudaErrorInvalidValue;
+    if (n_seqs > 0 && (D.b != 128 || !block_cnt)) return cudaErrorInvalidValue;   // varlen: sparse, b = 128
     CUtensorMap mq, mk, mv;
     if (!make_map_bf16_sw128_3d(&mq, Q, D.Hl, D.N, D.q_ts, D.q_hs, 128, D.d) ||
         !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d) ||
@@ -863,7 +892,9 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 0;
     }
     AttnKernel kern = nullptr;
-    if (D.d == 128 && D.b == 128) {
+    if (n_seqs > 0) {          // varlen instantiations (b = 128; the default exp2 split per d)
+        kern = D.d == 128 ? kernel_with_attr<128, 128, 0, true>() : kernel_with_attr<64, 128, 2, true>();
+    } else if (D.d == 128 && D.b == 128) {
         kern = emu == 0 ? kernel_with_attr<128, 128, 0>() : emu == 1 ? kernel_with_attr<128, 128, 1>()
              : emu == 2 ? kernel_with_attr<128, 128, 2>() : emu == 3 ? kernel_with_attr<128, 128, 3>()
                                                           : kernel_with_attr<128, 128, 4>();
@@ -888,7 +919,8 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     const bool pair = D.b == 64;
     // work units: (head, block row), or (head, row pair) for b = 64
     const int nrows = pair ? (D.re + 1) / 2 - D.rb / 2 : D.re - D.rb;
-    const size_t n_items = static_cast<size_t>(D.Hl) * static_cast<size_t>(nrows);
+    const size_t n_items = n_seqs > 0 ? static_cast<size_t>(varlen_items)
+                                      : static_cast<size_t>(D.Hl) * static_cast<size_t>(nrows);
     SchedBuf* sb = sched_for(st, n_items);
     if (!sb) return cudaErrorMemoryAllocation;
     cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);
@@ -904,7 +936,7 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     }
     // KV heads in decreasing work (sparse launches with more than one local KV head, <= 64)
     const int* kvperm = nullptr;
-    if (block_cnt && D.Hkvl > 1 && D.Hkvl <= 64) {
+    if (block_cnt && n_seqs == 0 && D.Hkvl > 1 && D.Hkvl <= 64) {
         kv_order_kernel<<<D.Hkvl, 1024, 0, st>>>(block_cnt, D.M, D.r, D.rb, D.re, D.Hkvl, sb->kvsum,
                                                  sb->kvdone, sb->kvperm);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -927,11 +959,24 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
         kern<<<grid, kThreads, smem, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
             D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
-            D.q_hs, D.q_ts, sb->ucnt, noload, kvperm);
+            D.q_hs, D.q_ts, sb->ucnt, noload, kvperm, seqs, n_seqs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
+                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
+    return launch_tc8(D, Q, K, V, block_cnt, block_idx, O, st, nullptr, 0, 0);
+}
+
+cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, const void* V,
+                                   const int* block_cnt, const int* block_idx, void* O,
+                                   const SeqDesc* seqs, int n_seqs, int n_items, cudaStream_t st) {
+    return launch_tc8(D, Q, K, V, block_cnt, block_idx, O, st, seqs, n_seqs, n_items);
 }
 
 }  // namespace pa

@@ -47,6 +47,17 @@ cudaError_t launch_attn_tc6(const Dims& D, const void* Q, const void* K, const v
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 cudaError_t launch_attn_tc7(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
+// Varlen (one packed launch over several sequences, token-major, b = 128): sequence s owns the
+// tokens [tok0, tok0 + N) of the packed tensors, its block lists start at cnt_off / idx_off
+// ([Hl][M] / [Hl][M][M] of its own M), and its work items are [item0, item0 + Hl * M).
+struct SeqDesc {
+    long long tok0, cnt_off, idx_off;
+    int N, M, item0, pad;
+};
+// D: the packed layout (seq_len = total tokens); seqs: device array of n_seqs descriptors.
+cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, const void* V,
+                                   const int* block_cnt, const int* block_idx, void* O,
+                                   const SeqDesc* seqs, int n_seqs, int n_items, cudaStream_t st);
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 long long*& attn_trace_ptr();
