@@ -194,8 +194,8 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const v
  * Everything is enqueued on `stream`; the estimate scratch is reused sequence after
  * sequence.  bf16 with b = 128: the sequences' block lists are kept side by side in the
  * workspace and ONE attention launch covers every sequence (longest first); otherwise one
- * prefill per sequence.  The sequence table is copied from host memory at the start of the
- * call (the call is not capturable in a CUDA graph).
+ * prefill per sequence.  The sequence table travels as kernel parameters (no host copy), so
+ * the call is asynchronous.
  * kstar (optional, DEVICE [n_seqs][Hl] int32) receives each sequence's K*_h. */
 int proxyattn_varlen_workspace_bytes(const proxyattn_cfg* cfg, int32_t n_seqs,
                                      const int64_t* cu_seqlens, size_t* out_bytes);

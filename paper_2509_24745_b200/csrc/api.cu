@@ -548,6 +548,7 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
 // sequences first); otherwise one prefill per sequence.
 struct VarlenLayout {
     size_t kstar, budget, cnt, idx, descs, ws, total;
+    size_t kstar2, budget2, ws2;   // packed: the second concurrent estimate's staging / scratch
     bool packed;
 };
 static bool varlen_packed(const pa::Dims& D) {
@@ -586,7 +587,26 @@ static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu,
     L.idx = off;    off = pa::align256(off + n_idx * 4);
     L.descs = off;  off = pa::align256(off + (L.packed ? (size_t)n * sizeof(pa::SeqDesc) : 0));
     L.ws = off;     off = pa::align256(off + pa::workspace_layout(D).total);
+    L.kstar2 = L.budget2 = L.ws2 = 0;
+    if (L.packed) {   // two sequences' estimates in flight (two streams)
+        L.kstar2 = off;  off = pa::align256(off + (size_t)D.Hl * 4);
+        L.budget2 = off; off = pa::align256(off + (size_t)D.Hl * 4);
+        L.ws2 = off;     off = pa::align256(off + pa::workspace_layout(D).total);
+    }
     L.total = off;
+    return PROXYATTN_OK;
+}
+
+// Per-device second stream of the packed varlen path (created once, non-blocking).
+static int varlen_stream(cudaStream_t* out) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> per_dev;
+    int dev = 0;
+    PA_CUDA(cudaGetDevice(&dev), "get device");
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& s = per_dev[dev];
+    if (!s) PA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    *out = s;
     return PROXYATTN_OK;
 }
 
@@ -649,21 +669,36 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
         }
         if (item0 > INT32_MAX || cu[n_seqs] > INT32_MAX)
             return fail(PROXYATTN_E_UNSUPPORTED, "varlen batch too large for one launch");
-        if (!descs.empty())   // before any kernel: a pageable copy synchronises the stream first
-            PA_CUDA(cudaMemcpyAsync(at<char>(ws, L.descs), descs.data(), descs.size() * sizeof(pa::SeqDesc),
-                                    cudaMemcpyHostToDevice, st), "varlen descriptors");
+        if (!descs.empty())   // through kernel parameters: no pageable copy, the call stays async
+            PA_CUDA(pa::write_seq_descs(at<pa::SeqDesc>(ws, L.descs), descs.data(),
+                                        static_cast<int>(descs.size()), st), "varlen descriptors");
     }
+    // packed: consecutive sequences' estimates alternate between `stream` and a second stream
+    // (each with its own scratch) so the short, latency-bound estimates overlap
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (L.packed && !descs.empty()) {
+        if ((rc = varlen_stream(&st2))) return rc;
+        PA_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
+        PA_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event create");
+        PA_CUDA(cudaEventRecord(ev_fork, st), "record");
+        PA_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0), "wait");
+    }
+    int n_done = 0;
     for (int32_t i = 0; i < n_seqs; ++i) {
         const int64_t n = cu[i + 1] - cu[i];
         if (n == 0) continue;
         c.seq_len = n;
         const size_t qo = (size_t)cu[i] * D0.q_ts * el, ko = (size_t)cu[i] * D0.kv_ts * el;
-        int32_t* ks = at<int32_t>(ws, L.kstar);
+        const bool second = st2 && (n_done++ & 1);
+        cudaStream_t si = second ? st2 : st;
+        int32_t* ks = at<int32_t>(ws, second ? L.kstar2 : L.kstar);
+        float* bu = at<float>(ws, second ? L.budget2 : L.budget);
+        const size_t wo = second ? L.ws2 : L.ws;
         int32_t* cnt = at<int32_t>(ws, L.cnt) + cnt_off[i];
         int32_t* idx = at<int32_t>(ws, L.idx) + idx_off[i];
         rc = proxyattn_estimate(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
-                                at<char>(ws, L.ws), ws_bytes - L.ws, ks, at<float>(ws, L.budget), cnt, idx,
-                                stream);
+                                at<char>(ws, wo), ws_bytes - wo, ks, bu, cnt, idx, si);
         if (rc) return rc;
         if (!L.packed) {
             rc = proxyattn_prefill(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
@@ -673,7 +708,13 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
         }
         if (kstar)
             PA_CUDA(cudaMemcpyAsync(kstar + (size_t)i * D0.Hl, ks, (size_t)D0.Hl * 4,
-                                    cudaMemcpyDeviceToDevice, st), "varlen kstar");
+                                    cudaMemcpyDeviceToDevice, si), "varlen kstar");
+    }
+    if (st2) {
+        PA_CUDA(cudaEventRecord(ev_join, st2), "record");
+        PA_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "wait");
+        cudaEventDestroy(ev_fork);   // released once the recorded work completes
+        cudaEventDestroy(ev_join);
     }
     if (L.packed && !descs.empty()) {
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token

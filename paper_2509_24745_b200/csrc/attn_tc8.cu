@@ -973,6 +973,28 @@ cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const v
     return launch_tc8(D, Q, K, V, block_cnt, block_idx, O, st, nullptr, 0, 0);
 }
 
+namespace {
+struct DescChunk {
+    SeqDesc d[64];
+    int n;
+};
+__global__ void write_descs_kernel(SeqDesc* dst, const __grid_constant__ DescChunk c) {
+    if (static_cast<int>(threadIdx.x) < c.n) dst[threadIdx.x] = c.d[threadIdx.x];
+}
+}  // namespace
+
+cudaError_t write_seq_descs(SeqDesc* dst, const SeqDesc* host, int n, cudaStream_t st) {
+    for (int i = 0; i < n; i += 64) {
+        DescChunk c{};
+        c.n = n - i < 64 ? n - i : 64;
+        for (int k = 0; k < c.n; ++k) c.d[k] = host[i + k];
+        write_descs_kernel<<<1, 64, 0, st>>>(dst + i, c);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, const void* V,
                                    const int* block_cnt, const int* block_idx, void* O,
                                    const SeqDesc* seqs, int n_seqs, int n_items, cudaStream_t st) {

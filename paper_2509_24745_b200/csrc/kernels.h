@@ -54,6 +54,9 @@ struct SeqDesc {
     long long tok0, cnt_off, idx_off;
     int N, M, item0, pad;
 };
+// Writes n descriptors into device memory from kernel parameters (no pageable host copy, so
+// the varlen call stays asynchronous): 64 per launch.
+cudaError_t write_seq_descs(SeqDesc* dst, const SeqDesc* host, int n, cudaStream_t st);
 // D: the packed layout (seq_len = total tokens); seqs: device array of n_seqs descriptors.
 cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, const void* V,
                                    const int* block_cnt, const int* block_idx, void* O,

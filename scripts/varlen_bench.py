@@ -34,6 +34,20 @@ def timed(fn, it=10):
 
 
 t_packed = timed(lambda: pa.forward_varlen(cfg, cu, *packed))
+# the same call replayed from a CUDA graph (the call is asynchronous and capturable): GPU time
+wsv = torch.empty(pa.varlen_workspace_bytes(cfg, cu), dtype=torch.uint8, device=dev)
+Ov = torch.empty_like(packed[0])
+ksv = torch.zeros(len(lens), Hq, dtype=torch.int32, device=dev)
+st = torch.cuda.Stream()
+st.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(st):
+    pa.forward_varlen(cfg, cu, *packed, O=Ov, workspace=wsv, kstar=ksv)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        pa.forward_varlen(cfg, cu, *packed, O=Ov, workspace=wsv, kstar=ksv)
+torch.cuda.synchronize()
+t_graph = timed(g.replay)
 cfgs = [pa.Config(Hq, Hkv, 128, n, 128, 4, 1, 0.9) for n in lens]
 wss = [pa.alloc_workspace(c, dev) for c in cfgs]
 
@@ -45,4 +59,5 @@ def loop():
 
 
 t_loop = timed(loop)
-print(json.dumps({"lens": lens, "packed_one_launch_ms": t_packed, "per_sequence_calls_ms": t_loop}))
+print(json.dumps({"lens": lens, "packed_one_launch_ms": t_packed, "packed_graph_replay_ms": t_graph,
+                  "per_sequence_calls_ms": t_loop}))
