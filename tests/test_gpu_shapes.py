@@ -281,3 +281,21 @@ def test_varlen_packed_equals_one_call_per_sequence(d, b):
         O1 = pa.prefill(c1, Q, K, V, cnt, idx)
         assert torch.equal(kstar[i], k1)
         assert torch.equal(O[cu[i]:cu[i + 1]], tok(O1))
+
+
+@pytest.mark.parametrize("d,b", SHAPES + [(128, 128)])
+@pytest.mark.parametrize("N", [1, 63, 65, 129, 200])
+def test_tiny_and_ragged_lengths(d, b, N):
+    # a single token, lengths just below / above a block, fewer rows than a row pair
+    cfg = cfg_of(d, b, N, heads=(4, 2), g=2, gamma=0.9)
+    Q, K, V, _ = workloads.structured(4, 2, N, d, seed=110 + N)
+    run_staged(cfg, Q, K, V, min_checked=0.0)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_block64_stride8_simt_estimation_fallback(d):
+    # b / s = 8 sampled rows per block: below the score engine's 16-column windows, so the
+    # bf16 estimate runs the SIMT kernels; the attention stays on tcgen05
+    cfg = cfg_of(d, 64, 2048, heads=(8, 2), stride=8)
+    Q, K, V, _ = workloads.structured(8, 2, 2048, d, seed=120)
+    run_staged(cfg, Q, K, V)
