@@ -323,6 +323,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     w = dict(WORKLOADS[args.workload])
+    if args.gamma:
+        w["gamma"] = args.gamma
+        w["name"] = w["name"] + f"-gamma{args.gamma:g}"
     if args.seq_len:
         w["seq_len"] = args.seq_len
         w["name"] = w["name"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
@@ -708,6 +711,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq-len", type=int, default=0, help="override N (sweep)")
+    ap.add_argument("--gamma", type=float, default=0.0, help="override the Alg. 1 threshold (sweep)")
     ap.add_argument("--workload", default="llama3.1-8b-attn-128k", choices=sorted(WORKLOADS))
     ap.add_argument("--shard", default="rows", choices=["rows", "heads"],
                     help="N > 1: zig-zag query-block-row sharding (balanced, no traffic) or "
