@@ -295,6 +295,10 @@ __global__ void budget_mass_simt(Dims D, const T* __restrict__ Q, const T* __res
 }
 
 // Bitonic sort of (key, id) pairs in shared memory, order: key descending, id ascending.
+// A stage with stride <= 16 only pairs elements inside the 64-element segments a warp's 32
+// threads own (pair t: lo = 2t - t mod stride), so consecutive such stages need only a
+// __syncwarp; cross-warp stages (stride >= 32) and the end of every merge size keep the
+// block barrier.  Same comparisons, same result.
 __device__ __forceinline__ bool before(float ka, int ia, float kb, int ib) {
     return ka > kb || (ka == kb && ia < ib);
 }
@@ -312,8 +316,10 @@ __device__ void bitonic_sort(float* key, int* id, int P) {
                     const int ti = id[lo]; id[lo] = id[hi]; id[hi] = ti;
                 }
             }
-            __syncthreads();
+            if (stride > 16) __syncthreads();
+            else __syncwarp();
         }
+        __syncthreads();
     }
 }
 
