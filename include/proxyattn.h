@@ -176,7 +176,11 @@ int proxyattn_select_ws(const proxyattn_cfg* cfg, const void* workspace, size_t 
 /* End-to-end call on HOST buffers (pinned or pageable): copies Q/K/V to the device
  * workspace, runs estimate + prefill, copies O (and kstar when non-NULL) back, and
  * synchronises `stream` before returning.  device_ws must hold
- * proxyattn_forward_host_workspace_bytes(cfg) bytes. */
+ * proxyattn_forward_host_workspace_bytes(cfg) bytes.  Pipelined over query-block-row chunks,
+ * last rows first (K, the last Q chunk, V, then the other Q chunks on an upload stream; each
+ * chunk's row-range estimate and attention as soon as it lands; O chunks down on a third
+ * stream); outputs equal the device-resident estimate + prefill bit for bit.  Needs every
+ * proxy group of the shard to be local and no row range. */
 int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out_bytes);
 int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const void* K_host,
                            const void* V_host, void* O_host, int32_t* kstar_host,

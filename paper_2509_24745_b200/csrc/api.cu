@@ -479,57 +479,104 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     pa::Dims D;
     int rc = derive(cfg, D);
     if (rc) return rc;
+    if (!groups_complete(D))
+        return fail(PROXYATTN_E_CONFIG, "forward_host needs every proxy group of the shard to be local");
+    if (D.rb != 0 || D.re != D.M) return fail(PROXYATTN_E_CONFIG, "forward_host takes no row range");
     const HostLayout H = host_layout(D);
     if (!dws || dws_bytes < H.total) return fail(PROXYATTN_E_WORKSPACE, "device workspace needs %zu bytes", H.total);
     if (!Qh || !Kh || !Vh || !Oh) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
     cudaStream_t st = S(stream);
-    const size_t qb = q_bytes(D), kb = kv_bytes(D);
-    // Pipeline (head-major): K and Q up on `stream` -> estimate; V up per KV head on the
-    // upload stream meanwhile; attention per KV head (its r query heads) as soon as that
-    // head's V has landed; each head's O down on the download stream while the next head
-    // computes.  Token-major tensors interleave heads, so they take the serial order.
-    const int chunks = D.tok ? 1 : D.Hkvl;
+    const size_t el = D.fp32 ? 4 : 2;
+    const size_t kb = kv_bytes(D);
+    // Pipeline over query-block-row chunks, LAST rows first.  The block lists of rows [r0, r1)
+    // need only their own queries, the keys before them and K* (Alg. 1: the last block's
+    // queries), so: K up, then the last row chunk of Q (Alg. 1 and that chunk's estimate can
+    // start), then V, then the remaining Q chunks in reverse order; each chunk's row-range
+    // estimate (K* given) and attention run as soon as it has landed, and its O goes down on
+    // a third stream.  The heaviest rows (the longest causal lists) thus compute while the rest
+    // of Q is still crossing PCIe.  Chunk edges sit on 128-row proxy tiles (and on b = 64 row
+    // pairs), so every chunk's lists and outputs equal the one-shot call's bit for bit.
+    const int align = std::max(D.b == 64 ? 2 : 1, std::max(1, 128 / D.bs));
+    const int units = (D.M + align - 1) / align;
+    static int want = -1;          // PROXYATTN_HOST_CHUNKS overrides the 16 row chunks (128K:
+    if (want < 0) {                // 1 / 4 / 8 / 16 / 24 chunks -> 63.5 / 41.2 / 37.3 / 35.8 / 35.8 ms)
+        const char* e = getenv("PROXYATTN_HOST_CHUNKS");
+        want = e ? std::max(1, atoi(e)) : 16;
+    }
+    const int n_ch = std::max(1, std::min(want, units));
+    std::vector<std::pair<int, int>> ch;                  // [r0, r1) block rows, last rows first
+    for (int c = n_ch - 1; c >= 0; --c) {
+        const int r0 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * c) / n_ch));
+        const int r1 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * (c + 1)) / n_ch));
+        if (r1 > r0) ch.emplace_back(r0, r1);
+    }
     HostStreams hs;
     if ((rc = host_streams(hs))) return rc;
-    std::vector<cudaEvent_t> ev(2 * chunks + 2);
+    const int nc = static_cast<int>(ch.size());
+    std::vector<cudaEvent_t> ev(2 * nc + 3);
     for (auto& e : ev) PA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     auto cleanup = [&]() { for (auto& e : ev) cudaEventDestroy(e); };
-    cudaEvent_t ev_qk = ev[0], ev_done = ev[1];
-    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, st), "H2D K");
-    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.q), Qh, qb, cudaMemcpyHostToDevice, st), "H2D Q");
-    PA_CUDA(cudaEventRecord(ev_qk, st), "record");
-    PA_CUDA(cudaStreamWaitEvent(hs.up, ev_qk, 0), "wait");        // V after Q/K on the link
-    const size_t vchunk = kb / chunks;
-    for (int c = 0; c < chunks; ++c) {
-        PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v) + c * vchunk, static_cast<const char*>(Vh) + c * vchunk,
-                                vchunk, cudaMemcpyHostToDevice, hs.up), "H2D V");
-        PA_CUDA(cudaEventRecord(ev[2 + c], hs.up), "record");
-    }
-    rc = proxyattn_estimate(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws),
-                            dws_bytes - H.ws, at<int32_t>(dws, H.kstar), at<float>(dws, H.budget),
-                            at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), stream);
-    if (rc) { cleanup(); return rc; }
-    const size_t el = D.fp32 ? 4 : 2;
-    const size_t qchunk = qb / chunks;
-    const int hq = D.Hl / chunks;                               // query heads per chunk (= r)
-    for (int c = 0; c < chunks; ++c) {
-        PA_CUDA(cudaStreamWaitEvent(st, ev[2 + c], 0), "wait");
-        proxyattn_cfg cc = *cfg;
-        if (chunks > 1) {
-            cc.q_head_begin = D.qb + c * hq;
-            cc.q_head_end = cc.q_head_begin + hq;
+    cudaEvent_t ev_k = ev[0], ev_v = ev[1], ev_done = ev[2];
+    // token range [t0, t1) of Q / O between host and device, in the configured layout
+    auto copy_rows = [&](void* dst, const void* src, int r0, int r1, cudaMemcpyKind kind, cudaStream_t s) -> int {
+        const long long t0 = static_cast<long long>(r0) * D.b, t1 = std::min<long long>(static_cast<long long>(r1) * D.b, D.N);
+        if (t1 <= t0) return PROXYATTN_OK;
+        if (D.tok) {   // [N][token stride]: one contiguous range
+            const size_t off = static_cast<size_t>(t0) * D.q_ts * el, n = static_cast<size_t>(t1 - t0) * D.q_ts * el;
+            PA_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n, kind, s),
+                    "copy rows");
+        } else {       // [Hl][N][d]: one strided block per head
+            const size_t pitch = static_cast<size_t>(D.N) * D.d * el, off = static_cast<size_t>(t0) * D.d * el;
+            PA_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + off, pitch, static_cast<const char*>(src) + off, pitch,
+                                      static_cast<size_t>(t1 - t0) * D.d * el, D.Hl, kind, s), "copy rows");
         }
-        rc = proxyattn_prefill(&cc, at<char>(dws, H.q) + c * qchunk, at<char>(dws, H.k) + c * vchunk,
-                               at<char>(dws, H.v) + c * vchunk, at<int32_t>(dws, H.cnt) + (size_t)c * hq * D.M,
-                               at<int32_t>(dws, H.idx) + (size_t)c * hq * D.M * D.M,
-                               at<char>(dws, H.o) + c * qchunk, stream);
-        if (rc) { cleanup(); return rc; }
-        PA_CUDA(cudaEventRecord(ev[2 + chunks + c], st), "record");
-        PA_CUDA(cudaStreamWaitEvent(hs.down, ev[2 + chunks + c], 0), "wait");
-        PA_CUDA(cudaMemcpyAsync(static_cast<char*>(Oh) + c * qchunk, at<char>(dws, H.o) + c * qchunk, qchunk,
-                                cudaMemcpyDeviceToHost, hs.down), "D2H O");
+        return PROXYATTN_OK;
+    };
+    // uploads: K, Q chunk 0 (the last rows), V, the other Q chunks
+    PA_CUDA(cudaEventRecord(ev[0], st), "record");                 // after the caller's prior work
+    PA_CUDA(cudaStreamWaitEvent(hs.up, ev[0], 0), "wait");
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, hs.up), "H2D K");
+    PA_CUDA(cudaEventRecord(ev_k, hs.up), "record");
+    for (int c = 0; c < nc; ++c) {
+        if ((rc = copy_rows(at<char>(dws, H.q), Qh, ch[c].first, ch[c].second, cudaMemcpyHostToDevice, hs.up))) {
+            cleanup();
+            return rc;
+        }
+        PA_CUDA(cudaEventRecord(ev[3 + c], hs.up), "record");
+        if (c == 0) {
+            PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, hs.up), "H2D V");
+            PA_CUDA(cudaEventRecord(ev_v, hs.up), "record");
+        }
     }
-    (void)el;
+    // compute: Alg. 1 once, then per chunk estimate (K* given) + attention; O chunks down
+    proxyattn_cfg cc = *cfg;
+    for (int c = 0; c < nc; ++c) {
+        PA_CUDA(cudaStreamWaitEvent(st, c == 0 ? ev_k : ev[3 + c], 0), "wait");
+        if (c == 0) {
+            PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");
+            rc = proxyattn_budgets(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws), dws_bytes - H.ws,
+                                   at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), stream);
+            if (rc) { cleanup(); return rc; }
+        }
+        cc.row_begin = ch[c].first;
+        cc.row_end = ch[c].second;
+        cc.flags = cfg->flags | PROXYATTN_FLAG_KSTAR_GIVEN;
+        rc = proxyattn_estimate(&cc, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws), dws_bytes - H.ws,
+                                at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), at<int32_t>(dws, H.cnt),
+                                at<int32_t>(dws, H.idx), stream);
+        if (rc) { cleanup(); return rc; }
+        if (c == 0) PA_CUDA(cudaStreamWaitEvent(st, ev_v, 0), "wait");
+        cc.flags = cfg->flags;
+        rc = proxyattn_prefill(&cc, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.v),
+                               at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), at<char>(dws, H.o), stream);
+        if (rc) { cleanup(); return rc; }
+        PA_CUDA(cudaEventRecord(ev[3 + nc + c], st), "record");
+        PA_CUDA(cudaStreamWaitEvent(hs.down, ev[3 + nc + c], 0), "wait");
+        if ((rc = copy_rows(Oh, at<char>(dws, H.o), ch[c].first, ch[c].second, cudaMemcpyDeviceToHost, hs.down))) {
+            cleanup();
+            return rc;
+        }
+    }
     PA_CUDA(cudaEventRecord(ev_done, hs.down), "record");
     PA_CUDA(cudaStreamWaitEvent(st, ev_done, 0), "wait");
     if (kstar_h)
