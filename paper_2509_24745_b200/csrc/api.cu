@@ -504,8 +504,17 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
         want = e ? std::max(1, atoi(e)) : 16;
     }
     const int n_ch = std::max(1, std::min(want, units));
-    std::vector<std::pair<int, int>> ch;                  // [r0, r1) block rows, last rows first
-    for (int c = n_ch - 1; c >= 0; --c) {
+    // order: PROXYATTN_HOST_ORDER=fwd processes the FIRST rows first (K and the last Q block
+    // up front for Alg. 1, then V and Q chunk by chunk in row order: each chunk needs only the
+    // keys / values before its rows); the default processes the last (heaviest) rows first
+    static int fwd = -1;
+    if (fwd < 0) {
+        const char* e = getenv("PROXYATTN_HOST_ORDER");
+        fwd = (e && e[0] == 'f') ? 1 : 0;
+    }
+    std::vector<std::pair<int, int>> ch;                  // [r0, r1) block rows in processing order
+    for (int k = 0; k < n_ch; ++k) {
+        const int c = fwd ? k : n_ch - 1 - k;
         const int r0 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * c) / n_ch));
         const int r1 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * (c + 1)) / n_ch));
         if (r1 > r0) ch.emplace_back(r0, r1);
@@ -532,18 +541,40 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
         }
         return PROXYATTN_OK;
     };
-    // uploads: K, Q chunk 0 (the last rows), V, the other Q chunks
+    // value rows [t0, t1) of V (head-major [Hkv_l][N][d] or token-major)
+    auto copy_v = [&](int r0, int r1) -> int {
+        const long long t0 = static_cast<long long>(r0) * D.b, t1 = std::min<long long>(static_cast<long long>(r1) * D.b, D.N);
+        if (t1 <= t0) return PROXYATTN_OK;
+        if (D.tok) {
+            const size_t off = static_cast<size_t>(t0) * D.kv_ts * el, n = static_cast<size_t>(t1 - t0) * D.kv_ts * el;
+            PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v) + off, static_cast<const char*>(Vh) + off, n,
+                                    cudaMemcpyHostToDevice, hs.up), "H2D V rows");
+        } else {
+            const size_t pitch = static_cast<size_t>(D.N) * D.d * el, off = static_cast<size_t>(t0) * D.d * el;
+            PA_CUDA(cudaMemcpy2DAsync(at<char>(dws, H.v) + off, pitch, static_cast<const char*>(Vh) + off, pitch,
+                                      static_cast<size_t>(t1 - t0) * D.d * el, D.Hkvl, cudaMemcpyHostToDevice, hs.up),
+                    "H2D V rows");
+        }
+        return PROXYATTN_OK;
+    };
+    // uploads — reverse: K, Q chunk 0 (the last rows), V, the other Q chunks; forward: K, the
+    // last Q block (Alg. 1), then per chunk its V rows and Q rows
     PA_CUDA(cudaEventRecord(ev[0], st), "record");                 // after the caller's prior work
     PA_CUDA(cudaStreamWaitEvent(hs.up, ev[0], 0), "wait");
     PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, hs.up), "H2D K");
+    if (fwd && (rc = copy_rows(at<char>(dws, H.q), Qh, D.M - 1, D.M, cudaMemcpyHostToDevice, hs.up))) {
+        cleanup();
+        return rc;
+    }
     PA_CUDA(cudaEventRecord(ev_k, hs.up), "record");
     for (int c = 0; c < nc; ++c) {
+        if (fwd && (rc = copy_v(ch[c].first, ch[c].second))) { cleanup(); return rc; }
         if ((rc = copy_rows(at<char>(dws, H.q), Qh, ch[c].first, ch[c].second, cudaMemcpyHostToDevice, hs.up))) {
             cleanup();
             return rc;
         }
         PA_CUDA(cudaEventRecord(ev[3 + c], hs.up), "record");
-        if (c == 0) {
+        if (!fwd && c == 0) {
             PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, hs.up), "H2D V");
             PA_CUDA(cudaEventRecord(ev_v, hs.up), "record");
         }
@@ -553,10 +584,11 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     for (int c = 0; c < nc; ++c) {
         PA_CUDA(cudaStreamWaitEvent(st, c == 0 ? ev_k : ev[3 + c], 0), "wait");
         if (c == 0) {
-            PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");
+            if (!fwd) PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");   // the last rows' Q
             rc = proxyattn_budgets(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws), dws_bytes - H.ws,
                                    at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), stream);
             if (rc) { cleanup(); return rc; }
+            if (fwd) PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");      // the first chunk's V / Q
         }
         cc.row_begin = ch[c].first;
         cc.row_end = ch[c].second;
@@ -565,7 +597,7 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
                                 at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), at<int32_t>(dws, H.cnt),
                                 at<int32_t>(dws, H.idx), stream);
         if (rc) { cleanup(); return rc; }
-        if (c == 0) PA_CUDA(cudaStreamWaitEvent(st, ev_v, 0), "wait");
+        if (!fwd && c == 0) PA_CUDA(cudaStreamWaitEvent(st, ev_v, 0), "wait");
         cc.flags = cfg->flags;
         rc = proxyattn_prefill(&cc, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.v),
                                at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), at<char>(dws, H.o), stream);
