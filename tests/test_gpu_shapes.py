@@ -299,3 +299,28 @@ def test_block64_stride8_simt_estimation_fallback(d):
     cfg = cfg_of(d, 64, 2048, heads=(8, 2), stride=8)
     Q, K, V, _ = workloads.structured(8, 2, 2048, d, seed=120)
     run_staged(cfg, Q, K, V)
+
+
+@pytest.mark.parametrize("token_major", [False, True])
+@pytest.mark.parametrize("d,b", [(128, 128), (128, 64)])
+def test_forward_host_many_chunks_ragged(token_major, d, b):
+    # the host path's row-chunk pipeline with 16 chunks, a ragged last block, both layouts:
+    # bit-identical to estimate + prefill on device-resident tensors
+    N = 8192 + 37
+    cfg = cfg_of(d, b, N, heads=(8, 2))
+    Q, K, V, _ = workloads.structured(8, 2, N, d, seed=130)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    if token_major:
+        cfg = cfg.replace(token_major=True)
+        Q, K, V = (t.transpose(0, 1).contiguous() for t in (Q, K, V))
+    Qh, Kh, Vh = Q.pin_memory(), K.pin_memory(), V.pin_memory()
+    Oh = torch.empty_like(Qh).pin_memory()
+    ks = torch.empty(8, dtype=torch.int32).pin_memory()
+    ws = torch.empty(pa.forward_host_workspace_bytes(cfg), dtype=torch.uint8, device=DEV)
+    pa.forward_host(cfg, Qh, Kh, Vh, Oh, ws, ks)
+    torch.cuda.synchronize()
+    assert torch.equal(ks, kstar.cpu())
+    ref = O.cpu()
+    assert torch.equal(Oh.transpose(0, 1) if token_major else Oh, ref)
