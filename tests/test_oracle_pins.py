@@ -616,3 +616,42 @@ def test_ragged_n_sampled_rows_and_gamma_one_equals_dense():
     assert np.array_equal(Pq[0, 249], Q[:, 996].astype(np.float64).sum(0))
     est = oracle.pipeline(cfg, Q, K, V)
     assert np.max(np.abs(est["O"] - oracle.dense(cfg, Q, K, V))) <= 1e-12
+
+
+def _attention_recall(oc, Q, K, cnt, idx):
+    """Mean over (head, query) of the dense causal softmax mass that falls on the query's
+    selected blocks (keys k <= t in them), fp64 brute force."""
+    H, N, d = Q.shape
+    r, b = oc.n_q_heads // oc.n_kv_heads, oc.block_size
+    tot = 0.0
+    t = np.arange(N)
+    for h in range(H):
+        S = (Q[h].astype(np.float64) @ K[h // r].astype(np.float64).T) / math.sqrt(d)
+        S[t[:, None] < t[None, :]] = -np.inf
+        P = np.exp(S - S.max(axis=1, keepdims=True))
+        P /= P.sum(axis=1, keepdims=True)
+        keep = np.zeros((N, N), bool)
+        for m in range((N + b - 1) // b):
+            for n in idx[h, m, :cnt[h, m]]:
+                keep[m * b:(m + 1) * b, n * b:(n + 1) * b] = True
+        tot += float((P * keep).sum(axis=1).mean())
+    return tot / H
+
+
+def test_recall_under_budget_shared_focus():
+    # SPEC AC6 as a pin of the estimate's intent (§3.2: gamma is the attention mass the budget
+    # should cover): gamma = 0.95, stride 4, one proxy group, shared-focus multi-temperature
+    # inputs -> mean dense-attention recall of the selected blocks above SPEC's hard floor 0.85
+    # (measured 0.881 on this generator: Alg. 1 sizes K* on the LAST block's rows, earlier rows
+    # get the per-row ratio of Z12 and the proxy ranking, so recall sits a little below gamma;
+    # SPEC's 0.90 target is for its own workload); and recall grows with gamma (0.759 at 0.90)
+    N, Hq, Hkv, d, b = 2048, 8, 2, 64, 64
+    Q, K, V, _ = workloads.structured(Hq, Hkv, N, d, seed=3)
+    Qf, Kf = Q.float().numpy(), K.float().numpy()
+    rec = {}
+    for gamma in (0.9, 0.95):
+        oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, 1, gamma, round_bf16=True)
+        est = oracle.estimate(oc, Qf, Kf)
+        rec[gamma] = _attention_recall(oc, Qf, Kf, est["block_cnt"], est["block_idx"])
+    assert rec[0.95] >= 0.85, rec
+    assert rec[0.95] > rec[0.9], rec
