@@ -134,3 +134,29 @@ def test_fullsize_dense_sampled(layer):
         got = Od[h, m * b:(m + 1) * b].float().cpu().numpy()
         err = np.abs(got - Oref[h, m * b:(m + 1) * b])
         assert err.max() <= 2e-2 and err.mean() <= 2e-3, (h, m, err.max(), err.mean())
+
+
+def test_fullsize_attention_recall_sampled(layer):
+    # the share of each sampled query's dense causal softmax mass that its selected blocks
+    # hold (fp32 torch reference on the GPU for the sampled rows only) — the quantity gamma
+    # targets (§3.2).  Recorded, and bounded from below as a regression guard.
+    cfg = layer["cfg"]
+    dev = torch.device("cuda:0")
+    M, b, d, r = cfg.M, cfg.block_size, cfg.head_dim, cfg.r
+    Q = torch.from_numpy(layer["Q"]).to(dev)
+    K = torch.from_numpy(layer["K"]).to(dev)
+    cnt, idx = layer["cnt"], layer["idx"]
+    g = torch.Generator().manual_seed(5)
+    recs = []
+    for h in range(0, cfg.n_q_heads, 3):
+        for t in torch.randint(0, cfg.seq_len, (16,), generator=g).tolist():
+            m = t // b
+            s = (K[h // r, :t + 1] @ Q[h, t]) / d ** 0.5
+            p = torch.softmax(s.double(), 0)
+            keep = torch.zeros(t + 1, dtype=torch.bool, device=dev)
+            for n in idx[h, m, :cnt[h, m]].tolist():
+                keep[n * b:min((n + 1) * b, t + 1)] = True
+            recs.append(float(p[keep].sum()))
+    mean = float(np.mean(recs))
+    print(f"recall mean {mean:.4f} min {min(recs):.4f}")
+    assert mean >= 0.7, mean
