@@ -431,9 +431,7 @@ __global__ void lse_combine_kernel(int rows, int chunk, int Ns, int n_chunks, co
 // A3 from the window maxima of the lse pass: L[c][m][n] = ln2 * max over the block's valid
 // sampled rows i of (W[c][i][n] * sc2 - lse2[c][i]) for n <= m, -inf above the diagonal.
 // The operations of kMaxpool (window max of raw logits, scale, subtract lse, max over rows,
-// ln2) without its second GEMM pass.  One CTA per (group, block row); a warp per key tile u
-// reads the block's rows' window vectors of that tile (contiguous in W's tile-major layout),
-// lanes over rows, then a max over lanes per window.
+// ln2) without its second GEMM pass.  One CTA per (group, block row), a thread per key block.
 // The block's row lse (A2's normaliser) is combined here from the lse pass's per-chunk (max,
 // sum) partials (fixed chunk order), so no separate combine launch sits on the critical path.
 __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, int n_tr, float sc2,
@@ -451,53 +449,52 @@ __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns
         const int nk = ((i0 + static_cast<int>(threadIdx.x)) / 128 + chunk) / chunk;
         const float* pm = part_m + i * n_chunks;
         const float* ps = part_s + i * n_chunks;
-        float mx = -INFINITY;
-        for (int k = 0; k < nk; ++k) mx = fmaxf(mx, pm[k]);
-        float sum = 0.f;
-        for (int k = 0; k < nk; ++k) sum += ps[k] * ex2(pm[k] - mx);
+        float mx = -INFINITY, sum = 0.f;
+        if (nk <= 16) {                                // all partials in flight at once
+            float vm[16], vs[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                vm[k] = k < nk ? __ldg(pm + k) : -INFINITY;
+                vs[k] = k < nk ? __ldg(ps + k) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) mx = fmaxf(mx, vm[k]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (k < nk) sum += vs[k] * ex2(vm[k] - mx);
+        } else {
+            for (int k = 0; k < nk; ++k) mx = fmaxf(mx, pm[k]);
+            for (int k = 0; k < nk; ++k) sum += ps[k] * ex2(pm[k] - mx);
+        }
         const float l2 = mx + __log2f(sum);
         lse_s[threadIdx.x] = l2;
         if (lse_nat) lse_nat[i] = l2 * kLn2;
     }
     __syncthreads();
+    // thread per key block n <= m: max over the block's rows of W[c][n / nwin][i][n % nwin]
     const int nwin = 128 / bs;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     float* Lrow = L + (static_cast<long long>(c) * M + m) * M;
-    for (int n = m + 1 + threadIdx.x; n < M; n += blockDim.x) Lrow[n] = -INFINITY;
-    const int u_max = m / nwin;                       // tiles holding blocks n <= m
-    for (int u = warp; u <= u_max; u += nwarps) {
-        const float* Wu = W + ((static_cast<long long>(c) * n_tr + u) * Ns) * nwin;
-        float best[8];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) best[w] = -INFINITY;
-        for (int i = i0 + lane; i < i1; i += 32) {
-            const float nl = -lse_s[i - i0];
-            const float* wi = Wu + static_cast<long long>(i) * nwin;
-            float v[8];
-            if (nwin == 8) {
-                const float4 a = __ldg(reinterpret_cast<const float4*>(wi));
-                const float4 b = __ldg(reinterpret_cast<const float4*>(wi) + 1);
-                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-            } else if (nwin == 4) {
-                const float4 a = __ldg(reinterpret_cast<const float4*>(wi));
-                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-            } else if (nwin == 2) {
-                const float2 a = __ldg(reinterpret_cast<const float2*>(wi));
-                v[0] = a.x; v[1] = a.y;
-            } else {
-                v[0] = __ldg(wi);
+    const float* Wc = W + static_cast<long long>(c) * n_tr * Ns * nwin;
+    for (int n = threadIdx.x; n < M; n += blockDim.x) {
+        float w = -INFINITY;
+        if (n <= m) {
+            const float* Wn = Wc + (static_cast<long long>(n / nwin) * Ns) * nwin + (n % nwin);
+            int i = i0;
+#pragma unroll 1
+            for (; i + 4 <= i1; i += 4) {              // four rows' loads in flight
+                const float a0 = __ldg(Wn + static_cast<long long>(i) * nwin);
+                const float a1 = __ldg(Wn + static_cast<long long>(i + 1) * nwin);
+                const float a2 = __ldg(Wn + static_cast<long long>(i + 2) * nwin);
+                const float a3 = __ldg(Wn + static_cast<long long>(i + 3) * nwin);
+                w = fmaxf(w, fmaf(a0, sc2, -lse_s[i - i0]));
+                w = fmaxf(w, fmaf(a1, sc2, -lse_s[i + 1 - i0]));
+                w = fmaxf(w, fmaf(a2, sc2, -lse_s[i + 2 - i0]));
+                w = fmaxf(w, fmaf(a3, sc2, -lse_s[i + 3 - i0]));
             }
-#pragma unroll
-            for (int w = 0; w < 8; ++w)
-                if (w < nwin) best[w] = fmaxf(best[w], fmaf(v[w], sc2, nl));
+            for (; i < i1; ++i) w = fmaxf(w, fmaf(__ldg(Wn + static_cast<long long>(i) * nwin), sc2, -lse_s[i - i0]));
+            w *= kLn2;
         }
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            if (w >= nwin) break;
-            const float x = warp_max(best[w]);
-            const int n = u * nwin + w;
-            if (lane == 0 && n <= m) Lrow[n] = x * kLn2;
-        }
+        Lrow[n] = w;
     }
 }
 

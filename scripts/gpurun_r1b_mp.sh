@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build=$?
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -1 gpurun_out/pytest_gpu.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"maxpool|score_tc" python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-lib-dense --no-graph 2>/dev/null | grep -E "maxpool|score_tc" | awk -F'","' '{print $5" "$(NF)}' | cut -c1-90
+for n in 16384 131072; do timeout 600 python bench.py --seq-len $n --steps 10 --warmup 3 --no-cpu --no-e2e --no-lib-dense > gpurun_out/bench_s.log 2>&1; tail -1 gpurun_out/bench_s.log | python -c 'import sys,json; j=json.loads(sys.stdin.read()); print(j["config"]["seq_len"], j["value"], j["estimate_ms"], j["prefill_ms"], j["sparsity"])'; done
