@@ -3,21 +3,23 @@
 //
 //   A2  proxy_lse     Eq. 1 softmax normaliser of the proxy logits over the sampled causal
 //                     keys (Z4): per (sampled row, key chunk) online (max, sum) in
-//                     log2 units, combined per row afterwards -> lse2[c][i].
-//   A3  proxy_maxpool Eq. 1 max-pool (Z6): L[c][m][n] = max over the 32 x 32
-//                     sampled window of z_ij - lse_i (b/s = 32 rows = one warp's TMEM lanes,
-//                     so the row-window max is a warp reduction).
+//                     log2 units; the same pass stores each row's window maxima W (the
+//                     raw-logit max over the b/s sampled keys of every key block).
+//   A3  max-pool      Eq. 1 max-pool (Z6): maxpool_from_windows_kernel combines the
+//                     rows' chunk partials into lse and takes L[c][m][n] = max over the block
+//                     row's sampled rows of (W - lse), no second GEMM pass.
 //   A4  budget        Alg. 1 line 1-2 (Z7, Z8): per head, last block's b queries
 //                     against every key block: per (row t, block n) max m_tn and
 //                     s_tn = sum_k exp2(x_tk - m_tn); combined + sorted afterwards.  With
 //                     b = 64 the A tile's rows 64-127 are padding and each 128-key tile
 //                     holds two key blocks (one partial per 64-column half).
 //
-// All three share one warp-specialised tile engine (192 threads):
+// Both passes share one warp-specialised tile engine (320 threads, 2 CTAs / SM):
 //   warp 0 TMA producer (A tile once, then 128-key B tiles into a 2-stage ring),
 //   warp 1 TMEM allocator + single-thread tcgen05.mma issuer (S = A B^T, K = d,
 //          SS operands K-major SWIZZLE_128B, fp32 accumulators double-buffered in TMEM),
-//   warps 2-5 epilogue: thread = tile row (TMEM lane), tcgen05.ld 128 columns, mode math.
+//   warps 2-5 / 6-9 two epilogue warpgroups, one per S buffer (even / odd tiles): thread =
+//          tile row (TMEM lane), the tile read in two 64-column halves, mode math.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -33,10 +35,10 @@ namespace {
 constexpr int kBox = 128 * 64 * 2;   // one [128 rows][64 bf16] SWIZZLE_128B box
 constexpr int kTile = 2 * kBox;      // 128 x 128 bf16
 constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // TMA warp, MMA warp, two epilogue warpgroups
 constexpr int kChunk = 16;           // default key tiles per CTA (proxy / budget)
 
-enum Mode { kLse = 0, kMaxpool = 1, kBudget = 2 };
+enum Mode { kLse = 0, kBudget = 2 };
 
 struct __align__(8) SBars {
     uint64_t a_full;
@@ -45,7 +47,8 @@ struct __align__(8) SBars {
     uint64_t s_full[2];
     uint64_t s_empty[2];
     uint32_t tmem_base;
-    float red[4][2];        // MAXPOOL, bs >= 64: per lane-quarter window maxima
+    float red_m[128];       // LSE: the second epilogue warpgroup's (max, sum) per row
+    float red_s[128];
 };
 constexpr size_t kSmem = 1024 + kTile * (1 + kStages) + sizeof(SBars);
 
@@ -65,8 +68,6 @@ struct ScoreParams {
     float sc2;       // logit scale in log2 units
     float* part_m;   // LSE: [gl][Ns][n_chunks]; BUDGET: [Hl][M][128]
     float* part_s;
-    const float* lse2;  // MAXPOOL: [gl][Ns] (log2 units)
-    float* L;           // MAXPOOL: [gl][M][M] (natural log)
     float* W;           // LSE (optional): [gl][n_tr][Ns][nwin] raw-logit max of each row over
                         // the bs sampled keys of block n = u * nwin + w of key tile u (causal
                         // mask applied); tile-major so a warp's store of its 32 rows' windows
@@ -178,224 +179,156 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
         }
     } else {
+        // Two epilogue warpgroups (warps 2-5 and 6-9), one per S buffer: warpgroup e takes the
+        // tiles j with j % 2 == e.  A thread is a tile row (TMEM lane); a tile's 128 columns are
+        // read in two 64-column halves, which keeps a thread within the register budget of two
+        // warpgroups (16 epilogue warps per SM at 2 CTAs) to hide the MUFU / FMNMX latencies.
+        const int eg = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int rr = quarter * 32 + lane;                  // tile row
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-        float m_run = -INFINITY, s_run = 0.f;
+        float m_run = -INFINITY, s_run = 0.f;                // kLse: online (max, sum), log2 units
         // diagonal tile: key column c is masked when c > rr + diag_off (key position past the
         // query's); 0 except in the b = 64 budget pass, where the last block can sit in the
         // second half of its 128-key tile (diag_off = 64)
         const int diag_off = kB64 && p.mode == kBudget ? a_row - diag_u * 128 : 0;
-        float lse_row = 0.f;
         // rows past the end (partial last tile / block): padded, excluded from every output
         const bool row_ok = (p.mode == kBudget) ? (rr < p.b && a_row + rr < p.N) : (tr * 128 + rr < p.Ns);
-        if (p.mode == kMaxpool)
-            lse_row = row_ok ? p.lse2[static_cast<long long>(prob) * p.Ns + tr * 128 + rr] : INFINITY;
-        for (int j = 0; j < nt; ++j) {
+        const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
+        for (int j = eg; j < nt; j += 2) {
             const int u = u_begin + j;
-            mbar_wait(&bars->s_full[j & 1], (j >> 1) & 1);
+            mbar_wait(&bars->s_full[eg], (j >> 1) & 1);
             tc_fence_after();
-            uint32_t raw[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tbase + lane_off + (j & 1) * 128 + c * 32, raw[c]);
-            tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&bars->s_empty[j & 1]);
             const bool diag = (u == diag_u);
-            if (p.mode == kMaxpool) {
-                // Eq. 1 max-pool over (bs x bs) windows, bs = b/s sampled rows/keys per block
-                // (16, 32, 64 or 128): max of the raw logits over each 16-column group first
-                // (the scale is positive), then over the bs columns of a window, then over the
-                // bs rows of the block (lanes / warps), then scale and subtract lse.
-                float h8[8];
+            float h8[8];                                     // 16-column group maxima (raw logits)
+            float tm[2], ac[2];                              // budget: per-half max (log2) and sum
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    float w2[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int col = g * 16 + e;
-                        const float x = (diag && col > rr) ? -INFINITY
-                                                           : __uint_as_float(raw[col >> 5][col & 31]);
-                        w2[e & 1] = fmaxf(w2[e & 1], x);
-                    }
-                    h8[g] = fmaxf(w2[0], w2[1]);
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t raw[2][32];
+                tmem_ld32(tbase + lane_off + eg * 128 + hf * 64, raw[0]);
+                tmem_ld32(tbase + lane_off + eg * 128 + hf * 64 + 32, raw[1]);
+                tmem_ld_wait();
+                if (hf == 1) {                               // S read out: the next MMA may reuse it
+                    tc_fence_before();
+                    mbar_arrive(&bars->s_empty[eg]);
                 }
-                const int nwin = 128 / p.bs;                 // windows (block columns) per tile
-                float win[8];                                // window maxima (first nwin valid)
+                if (diag) {
+                    const int thr = rr + diag_off - hf * 64;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > thr) raw[c][e] = 0xff800000u;   // -inf
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    float m2[2] = {__uint_as_float(raw[g >> 1][(g & 1) * 16]),
+                                   __uint_as_float(raw[g >> 1][(g & 1) * 16 + 1])};
+#pragma unroll
+                    for (int e = 2; e < 16; ++e)
+                        m2[e & 1] = fmaxf(m2[e & 1], __uint_as_float(raw[g >> 1][(g & 1) * 16 + e]));
+                    h8[hf * 4 + g] = fmaxf(m2[0], m2[1]);
+                }
+                const float hmax = fmaxf(fmaxf(h8[hf * 4], h8[hf * 4 + 1]), fmaxf(h8[hf * 4 + 2], h8[hf * 4 + 3])) * p.sc2;
+                // exps of the half relative to ref (log2 units)
+                const float ref = (p.mode == kLse) ? fmaxf(m_run, hmax) : hmax;
+                float acc = 0.f;
+                if (ref > -INFINITY) {
+                    const uint64_t nref = f2_pack(-ref, -ref);
+                    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const int e0 = 2 * q;
+                        const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
+                                                           __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
+                                                   sc2, nref);
+                        float e0v, e1v;
+                        if ((q & 3) < kEmu) {
+                            ex2_poly2_d4(x2, e0v, e1v);
+                        } else {
+                            float x0, x1;
+                            f2_unpack(x2, x0, x1);
+                            e0v = ex2(x0);
+                            e1v = ex2(x1);
+                        }
+                        acc2[q & 3] = f2_add(acc2[q & 3], f2_pack(e0v, e1v));
+                    }
+                    float a0, a1;
+                    f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
+                    acc = a0 + a1;
+                }
+                if (p.mode == kLse) {
+                    if (ref > -INFINITY) {
+                        s_run = (m_run > -INFINITY ? s_run * ex2(m_run - ref) : 0.f) + acc;
+                        m_run = ref;
+                    }
+                } else if (kB64) {                          // b = 64: the half is key block 2u + hf
+                    const int n = 2 * u + hf;
+                    if (n < p.M) {
+                        const long long o = (static_cast<long long>(prob) * p.M + n) * 128 + rr;
+                        const bool ok = row_ok && hmax > -INFINITY;
+                        p.part_m[o] = ok ? hmax : -INFINITY;   // padded rows carry no mass
+                        p.part_s[o] = ok ? acc : 0.f;
+                    }
+                } else {
+                    tm[hf] = hmax;
+                    ac[hf] = acc;
+                }
+            }
+            if (p.mode == kBudget && !kB64) {               // b = 128: the tile is key block u
+                const float mm = fmaxf(tm[0], tm[1]);
+                float ss = 0.f;
+                if (mm > -INFINITY) {
+                    ss = (tm[0] > -INFINITY ? ac[0] * ex2(tm[0] - mm) : 0.f) +
+                         (tm[1] > -INFINITY ? ac[1] * ex2(tm[1] - mm) : 0.f);
+                }
+                const long long o = (static_cast<long long>(prob) * p.M + u) * 128 + rr;
+                p.part_m[o] = row_ok ? mm : -INFINITY;       // padded rows carry no mass
+                p.part_s[o] = row_ok ? ss : 0.f;
+            }
+            if (p.mode == kLse && p.W != nullptr && row_ok) {
+                // A3 by-product: the window maxima (16-column groups folded to b/s columns);
+                // the max-pool itself runs afterwards from W and the row lse
+                const int nwin = 128 / p.bs;
+                float* wrow = p.W + ((static_cast<long long>(prob) * p.n_tr + u) * p.Ns + tr * 128 + rr) * nwin;
+                float win[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
                     win[c] = p.bs == 16 ? h8[c]
                            : p.bs == 32 ? fmaxf(h8[(2 * c) & 7], h8[(2 * c + 1) & 7])
                            : p.bs == 64 ? fmaxf(fmaxf(h8[(4 * c) & 7], h8[(4 * c + 1) & 7]),
                                                 fmaxf(h8[(4 * c + 2) & 7], h8[(4 * c + 3) & 7]))
                                         : fmaxf(fmaxf(fmaxf(h8[0], h8[1]), fmaxf(h8[2], h8[3])),
                                                 fmaxf(fmaxf(h8[4], h8[5]), fmaxf(h8[6], h8[7])));
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (c >= nwin) break;
-                    float w = win[c] * p.sc2 - lse_row;
-                    const int n = u * nwin + c;
-                    if (p.bs == 16) {                        // block rows = half warps
-#pragma unroll
-                        for (int o = 8; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
-                        if ((lane & 15) == 0) {
-                            const int m = tr * 8 + quarter * 2 + (lane >> 4);
-                            if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
-                        }
-                    } else {
-                        w = warp_max(w);
-                        if (p.bs == 32) {
-                            if (lane == 0) {
-                                const int m = tr * 4 + quarter;
-                                if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
-                            }
-                        } else {                              // 64 / 128: combine warps in smem
-                            if (lane == 0) bars->red[quarter][c] = w;
-                        }
-                    }
-                }
-                if (p.bs >= 64) {
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    const int wpb = p.bs / 32;               // warps (lane quarters) per block row
-                    if (threadIdx.x % 32 == 0 && (quarter % wpb) == 0) {
-                        for (int c = 0; c < nwin; ++c) {   // nwin <= 2 here
-                            float w = -INFINITY;
-                            for (int q = quarter; q < quarter + wpb; ++q) w = fmaxf(w, bars->red[q][c]);
-                            const int m = tr * nwin + quarter / wpb, n = u * nwin + c;
-                            if (m < p.M && n < p.M) p.L[(static_cast<long long>(prob) * p.M + m) * p.M + n] = w * kLn2;
-                        }
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                }
-            } else {
-                // raw logits; causal mask inside the diagonal tile (key position > query
-                // position); 8 independent max chains
-                if (diag) {
-                    const int thr = rr + diag_off;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (c * 32 + e > thr) raw[c][e] = 0xff800000u;  // -inf
-                }
-                if (kB64 && p.mode == kBudget) {
-                    // two key blocks per tile: (max, sum) of each 64-column half
-#pragma unroll
-                    for (int hb = 0; hb < 2; ++hb) {
-                        float mx[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) mx[k] = __uint_as_float(raw[2 * hb][k]);
-#pragma unroll
-                        for (int c = 2 * hb; c < 2 * hb + 2; ++c)
-#pragma unroll
-                            for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(raw[c][e]));
-                        const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.sc2;
-                        float acc = 0.f;
-                        if (tmax > -INFINITY) {
-                            const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
-                            const uint64_t nref = f2_pack(-tmax, -tmax);
-                            uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-                            for (int c = 0; c < 32; ++c) {
-                                const int e0 = 64 * hb + 2 * c;
-                                const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
-                                                                   __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
-                                                           sc2, nref);
-                                float x0, x1;
-                                f2_unpack(x2, x0, x1);
-                                acc2[c & 3] = f2_add(acc2[c & 3], f2_pack(ex2(x0), ex2(x1)));
-                            }
-                            float a0, a1;
-                            f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
-                            acc = a0 + a1;
-                        }
-                        const int n = 2 * u + hb;
-                        if (n < p.M) {
-                            const long long o = (static_cast<long long>(prob) * p.M + n) * 128 + rr;
-                            const bool ok = row_ok && tmax > -INFINITY;
-                            p.part_m[o] = ok ? tmax : -INFINITY;   // padded rows carry no mass
-                            p.part_s[o] = ok ? acc : 0.f;
-                        }
-                    }
-                    continue;
-                }
-                float mx[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) mx[k] = __uint_as_float(raw[k >> 1][(k & 1) * 16]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        mx[c * 2 + (e >> 4)] = fmaxf(mx[c * 2 + (e >> 4)], __uint_as_float(raw[c][e]));
-                if (p.mode == kLse && p.W != nullptr && row_ok) {
-                    // A3 by-product: mx[k] is the max of 16-column group k, so the window
-                    // maxima of A3 are folds of it; the max-pool itself runs afterwards
-                    // from W and lse (maxpool_from_windows_kernel), bit-identical to kMaxpool
-                    const int nwin = 128 / p.bs;
-                    float* wrow = p.W + ((static_cast<long long>(prob) * p.n_tr + u) * p.Ns + tr * 128 + rr) * nwin;
-                    float win[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        win[c] = p.bs == 16 ? mx[c]
-                               : p.bs == 32 ? fmaxf(mx[(2 * c) & 7], mx[(2 * c + 1) & 7])
-                               : p.bs == 64 ? fmaxf(fmaxf(mx[(4 * c) & 7], mx[(4 * c + 1) & 7]),
-                                                    fmaxf(mx[(4 * c + 2) & 7], mx[(4 * c + 3) & 7]))
-                                            : fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                                    fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-                    if (nwin == 8) {
-                        reinterpret_cast<float4*>(wrow)[0] = make_float4(win[0], win[1], win[2], win[3]);
-                        reinterpret_cast<float4*>(wrow)[1] = make_float4(win[4], win[5], win[6], win[7]);
-                    } else if (nwin == 4) {
-                        *reinterpret_cast<float4*>(wrow) = make_float4(win[0], win[1], win[2], win[3]);
-                    } else if (nwin == 2) {
-                        *reinterpret_cast<float2*>(wrow) = make_float2(win[0], win[1]);
-                    } else {
-                        *wrow = win[0];
-                    }
-                }
-                const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.sc2;
-                const float ref = (p.mode == kLse) ? fmaxf(m_run, tmax) : tmax;
-                const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
-                const uint64_t nref = f2_pack(-ref, -ref);
-                uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const int e0 = 2 * c;
-                    const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(raw[e0 >> 5][e0 & 31]),
-                                                       __uint_as_float(raw[e0 >> 5][(e0 & 31) + 1])),
-                                               sc2, nref);
-                    float e0v, e1v;
-                    if ((c & 3) < kEmu) {
-                        ex2_poly2_d4(x2, e0v, e1v);
-                    } else {
-                        float x0, x1;
-                        f2_unpack(x2, x0, x1);
-                        e0v = ex2(x0);
-                        e1v = ex2(x1);
-                    }
-                    acc2[c & 3] = f2_add(acc2[c & 3], f2_pack(e0v, e1v));
-                }
-                float a0, a1;
-                f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
-                const float acc = a0 + a1;
-                if (p.mode == kLse) {
-                    s_run = s_run * ex2(m_run - ref) + acc;
-                    m_run = ref;
+                if (nwin == 8) {
+                    reinterpret_cast<float4*>(wrow)[0] = make_float4(win[0], win[1], win[2], win[3]);
+                    reinterpret_cast<float4*>(wrow)[1] = make_float4(win[4], win[5], win[6], win[7]);
+                } else if (nwin == 4) {
+                    *reinterpret_cast<float4*>(wrow) = make_float4(win[0], win[1], win[2], win[3]);
+                } else if (nwin == 2) {
+                    *reinterpret_cast<float2*>(wrow) = make_float2(win[0], win[1]);
                 } else {
-                    const long long o = (static_cast<long long>(prob) * p.M + u) * 128 + rr;
-                    p.part_m[o] = row_ok ? tmax : -INFINITY;   // padded rows carry no mass
-                    p.part_s[o] = row_ok ? acc : 0.f;
+                    *wrow = win[0];
                 }
             }
         }
-        if (p.mode == kLse && row_ok) {
-            const int k = u_begin / p.chunk;
-            const long long o =
-                (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.n_chunks + k;
-            p.part_m[o] = m_run;
-            p.part_s[o] = s_run;
+        if (p.mode == kLse) {
+            // the two warpgroups' (max, sum) of each row -> one partial (fixed order: WG0 then WG1)
+            if (eg == 1) {
+                bars->red_m[rr] = m_run;
+                bars->red_s[rr] = s_run;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (eg == 0 && row_ok) {
+                const float m1 = bars->red_m[rr], s1 = bars->red_s[rr];
+                const float mm = fmaxf(m_run, m1);
+                const float ss = (m_run > -INFINITY ? s_run * ex2(m_run - mm) : 0.f) +
+                                 (m1 > -INFINITY ? s1 * ex2(m1 - mm) : 0.f);
+                const int k = u_begin / p.chunk;
+                const long long o = (static_cast<long long>(prob) * p.Ns + tr * 128 + rr) * p.n_chunks + k;
+                p.part_m[o] = mm;
+                p.part_s[o] = ss;
+            }
         }
     }
     tc_fence_before();
@@ -407,31 +340,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 }
 
-// lse2[c][i] = m* + log2(sum_k s_k 2^(m_k - m*)) over the row's chunks (fixed order).
-__global__ void lse_combine_kernel(int rows, int chunk, int Ns, int n_chunks, const float* part_m,
-                                   const float* part_s, float* lse2, float* lse_nat, int i0, int i1) {
-    // rows [i0, i1) of every group (row-range estimate); rows = groups * (i1 - i0)
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= rows) return;
-    const long long i = (t / (i1 - i0)) * Ns + i0 + t % (i1 - i0);
-    const int row_in_group = static_cast<int>(i % Ns);
-    const int tr = row_in_group / 128;
-    const int nk = (tr + chunk) / chunk;     // chunks that exist for this tile row
-    const float* pm = part_m + i * n_chunks;
-    const float* ps = part_s + i * n_chunks;
-    float mx = -INFINITY;
-    for (int k = 0; k < nk; ++k) mx = fmaxf(mx, pm[k]);
-    float s = 0.f;
-    for (int k = 0; k < nk; ++k) s += ps[k] * ex2(pm[k] - mx);
-    const float l2 = mx + __log2f(s);
-    lse2[i] = l2;
-    if (lse_nat) lse_nat[i] = l2 * kLn2;
-}
 
 // A3 from the window maxima of the lse pass: L[c][m][n] = ln2 * max over the block's valid
 // sampled rows i of (W[c][i][n] * sc2 - lse2[c][i]) for n <= m, -inf above the diagonal.
-// The operations of kMaxpool (window max of raw logits, scale, subtract lse, max over rows,
-// ln2) without its second GEMM pass.  One CTA per (group, block row), a thread per key block.
+// The operations of a second max-pool GEMM pass (window max of raw logits, scale, subtract lse,
+// max over rows, ln2) without the pass.  One CTA per (group, block row), a thread per key block.
 // The block's row lse (A2's normaliser) is combined here from the lse pass's per-chunk (max,
 // sum) partials (fixed chunk order), so no separate combine launch sits on the critical path.
 __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns, int bs, int n_tr, float sc2,
@@ -444,7 +357,7 @@ __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns
     __shared__ float lse_s[128];
     const int m = rb + blockIdx.x % (re - rb), c = blockIdx.x / (re - rb);   // block rows [rb, re)
     const int i0 = m * bs, i1 = min(i0 + bs, Ns);
-    if (threadIdx.x < i1 - i0) {                       // lse2 of the block's rows (lse_combine's formula)
+    if (threadIdx.x < i1 - i0) {                       // lse2 of the block's rows from the chunk partials
         const long long i = static_cast<long long>(c) * Ns + i0 + threadIdx.x;
         const int nk = ((i0 + static_cast<int>(threadIdx.x)) / 128 + chunk) / chunk;
         const float* pm = part_m + i * n_chunks;
@@ -498,10 +411,6 @@ __global__ void __launch_bounds__(256) maxpool_from_windows_kernel(int M, int Ns
     }
 }
 
-__global__ void fill_neg_inf_kernel(float* L, long long n) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) L[i] = -INFINITY;
-}
 
 // Alg. 1 lines 1-2 from the per-(block u, row t) partials (m_tu, s_tu) of the budget pass,
 // in two grid-wide phases (the single-CTA-per-head version left 116 of 148 SMs idle):
@@ -590,8 +499,6 @@ int score_emu() {
     return v;
 }
 
-// PROXYATTN_MAXPOOL_PASS=1: A3 as a second tcgen05 pass (kMaxpool) instead of from the
-// window maxima the lse pass stores (diagnostics / comparison only).
 // Key tiles per CTA of the score passes; PROXYATTN_SCORE_CHUNK=16/32/64 overrides.
 // Key tiles per CTA of the proxy (A2) pass: the default unless the causal grid of this
 // config would leave the GPU under-filled (short N), then the largest of 8 / 4 / 2 that gives
@@ -620,14 +527,6 @@ int score_chunk() {
     return v;
 }
 
-bool maxpool_pass() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PROXYATTN_MAXPOOL_PASS");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
 
@@ -707,29 +606,15 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.part_s = part_s;
     // W: 32-byte aligned (its rows are stored as float4 / float2 vectors)
     const uintptr_t w_addr = reinterpret_cast<uintptr_t>(lse2 + static_cast<size_t>(D.gl) * D.Ns);
-    p.W = maxpool_pass() ? nullptr : reinterpret_cast<float*>((w_addr + 31) & ~static_cast<uintptr_t>(31));
+    p.W = reinterpret_cast<float*>((w_addr + 31) & ~static_cast<uintptr_t>(31));
     const unsigned grid = static_cast<unsigned>(D.gl) * (p.tr_hi - p.tr_lo) * p.n_chunks;
     p.mode = kLse;
     score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (!maxpool_pass()) {   // lse combine fused into the max-pool (rows of the block rows)
-        maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
-            D.M, p.Ns, p.bs, p.n_tr, p.sc2, p.W, part_m, part_s, p.chunk, p.n_chunks, lse_nat, L, D.rb, D.re);
-        return cudaGetLastError();
-    }
-    const int i0 = p.tr_lo * 128, i1 = static_cast<int>(p.tr_hi * 128 < D.Ns ? p.tr_hi * 128 : D.Ns);
-    const long long rws = static_cast<long long>(D.gl) * (i1 - i0);
-    lse_combine_kernel<<<static_cast<unsigned>((rws + 255) / 256), 256, 0, st>>>(
-        static_cast<int>(rws), p.chunk, p.Ns, p.n_chunks, part_m, part_s, lse2, lse_nat, i0, i1);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const long long cells = static_cast<long long>(D.gl) * D.M * D.M;
-    fill_neg_inf_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(L, cells);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    p.mode = kMaxpool;
-    p.lse2 = lse2;
-    p.L = L;
-    score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    // A3: the max-pool (with the row lse combine) from the window maxima, block rows [rb, re)
+    maxpool_from_windows_kernel<<<static_cast<unsigned>(D.gl) * (D.re - D.rb), 256, 0, st>>>(
+        D.M, p.Ns, p.bs, p.n_tr, p.sc2, p.W, part_m, part_s, p.chunk, p.n_chunks, lse_nat, L, D.rb, D.re);
     return cudaGetLastError();
 }
 
