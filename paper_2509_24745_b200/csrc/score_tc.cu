@@ -76,7 +76,7 @@ struct ScoreParams {
 
 // kEmu: of every 4 column pairs, kEmu use the FMA-pipe exp2 (degree 4); kB64: budget pass
 // with b = 64 (two key blocks per 128-key tile); kD: head dim (K of the MMAs)
-template <int kEmu, bool kB64, int kD>
+template <int kEmu, bool kB64, int kD, int kMode>
 __global__ void __launch_bounds__(kThreads, 2)
 score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 ScoreParams p) {
@@ -84,7 +84,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int a_row, b_row0, u_begin, u_end, diag_u, prob;  // prob: group (proxy) / local head
     int a_head = 0, b_head = 0;                        // budget: 3-D maps (any Q/K layout)
     int tr = 0;                                        // proxy tile row
-    if (p.mode == kBudget) {
+    if (kMode == kBudget) {
         prob = blockIdx.x / p.n_chunks;
         const int k = blockIdx.x % p.n_chunks;
         u_begin = k * p.chunk;
@@ -142,7 +142,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tma_prefetch(&tmA);
             tma_prefetch(&tmB);
             auto load = [&](uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int col, int row, int head) {
-                if (p.mode == kBudget) tma_load_3d(dst, map, bar, col, row, head);
+                if (kMode == kBudget) tma_load_3d(dst, map, bar, col, row, head);
                 else tma_load_2d(dst, map, bar, col, row);
             };
             constexpr int nbox = kD / 64;
@@ -191,9 +191,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // diagonal tile: key column c is masked when c > rr + diag_off (key position past the
         // query's); 0 except in the b = 64 budget pass, where the last block can sit in the
         // second half of its 128-key tile (diag_off = 64)
-        const int diag_off = kB64 && p.mode == kBudget ? a_row - diag_u * 128 : 0;
+        const int diag_off = kB64 && kMode == kBudget ? a_row - diag_u * 128 : 0;
         // rows past the end (partial last tile / block): padded, excluded from every output
-        const bool row_ok = (p.mode == kBudget) ? (rr < p.b && a_row + rr < p.N) : (tr * 128 + rr < p.Ns);
+        const bool row_ok = (kMode == kBudget) ? (rr < p.b && a_row + rr < p.N) : (tr * 128 + rr < p.Ns);
         const uint64_t sc2 = f2_pack(p.sc2, p.sc2);
         for (int j = eg; j < nt; j += 2) {
             const int u = u_begin + j;
@@ -231,7 +231,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 const float hmax = fmaxf(fmaxf(h8[hf * 4], h8[hf * 4 + 1]), fmaxf(h8[hf * 4 + 2], h8[hf * 4 + 3])) * p.sc2;
                 // exps of the half relative to ref (log2 units)
-                const float ref = (p.mode == kLse) ? fmaxf(m_run, hmax) : hmax;
+                const float ref = (kMode == kLse) ? fmaxf(m_run, hmax) : hmax;
                 float acc = 0.f;
                 if (ref > -INFINITY) {
                     const uint64_t nref = f2_pack(-ref, -ref);
@@ -257,7 +257,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), a0, a1);
                     acc = a0 + a1;
                 }
-                if (p.mode == kLse) {
+                if (kMode == kLse) {
                     if (ref > -INFINITY) {
                         s_run = (m_run > -INFINITY ? s_run * ex2(m_run - ref) : 0.f) + acc;
                         m_run = ref;
@@ -275,7 +275,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     ac[hf] = acc;
                 }
             }
-            if (p.mode == kBudget && !kB64) {               // b = 128: the tile is key block u
+            if (kMode == kBudget && !kB64) {                // b = 128: the tile is key block u
                 const float mm = fmaxf(tm[0], tm[1]);
                 float ss = 0.f;
                 if (mm > -INFINITY) {
@@ -286,7 +286,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 p.part_m[o] = row_ok ? mm : -INFINITY;       // padded rows carry no mass
                 p.part_s[o] = row_ok ? ss : 0.f;
             }
-            if (p.mode == kLse && p.W != nullptr && row_ok) {
+            if (kMode == kLse && p.W != nullptr && row_ok) {
                 // A3 by-product: the window maxima (16-column groups folded to b/s columns);
                 // the max-pool itself runs afterwards from W and the row lse
                 const int nwin = 128 / p.bs;
@@ -312,7 +312,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             }
         }
-        if (p.mode == kLse) {
+        if (kMode == kLse) {
             // the two warpgroups' (max, sum) of each row -> one partial (fixed order: WG0 then WG1)
             if (eg == 1) {
                 bars->red_m[rr] = m_run;
@@ -530,22 +530,27 @@ int score_chunk() {
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
 
-ScoreKernel score_kernel(int d, bool b64 = false) {
-    if (d == 64) return b64 ? score_tc_kernel<0, true, 64> : score_tc_kernel<0, false, 64>;
-    if (b64) return score_tc_kernel<0, true, 128>;
-    const int e = score_emu();
-    return e == 0 ? score_tc_kernel<0, false, 128> : e == 1 ? score_tc_kernel<1, false, 128>
-         : e == 2 ? score_tc_kernel<2, false, 128> : score_tc_kernel<3, false, 128>;
+// mode: kLse (the A2 pass) or kBudget (Alg. 1; b64 = block size 64)
+ScoreKernel score_kernel(int d, int mode, bool b64 = false) {
+    if (mode == kLse) {
+        if (d == 64) return score_tc_kernel<0, false, 64, kLse>;
+        const int e = score_emu();
+        return e == 0 ? score_tc_kernel<0, false, 128, kLse> : e == 1 ? score_tc_kernel<1, false, 128, kLse>
+             : e == 2 ? score_tc_kernel<2, false, 128, kLse> : score_tc_kernel<3, false, 128, kLse>;
+    }
+    if (d == 64) return b64 ? score_tc_kernel<0, true, 64, kBudget> : score_tc_kernel<0, false, 64, kBudget>;
+    return b64 ? score_tc_kernel<0, true, 128, kBudget> : score_tc_kernel<0, false, 128, kBudget>;
 }
 
 bool set_smem_attr() {
     static bool done = false;
     if (!done) {
         for (int d : {64, 128})
-            for (bool b64 : {false, true})
-                if (cudaFuncSetAttribute(score_kernel(d, b64), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmem)) != cudaSuccess)
-                    return false;
+            for (int mode : {static_cast<int>(kLse), static_cast<int>(kBudget)})
+                for (bool b64 : {false, true})
+                    if (cudaFuncSetAttribute(score_kernel(d, mode, b64), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kSmem)) != cudaSuccess)
+                        return false;
         done = true;
     }
     return true;
@@ -609,7 +614,7 @@ cudaError_t launch_proxy_tc(const Dims& D, const void* Pq, const void* Pk, float
     p.W = reinterpret_cast<float*>((w_addr + 31) & ~static_cast<uintptr_t>(31));
     const unsigned grid = static_cast<unsigned>(D.gl) * (p.tr_hi - p.tr_lo) * p.n_chunks;
     p.mode = kLse;
-    score_kernel(D.d)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.d, kLse)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // A3: the max-pool (with the row lse combine) from the window maxima, block rows [rb, re)
@@ -640,7 +645,7 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
     p.part_m = scratch;
     p.part_s = scratch + static_cast<size_t>(D.Hl) * D.M * 128;
     const unsigned grid = static_cast<unsigned>(D.Hl) * p.n_chunks;
-    score_kernel(D.d, D.b == 64)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
+    score_kernel(D.d, kBudget, D.b == 64)<<<grid, kThreads, kSmem, st>>>(ma, mb, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int n_comb = (D.M + kCombChunk - 1) / kCombChunk;
