@@ -494,7 +494,7 @@ int score_emu() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("PROXYATTN_SCORE_EMU");
-        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;   // 1/4 on the FMA pipe: A2 pass 213 -> 198 us
     }
     return v;
 }
@@ -539,7 +539,13 @@ ScoreKernel score_kernel(int d, int mode, bool b64 = false) {
              : e == 2 ? score_tc_kernel<2, false, 128, kLse> : score_tc_kernel<3, false, 128, kLse>;
     }
     if (d == 64) return b64 ? score_tc_kernel<0, true, 64, kBudget> : score_tc_kernel<0, false, 64, kBudget>;
-    return b64 ? score_tc_kernel<0, true, 128, kBudget> : score_tc_kernel<0, false, 128, kBudget>;
+    if (b64) return score_tc_kernel<0, true, 128, kBudget>;
+    static int eb = -1;   // PROXYATTN_BUDGET_EMU=0/1: the same split for the Alg. 1 pass (1: 178 -> 166 us)
+    if (eb < 0) {
+        const char* e = getenv("PROXYATTN_BUDGET_EMU");
+        eb = (e && e[0] == '0') ? 0 : 1;
+    }
+    return eb ? score_tc_kernel<1, false, 128, kBudget> : score_tc_kernel<0, false, 128, kBudget>;
 }
 
 bool set_smem_attr() {

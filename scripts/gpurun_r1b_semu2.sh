@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build=$?
+for e in 0 1 2; do
+PROXYATTN_SCORE_EMU=$e timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"score_tc" python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-lib-dense --no-graph 2>/dev/null | grep -E "score_tc" | python -c "
+import sys,csv
+print('emu $e', [r[-1] for r in csv.reader(sys.stdin)])"
+done
