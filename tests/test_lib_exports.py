@@ -105,9 +105,13 @@ def test_token_major_and_varlen_configs_on_host(so):
         with pytest.raises(pa.ProxyAttnError) as ei:
             pa.workspace_bytes(cfg)
         assert ei.value.code == pa._lib.E_CONFIG, name
-    # varlen: workspace sized by the longest sequence; validation of cu_seqlens
-    assert pa.varlen_workspace_bytes(tok, [0, 1000, 5096, 5096]) == \
-        pa.varlen_workspace_bytes(tok, [0, 4096])
+    # varlen: estimate scratch sized by the longest sequence, plus every sequence's block lists
+    # (one attention launch over all of them): more than the longest one alone, and growing
+    # with the other sequences; validation of cu_seqlens
+    one = pa.varlen_workspace_bytes(tok, [0, 4096])
+    three = pa.varlen_workspace_bytes(tok, [0, 1000, 5096, 5096])
+    assert three > one
+    assert pa.varlen_workspace_bytes(tok, [0, 1000, 5096, 9192]) > three
     for cu in ([1, 100], [0, 100, 50]):
         with pytest.raises(pa.ProxyAttnError):
             pa.varlen_workspace_bytes(tok, cu)
