@@ -53,7 +53,8 @@ typedef struct {
     int32_t  n_q_heads;          /* Hq (global) */
     int32_t  n_kv_heads;         /* Hkv (global) */
     int32_t  head_dim;           /* d */
-    int64_t  seq_len;            /* N */
+    int64_t  seq_len;            /* N; ceil(N / b) <= 16384 block rows (A4/A6 sort a row in
+                                    shared memory), else PROXYATTN_E_UNSUPPORTED */
     int32_t  block_size;         /* b (Z18) */
     int32_t  stride;             /* s, strided q/k sampling */
     int32_t  n_groups;           /* g, proxy heads */

@@ -40,6 +40,8 @@ int cuda_fail(cudaError_t e, const char* where) {
         if (_e != cudaSuccess) return cuda_fail(_e, where); \
     } while (0)
 
+constexpr int kMaxBlocks = 16384;
+
 // O1: validate the config and derive every size the kernels need.
 int derive(const proxyattn_cfg* c, pa::Dims& D) {
     if (!c) return fail(PROXYATTN_E_CONFIG, "cfg is NULL");
@@ -65,7 +67,10 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
         if (c->block_size != 64 && c->block_size != 128)
             return fail(PROXYATTN_E_UNSUPPORTED, "bf16 build needs block_size 64 or 128");
     }
-    if (c->seq_len / c->block_size > (1 << 20)) return fail(PROXYATTN_E_UNSUPPORTED, "too many blocks");
+    // A4/A6 sort one head's / one row's M block scores in shared memory (next_pow2(M) x 12 B
+    // <= 227 KB): M <= 16384, i.e. N <= 2M tokens at b = 128, 1M at b = 64
+    if ((c->seq_len + c->block_size - 1) / c->block_size > kMaxBlocks)
+        return fail(PROXYATTN_E_UNSUPPORTED, "seq_len / block_size > %d blocks", kMaxBlocks);
     D.Hq = c->n_q_heads;
     D.Hkv = c->n_kv_heads;
     D.d = c->head_dim;

@@ -573,6 +573,11 @@ cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar
                                    cudaStream_t st) {
     const int P = next_pow2(D.M);
     const size_t sm = static_cast<size_t>(P) * 8;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(budget_finalize_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+    }
     budget_finalize_kernel<<<D.Hl, 512, sm, st>>>(D, bmass, kstar, budget);
     return cudaGetLastError();
 }

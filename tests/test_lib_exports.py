@@ -66,11 +66,16 @@ def test_loads_and_validates_configs_on_host(so):
         "d = 96 in bf16": (good.replace(head_dim=96), pa._lib.E_UNSUPPORTED),
         "b = 256 in bf16": (good.replace(block_size=256), pa._lib.E_UNSUPPORTED),
         "shard not kv-aligned": (good.replace(q_head_begin=2, q_head_end=8), pa._lib.E_CONFIG),
+        "M > 16384 (b = 128)": (good.replace(seq_len=16384 * 128 + 1), pa._lib.E_UNSUPPORTED),
+        "M > 16384 (b = 64)": (good.replace(seq_len=16384 * 64 + 1, block_size=64), pa._lib.E_UNSUPPORTED),
     }
     for name, (cfg, code) in bad.items():
         with pytest.raises(pa.ProxyAttnError) as ei:
             pa.workspace_bytes(cfg)
         assert ei.value.code == code, name
+    # the largest supported M (16384 block rows: 2M tokens at b = 128, 1M at b = 64)
+    assert pa.workspace_bytes(good.replace(seq_len=16384 * 128)) > 0
+    assert pa.workspace_bytes(good.replace(seq_len=16384 * 64, block_size=64)) > 0
     # ragged N is accepted: M = ceil(N / b)
     assert pa.workspace_bytes(good.replace(seq_len=32768 + 64)) > 0
     # FP32_DEBUG accepts the small config A shape (d=64, b=64)
