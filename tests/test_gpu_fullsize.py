@@ -1,6 +1,6 @@
 """Full-size parity on bench.py's workloads (128K Llama-3.1-8B shape = the headline, its
 b = 64 variant, the d = 64 Llama-3.2-1B shape, Qwen2.5-7B at 64K with g = 4 and the 2048-token
-minimum budget; the same launch configuration bench.py times), checked against the oracle on SAMPLED
+minimum budget, the 256K sweep line; the same launch configuration bench.py times), checked against the oracle on SAMPLED
 outputs the oracle can compute one by one: L rows, Alg. 1 budgets of sampled heads,
 selected blocks on sampled rows (margin-gated), and O on sampled (head, row)
 items with the GPU mask injected.  Plus properties that hold at any size."""
@@ -23,6 +23,7 @@ WORKLOADS = {
     "llama3.1-8b-attn-128k-b64": (32, 8, 128, 131072, 64, 1, 0, "llama-128k"),
     "llama3.2-1b-attn-128k": (32, 8, 64, 131072, 128, 1, 0, "llama1b-128k"),
     "qwen2.5-7b-attn-64k": (28, 4, 128, 65536, 128, 4, 2048, "qwen-64k"),
+    "llama3.1-8b-attn-256k": (32, 8, 128, 262144, 128, 1, 0, "llama-256k"),   # bench --seq-len 262144
 }
 
 
