@@ -1,0 +1,83 @@
+"""GPU parity on seeded random configurations (bf16 tensor-core path) against the fp64 oracle,
+staged as in SURVEY §8(c).5: budgets on margin-qualified heads, block lists on
+margin-qualified rows, O with the GPU mask injected, and the dense path.  Each case draws
+head_dim and block size from the supported set, a GQA ratio (odd ones included), a
+proxy-group count dividing the KV heads, a stride dividing the block, gamma, a minimum
+budget, a ragged length spanning several tiles, and i.i.d. or structured inputs — the
+combinations the hand-written cases do not enumerate.  The FP32_DEBUG build is fuzzed over
+its wider shape set at the 1e-4 tolerance."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2509_24745_b200 as pa
+import workloads
+from test_gpu_parity import MARGIN, check_masks, check_out, ocfg_of, to_dev
+from test_gpu_shapes import run_staged
+
+pytestmark = pytest.mark.gpu
+
+
+def draw(case: int):
+    rng = np.random.default_rng(1000 + case)
+    d = int(rng.choice([64, 128]))
+    b = int(rng.choice([64, 128]))
+    Hkv = int(rng.choice([1, 2, 4]))
+    r = int(rng.choice([1, 2, 3, 4, 7]))
+    g = int(rng.choice([x for x in (1, 2, 4) if Hkv % x == 0]))
+    s = int(rng.choice([2, 4, 8]))
+    gamma = float(rng.choice([0.6, 0.8, 0.9, 0.95]))
+    min_budget = int(rng.choice([0, 0, b, 3 * b]))
+    N = int(rng.integers(3 * b, 24 * b)) | 1          # odd: always a partial last block
+    structured = bool(rng.integers(0, 2))
+    return dict(d=d, b=b, Hq=Hkv * r, Hkv=Hkv, g=g, s=s, gamma=gamma, min_budget=min_budget, N=N,
+                structured=structured)
+
+
+@pytest.mark.parametrize("case", range(64))
+def test_random_config_staged(case):
+    c = draw(case)
+    cfg = pa.Config(c["Hq"], c["Hkv"], c["d"], c["N"], c["b"], c["s"], c["g"], c["gamma"], c["min_budget"])
+    if c["structured"]:
+        Q, K, V, _ = workloads.structured(c["Hq"], c["Hkv"], c["N"], c["d"], seed=case)
+    else:
+        Q, K, V = (t.bfloat16() for t in workloads.iid(c["Hq"], c["Hkv"], c["N"], c["d"], seed=case))
+    run_staged(cfg, Q, K, V, min_checked=0.75)
+
+
+def draw_fp32(case: int):
+    rng = np.random.default_rng(5000 + case)
+    d = int(rng.choice([32, 64, 96, 128]))
+    b = int(rng.choice([16, 32, 48, 64, 128]))
+    s = int(rng.choice([x for x in (1, 2, 4, 8) if b % x == 0]))
+    Hkv = int(rng.choice([1, 2, 4]))
+    r = int(rng.choice([1, 2, 3, 4]))
+    g = int(rng.choice([x for x in (1, 2, 4) if Hkv % x == 0]))
+    gamma = float(rng.choice([0.5, 0.7, 0.9, 0.95, 1.0]))
+    min_budget = int(rng.choice([0, 0, b, 2 * b]))
+    N = int(rng.integers(2 * b, 20 * b))
+    return dict(d=d, b=b, s=s, Hq=Hkv * r, Hkv=Hkv, g=g, gamma=gamma, min_budget=min_budget, N=N)
+
+
+@pytest.mark.parametrize("case", range(32))
+def test_random_config_fp32_debug(case):
+    # the FP32_DEBUG build (SIMT kernels, the 1e-4 contract) over its wider shape set:
+    # d % 32 == 0, any b divisible by s, ragged N
+    c = draw_fp32(case)
+    cfg = pa.Config(c["Hq"], c["Hkv"], c["d"], c["N"], c["b"], c["s"], c["g"], c["gamma"], c["min_budget"],
+                    fp32_debug=True)
+    oc = ocfg_of(cfg)
+    Q, K, V = workloads.iid(c["Hq"], c["Hkv"], c["N"], c["d"], seed=case)
+    Qf, Kf, Vf = Q.numpy(), K.numpy(), V.numpy()
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, _, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    est = oracle.estimate(oc, Qf, Kf)
+    ks = kstar.cpu().numpy()
+    ok = est["budget_margin"] > MARGIN
+    assert np.array_equal(ks[ok], est["kstar"][ok])
+    assert np.all(np.abs(ks - est["kstar"]) <= 1)
+    checked, skipped = check_masks(oc, est["L"], ks, cnt, idx)
+    assert checked >= 0.75 * (checked + skipped)
+    O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+    check_out(O, oracle.attention(oc, Qf, Kf, Vf, cnt.cpu().numpy(), idx.cpu().numpy()), fp32=True)
+    check_out(pa.dense_prefill(cfg, Qd, Kd, Vd), oracle.dense(oc, Qf, Kf, Vf), fp32=True)
