@@ -167,12 +167,16 @@ def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, ks
     With kstar_given, `streams` and one workspace per range, the ranges' estimates run
     concurrently (each is a short chain of small, latency-bound kernels; they write disjoint
     rows of the outputs), forked from and joined back to the current stream.  With
-    scores_only the calls stop before the selection (select_rows finishes from each range's
+    scores_only (K* given, one workspace per range; a single range runs on the current
+    stream) the calls stop before the selection (select_rows finishes from each range's
     workspace), so the K* exchange can overlap the score passes."""
     if estimate is None:
         from . import _lib
 
         estimate = _lib.estimate
+    if scores_only:   # each range's L must survive in its own workspace until select_rows
+        assert kstar_given and out is not None and workspaces and len(workspaces) >= len(ranges), \
+            "scores_only needs kstar_given, out and one workspace per range"
     if kstar_given and streams and workspaces and len(ranges) > 1 and out is not None:
         cur = torch.cuda.current_stream()
         used = []
@@ -186,10 +190,10 @@ def estimate_rows(cfg, Q, K, ranges, workspace=None, out=None, estimate=None, ks
         for s in used:
             cur.wait_stream(s)
         return out
-    assert not scores_only, "scores_only needs kstar_given, streams and one workspace per range"
     for k, (b, e) in enumerate(ranges):
-        out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=kstar_given or k > 0), Q, K,
-                       workspace, out)
+        ws = workspaces[k % len(workspaces)] if workspaces else workspace
+        out = estimate(cfg.replace(row_begin=b, row_end=e, kstar_given=kstar_given or k > 0,
+                                   scores_only=scores_only), Q, K, ws, out)
     return out
 
 

@@ -12,7 +12,7 @@ import pytest
 import oracle
 import paper_2509_24745_b200 as pa
 import workloads
-from test_gpu_parity import MARGIN, check_masks, check_out, ocfg_of, to_dev
+from test_gpu_parity import DEV, MARGIN, check_masks, check_out, ocfg_of, to_dev
 from test_gpu_shapes import run_staged
 
 pytestmark = pytest.mark.gpu
@@ -81,3 +81,45 @@ def test_random_config_fp32_debug(case):
     O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
     check_out(O, oracle.attention(oc, Qf, Kf, Vf, cnt.cpu().numpy(), idx.cpu().numpy()), fp32=True)
     check_out(pa.dense_prefill(cfg, Qd, Kd, Vd), oracle.dense(oc, Qf, Kf, Vf), fp32=True)
+
+
+@pytest.mark.parametrize("case", range(32))
+def test_random_config_layouts_and_shards_bitwise(case):
+    # on the bf16 random configurations: token-major views, and the zig-zag row-sharded
+    # estimate (K* given, scores only + select) and prefill over 2-4 ranks, must reproduce the
+    # head-major one-call results BIT for bit (layout and row ranges change addressing only)
+    from paper_2509_24745_b200 import shard
+    import torch
+    c = draw(case)
+    cfg = pa.Config(c["Hq"], c["Hkv"], c["d"], c["N"], c["b"], c["s"], c["g"], c["gamma"], c["min_budget"])
+    Q, K, V, _ = workloads.structured(c["Hq"], c["Hkv"], c["N"], c["d"], seed=100 + case)
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    kstar, budget, cnt, idx = pa.estimate(cfg, Qd, Kd)
+    full = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
+
+    def same_lists(c2, i2, rows=None):
+        assert torch.equal(c2 if rows is None else c2[:, rows], cnt if rows is None else cnt[:, rows])
+        c_np, a, b_ = cnt.cpu().numpy(), idx.cpu().numpy(), i2.cpu().numpy()
+        for h in range(cfg.n_q_heads):
+            for m in (range(cfg.M) if rows is None else rows):
+                assert np.array_equal(a[h, m, :c_np[h, m]], b_[h, m, :c_np[h, m]]), (h, m)
+    tcfg = cfg.replace(token_major=True)
+    Qt, Kt, Vt = (x.transpose(0, 1).contiguous() for x in (Qd, Kd, Vd))
+    k2, _, c2, i2 = pa.estimate(tcfg, Qt, Kt)
+    assert torch.equal(k2, kstar)
+    same_lists(c2, i2)
+    assert torch.equal(pa.prefill(tcfg, Qt, Kt, Vt, c2, i2).transpose(0, 1), full)
+    world = 2 + case % 3
+    O = torch.zeros_like(full)
+    for rank in range(world):
+        rows = shard.zigzag_rows(cfg.M, world, rank, shard.row_align(cfg))
+        wss = [pa.alloc_workspace(cfg, DEV), pa.alloc_workspace(cfg, DEV)]
+        out = (kstar.clone(), budget.clone(), torch.zeros_like(cnt), torch.zeros_like(idx))
+        shard.estimate_rows(cfg, Qd, Kd, rows, out=out, kstar_given=True, scores_only=True,
+                            streams=[torch.cuda.Stream(), torch.cuda.Stream()], workspaces=wss)
+        torch.cuda.synchronize()
+        shard.select_rows(cfg, rows, wss, out[0], (out[2], out[3]))
+        torch.cuda.synchronize()
+        same_lists(out[2], out[3], [m for b0, e0 in rows for m in range(b0, e0)])
+        shard.prefill_rows(cfg, Qd, Kd, Vd, out[2], out[3], O, rows)
+    assert torch.equal(O, full)
