@@ -123,3 +123,37 @@ def test_random_config_layouts_and_shards_bitwise(case):
         same_lists(out[2], out[3], [m for b0, e0 in rows for m in range(b0, e0)])
         shard.prefill_rows(cfg, Qd, Kd, Vd, out[2], out[3], O, rows)
     assert torch.equal(O, full)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_random_varlen_and_host_path_bitwise(case):
+    # random packed batches (1-6 sequences, lengths 0-3000 tokens, empty ones included) through
+    # proxyattn_forward_varlen == one estimate + prefill per sequence, bit for bit; and the
+    # pipelined host path (PROXYATTN_HOST_CHUNKS default) == the device-resident call
+    import torch
+    rng = np.random.default_rng(9000 + case)
+    c = draw(case)
+    Hq, Hkv, d, b = c["Hq"], c["Hkv"], c["d"], c["b"]
+    lens = [int(x) if rng.random() > 0.15 else 0 for x in rng.integers(1, 3000, int(rng.integers(1, 7)))]
+    cu = np.concatenate([[0], np.cumsum(lens)]).tolist()
+    if cu[-1] == 0:
+        lens[0], cu = 777, [0] + [777] * len(lens)
+    seqs = {i: workloads.structured(Hq, Hkv, n, d, seed=200 + case * 8 + i, device=DEV)
+            for i, n in enumerate(lens) if n}
+    packed = [torch.cat([seqs[i][j].transpose(0, 1) for i in sorted(seqs)], 0).contiguous() for j in range(3)]
+    vcfg = pa.Config(Hq, Hkv, d, 1, b, c["s"], c["g"], c["gamma"], c["min_budget"], token_major=True)
+    O, kstar = pa.forward_varlen(vcfg, cu, *packed)
+    for i, (Q, K, V, _) in seqs.items():
+        cfg = pa.Config(Hq, Hkv, d, lens[i], b, c["s"], c["g"], c["gamma"], c["min_budget"])
+        k1, _, cnt, idx = pa.estimate(cfg, Q, K)
+        O1 = pa.prefill(cfg, Q, K, V, cnt, idx)
+        assert torch.equal(kstar[i], k1), i
+        assert torch.equal(O[cu[i]:cu[i + 1]], O1.transpose(0, 1)), i
+        if i == max(seqs, key=lambda j: lens[j]):          # host path on the longest sequence
+            Qh, Kh, Vh = (t.cpu().pin_memory() for t in (Q, K, V))
+            Oh = torch.empty_like(Qh).pin_memory()
+            ks = torch.empty(Hq, dtype=torch.int32).pin_memory()
+            ws = torch.empty(pa.forward_host_workspace_bytes(cfg), dtype=torch.uint8, device=DEV)
+            pa.forward_host(cfg, Qh, Kh, Vh, Oh, ws, ks)
+            torch.cuda.synchronize()
+            assert torch.equal(ks, k1.cpu()) and torch.equal(Oh, O1.cpu())
