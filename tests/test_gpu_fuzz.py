@@ -157,3 +157,22 @@ def test_random_varlen_and_host_path_bitwise(case):
             pa.forward_host(cfg, Qh, Kh, Vh, Oh, ws, ks)
             torch.cuda.synchronize()
             assert torch.equal(ks, k1.cpu()) and torch.equal(Oh, O1.cpu())
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_config_method_variants(case):
+    # the method variants (designated proxy head, static K*, constant-K reading
+    # of Eq. 3, forced sink block), alone and combined, on the random bf16 configurations
+    rng = np.random.default_rng(7000 + case)
+    c = draw(case + 100)
+    M = -(-c["N"] // c["b"])
+    v = dict(designated_head=bool(rng.integers(0, 2)), constant_k=bool(rng.integers(0, 2)),
+             force_sink=bool(rng.integers(0, 2)))
+    if rng.random() < 0.3:
+        v["static_kstar"] = int(rng.integers(1, M + 1))
+    cfg = pa.Config(c["Hq"], c["Hkv"], c["d"], c["N"], c["b"], c["s"], c["g"], c["gamma"], c["min_budget"], **v)
+    Q, K, V, _ = workloads.structured(c["Hq"], c["Hkv"], c["N"], c["d"], seed=300 + case)
+    cnt, idx = run_staged(cfg, Q, K, V, min_checked=0.75)
+    if cfg.force_sink:
+        c_np, i_np = cnt.cpu().numpy(), idx.cpu().numpy()
+        assert np.all(i_np[:, 1:, 0][c_np[:, 1:] >= 2] == 0)
