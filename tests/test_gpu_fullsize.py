@@ -1,6 +1,6 @@
 """Full-size parity on bench.py's workloads (128K Llama-3.1-8B shape = the headline, its
 b = 64 variant, the d = 64 Llama-3.2-1B shape, Qwen2.5-7B at 64K with g = 4 and the 2048-token
-minimum budget, the 256K sweep line; the same launch configuration bench.py times), checked against the oracle on SAMPLED
+minimum budget, the 70B shape, gamma = 0.95, the 256K sweep line; the same launch configuration bench.py times), checked against the oracle on SAMPLED
 outputs the oracle can compute one by one: L rows, Alg. 1 budgets of sampled heads,
 selected blocks on sampled rows (margin-gated), and O on sampled (head, row)
 items with the GPU mask injected.  Plus properties that hold at any size."""
@@ -17,21 +17,24 @@ pytestmark = pytest.mark.gpu
 MARGIN = 1e-4
 
 
-# bench.py's workloads at full size: (Hq, Hkv, d, N, b, g, min budget, preset)
+# bench.py's workloads at full size: (Hq, Hkv, d, N, b, g, min budget, preset[, gamma])
 WORKLOADS = {
     "llama3.1-8b-attn-128k": (32, 8, 128, 131072, 128, 1, 0, "llama-128k"),
     "llama3.1-8b-attn-128k-b64": (32, 8, 128, 131072, 64, 1, 0, "llama-128k"),
     "llama3.2-1b-attn-128k": (32, 8, 64, 131072, 128, 1, 0, "llama1b-128k"),
     "qwen2.5-7b-attn-64k": (28, 4, 128, 65536, 128, 4, 2048, "qwen-64k"),
     "llama3.1-8b-attn-256k": (32, 8, 128, 262144, 128, 1, 0, "llama-256k"),   # bench --seq-len 262144
+    "llama3.1-70b-attn-128k": (64, 8, 128, 131072, 128, 1, 0, "llama-128k"),
+    "llama3.1-8b-attn-128k-g95": (32, 8, 128, 131072, 128, 1, 0, "llama-128k", 0.95),
 }
 
 
 @pytest.fixture(scope="module", params=list(WORKLOADS))
 def layer(request):
     dev = torch.device("cuda:0")
-    Hq, Hkv, d, N, b, g, mb, preset = WORKLOADS[request.param]
-    cfg = pa.Config(Hq, Hkv, d, N, b, 4, g, 0.9, mb)
+    Hq, Hkv, d, N, b, g, mb, preset, *rest = WORKLOADS[request.param]
+    gamma = rest[0] if rest else 0.9
+    cfg = pa.Config(Hq, Hkv, d, N, b, 4, g, gamma, mb)
     Q, K, V, _ = workloads.structured(Hq, Hkv, N, d, seed=0, params=workloads.PRESETS[preset],
                                       device=dev)
     kstar, budget, cnt, idx = pa.estimate(cfg, Q, K)
@@ -39,7 +42,7 @@ def layer(request):
     qsum, ksum = pa.pool(cfg, Q, K)
     L = pa.proxy_scores(cfg, qsum, ksum)
     torch.cuda.synchronize()
-    oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, g, 0.9, mb, round_bf16=True)
+    oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, g, gamma, mb, round_bf16=True)
     host = dict(Q=Q.float().cpu().numpy(), K=K.float().cpu().numpy(), V=V.float().cpu().numpy())
     return dict(cfg=cfg, oc=oc, kstar=kstar.cpu().numpy(), budget=budget.cpu().numpy(),
                 cnt=cnt.cpu().numpy(), idx=idx, O=O, L=L.cpu().numpy(), **host)
