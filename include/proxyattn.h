@@ -22,7 +22,13 @@
  *    Alg. 1 onto a library-owned per-device stream and joins it back to `stream` by
  *    events before returning, so its completion is still ordered on `stream` (and the
  *    call is capturable in a CUDA graph); PROXYATTN_SERIAL_ESTIMATE=1 disables the fork.
- *  - The library allocates no device memory: scratch comes from the caller's workspace.
+ *  - Scratch comes from the caller's workspace.  The only memory the library allocates is
+ *    the attention launch's scheduler state, once per (device, stream) on the first
+ *    prefill / forward on that stream (work counter, KV-head order, the exact-launch row
+ *    list: 20 bytes per work item, grown when a larger launch comes, kept until exit).
+ *    Hence CUDA-graph capture: make one call on the capture stream first (as bench.py
+ *    and tests/test_gpu_graphs.py do); every call is then asynchronous and capturable,
+ *    including proxyattn_forward_varlen.
  *  - Return codes: PROXYATTN_OK or one of the negative PROXYATTN_E_* codes; a
  *    human-readable reason is available from proxyattn_last_error() (thread-local).
  *    Validation errors are raised before anything is enqueued.
