@@ -132,6 +132,12 @@ def lib():
         L.oracle_cost_ratio.restype = ctypes.c_double
         L.oracle_num_threads.argtypes = []
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_num_threads.restype = None
+        L.oracle_seq_avgpool_scores.argtypes = [cp, _P, _P, _P]
+        L.oracle_seq_avgpool_scores.restype = None
+        L.oracle_select_heads.argtypes = [cp, _P, _P, _P, _P, _P]
+        L.oracle_select_heads.restype = None
         _lib = L
     return _lib
 
@@ -281,6 +287,42 @@ def cost_ratio(cfg: Cfg) -> float:
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().oracle_set_num_threads(int(n))
+
+
+def seq_avgpool_scores(cfg: Cfg, Q, K):
+    """O11: the seq-avgpool comparator's per-head log-domain block scores S [Hq][M][M]
+    (SPEC S:365-373), -inf above the diagonal."""
+    c = _check(cfg)
+    Q, K = _f32(Q), _f32(K)
+    S = np.full((cfg.n_q_heads, cfg.M, cfg.M), np.nan)
+    lib().oracle_seq_avgpool_scores(ctypes.byref(c), _ptr(Q), _ptr(K), _ptr(S))
+    return S
+
+
+def select_heads(cfg: Cfg, S, kstar):
+    """O9 on per-head maps S [Hq][M][M]: (block_cnt, block_idx (-1 padded), cut_margin)."""
+    c = _check(cfg)
+    S = np.ascontiguousarray(S, np.float64)
+    ks = _i32(kstar)
+    H, M = cfg.n_q_heads, cfg.M
+    cnt = np.zeros((H, M), np.int32)
+    idx = np.full((H, M, M), -1, np.int32)
+    mg = np.full((H, M), np.nan)
+    lib().oracle_select_heads(ctypes.byref(c), _ptr(S), _ptr(ks), _ptr(cnt), _ptr(idx), _ptr(mg))
+    return cnt, idx, mg
+
+
+def avgpool_estimate(cfg: Cfg, Q, K):
+    """The comparator end to end: O7 budgets (as the proxy path) + O11 scores + per-head O9."""
+    S = seq_avgpool_scores(cfg, Q, K)
+    kstar, budget, bmargin, mass = budgets(cfg, Q, K)
+    cnt, idx, cmargin = select_heads(cfg, S, kstar)
+    return dict(S=S, kstar=kstar, budget=budget, budget_margin=bmargin, block_cnt=cnt,
+                block_idx=idx, cut_margin=cmargin)
 
 
 def estimate(cfg: Cfg, Q, K):

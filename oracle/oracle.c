@@ -382,6 +382,89 @@ void oracle_dense(const oracle_cfg* c, const float* Q, const float* K, const flo
     }
 }
 
+/* ------------------------------------------------------------------- O11 -- */
+
+/* "q̄_m = mean of b query rows; k̄_n = mean of b key rows; score(m,n) = softmax
+ * over valid n of q̄_m·k̄_n/√d_k".  Block sums in fp64 (rounded to bf16 when round_bf16),
+ * divided by the block's real row count; softmax over n <= m, stored as log-probabilities. */
+void oracle_seq_avgpool_scores(const oracle_cfg* c, const float* Q, const float* K, double* S) {
+    const int d = c->head_dim, M = n_blocks(c), b = c->block_size;
+    const long N = c->seq_len;
+    const int r = c->n_q_heads / c->n_kv_heads;
+    double* qbar = (double*)malloc(sizeof(double) * (size_t)c->n_q_heads * M * d);
+    double* kbar = (double*)malloc(sizeof(double) * (size_t)c->n_kv_heads * M * d);
+    /* block means: sum the block's real rows, round the sum (bf16 contract), divide */
+    for (int role = 0; role < 2; ++role) {
+        const int H = role == 0 ? c->n_q_heads : c->n_kv_heads;
+        const float* X = role == 0 ? Q : K;
+        double* out = role == 0 ? qbar : kbar;
+        for (int h = 0; h < H; ++h) {
+            for (int m = 0; m < M; ++m) {
+                double* o = out + ((long)h * M + m) * d;
+                long t0 = (long)m * b, t1 = t0 + b < N ? t0 + b : N;
+                for (int e = 0; e < d; ++e) o[e] = 0.0;
+                for (long t = t0; t < t1; ++t)
+                    for (int e = 0; e < d; ++e) o[e] += (double)X[((long)h * N + t) * d + e];
+                for (int e = 0; e < d; ++e) {
+                    if (c->round_bf16) o[e] = oracle_rne_bf16(o[e]);
+                    o[e] /= (double)(t1 - t0);
+                }
+            }
+        }
+    }
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (long hm = 0; hm < (long)c->n_q_heads * M; ++hm) {
+        int h = (int)(hm / M), m = (int)(hm % M);
+        const double* q = qbar + ((long)h * M + m) * d;
+        double* row = S + ((long)h * M + m) * M;
+        double mx = -INFINITY;
+        for (int n = 0; n < M; ++n) {
+            if (n > m) { row[n] = -INFINITY; continue; }
+            const double* k = kbar + ((long)(h / r) * M + n) * d;
+            double dot = 0.0;
+            for (int e = 0; e < d; ++e) dot += q[e] * k[e];
+            row[n] = dot / sqrt((double)d);
+            if (row[n] > mx) mx = row[n];
+        }
+        double sum = 0.0;
+        for (int n = 0; n <= m; ++n) sum += exp(row[n] - mx);
+        double lse = mx + log(sum);
+        for (int n = 0; n <= m; ++n) row[n] -= lse;
+    }
+    free(qbar);
+    free(kbar);
+}
+
+void oracle_select_heads(const oracle_cfg* c, const double* S, const int32_t* kstar,
+                         int32_t* block_cnt, int32_t* block_idx, double* cut_margin) {
+    const int M = n_blocks(c);
+    #pragma omp parallel
+    {
+        vi_pair* s = (vi_pair*)malloc(sizeof(vi_pair) * (size_t)M);
+        unsigned char* sel = (unsigned char*)malloc((size_t)M);
+        #pragma omp for schedule(dynamic, 1)
+        for (long hm = 0; hm < (long)c->n_q_heads * M; ++hm) {
+            int h = (int)(hm / M), m = (int)(hm % M);
+            const double* row = S + ((long)h * M + m) * M;
+            /* the same Eq. 3 rule as O9: diagonal forced first (Z15), (score desc, index asc) */
+            for (int n = 0; n < m; ++n) { s[n].v = row[n]; s[n].n = n; }
+            if (c->force_sink && m > 0) s[0].v = INFINITY;
+            qsort(s, (size_t)m, sizeof(vi_pair), cmp_desc_then_index);
+            int K = oracle_row_count(c, kstar[h], m);
+            int k = K - 1;
+            memset(sel, 0, (size_t)M);
+            sel[m] = 1;
+            for (int j = 0; j < k; ++j) sel[s[j].n] = 1;
+            int w = 0;
+            for (int n = 0; n <= m; ++n) if (sel[n]) block_idx[hm * M + w++] = n;
+            block_cnt[hm] = w;
+            if (cut_margin) cut_margin[hm] = (k == 0 || k == m) ? INFINITY : (s[k - 1].v - s[k].v);
+        }
+        free(s);
+        free(sel);
+    }
+}
+
 /* ------------------------------------------------------------- cost model -- */
 
 double oracle_cost_ratio(const oracle_cfg* c) {
@@ -393,5 +476,13 @@ int oracle_num_threads(void) {
     return omp_get_max_threads();
 #else
     return 1;
+#endif
+}
+
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n >= 1) omp_set_num_threads(n);
+#else
+    (void)n;
 #endif
 }

@@ -106,8 +106,24 @@ void oracle_dense(const oracle_cfg* c, const float* Q, const float* K, const flo
 /* §3.1 cost model: g / (Hq * s^2). */
 double oracle_cost_ratio(const oracle_cfg* c);
 
-/* Number of OpenMP threads the oracle uses. */
+/* O11 — the seq-avgpool comparator (SPEC S:365-373 seq_avgpool_scores;
+ * paper §1 / §2.1, "pooling methods along the sequence dimension"): per query head h,
+ * qbar_m = mean of block m's real query rows of head h, kbar_n = mean of block n's real key
+ * rows of kv(h) (the padded last block averages its real rows only), and
+ * S[h][m][n] = z_mn - log sum_{n' <= m} exp(z_mn'),  z_mn = qbar_m . kbar_n / sqrt(d),
+ * for n <= m; -inf for n > m.  round_bf16: the block SUMS are rounded to bf16 before the
+ * division (the precision contract of the bf16 build, as O3's proxies).
+ * Q: [Hq][N][d], K: [Hkv][N][d]; S: [Hq][M][M]. */
+void oracle_seq_avgpool_scores(const oracle_cfg* c, const float* Q, const float* K, double* S);
+
+/* O9 over PER-HEAD score maps (the comparator's selection): as oracle_select, but head h
+ * ranks row m of its own map S[h] (S: [Hq][M][M]). */
+void oracle_select_heads(const oracle_cfg* c, const double* S, const int32_t* kstar,
+                         int32_t* block_cnt, int32_t* block_idx, double* cut_margin);
+
+/* Number of OpenMP threads the oracle uses; set_num_threads changes it (n >= 1). */
 int oracle_num_threads(void);
+void oracle_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

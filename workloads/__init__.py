@@ -136,3 +136,30 @@ def needle(n_heads: int, seq_len: int, head_dim: int, pos: int, boost: float, se
     Q += w                                   # every query has a unit component along w
     K[:, pos] = boost * np.sqrt(head_dim) * w  # logit(t, pos) ~ boost
     return Q.to(dtype), K.to(dtype), V.to(dtype)
+
+
+def needle_in_cold_block(n_blocks: int, block_size: int, head_dim: int, seed: int, boost: float = 12.0,
+                         bias_hi: float = 2.0, dtype=torch.float32):
+    """One head (Q, K, V [1][N][d], N = n_blocks * block_size) for SPEC's granularity
+    criterion (AC5; the needle construction of S:372 and S:405): every query is a unit
+    vector w plus small noise; the keys of block n carry a block-level logit bias
+    beta_n ~ U[0, bias_hi] along w (distractor blocks with elevated AVERAGE scores) plus
+    small noise, except one "cold" block n* (beta = 0) that hides a single needle key whose
+    logit is `boost` for every query.  Returns (Q, K, V, n_star, needle_pos).  Deterministic
+    in `seed`."""
+    g = _gen("cpu", seed)
+    rng = np.random.default_rng(seed)
+    N = n_blocks * block_size
+    n_star = 1 + seed % max(1, min(8, n_blocks - 2))
+    pos = n_star * block_size + int(rng.integers(0, block_size))
+    w = torch.randn(head_dim, generator=g)
+    w /= w.norm()
+    beta = torch.tensor(rng.uniform(0.0, bias_hi, n_blocks), dtype=torch.float32)
+    beta[n_star] = 0.0
+    sd = float(np.sqrt(head_dim))
+    Q = (w + 0.05 * torch.randn(N, head_dim, generator=g)).unsqueeze(0)
+    K = 0.05 * torch.randn(N, head_dim, generator=g)
+    K += (beta.repeat_interleave(block_size) * sd).unsqueeze(1) * w     # logit ~ beta_n per token
+    K[pos] = boost * sd * w                                              # the needle: logit ~ boost
+    V = torch.randn(1, N, head_dim, generator=g)
+    return Q.to(dtype), K.unsqueeze(0).to(dtype), V.to(dtype), n_star, pos
