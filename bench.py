@@ -228,100 +228,117 @@ def gen_inputs(w, device):
 
 
 # ------------------------------------------------------------------------ oracle --
-def oracle_sample(w, Q, K, V):
+def oracle_sample(w, Q, K, V, threads=None, scale=1.0):
     """Time the fp64 CPU oracle (as it stands) on a bounded sample of one layer and
-    extrapolate to the full layer (ms).  Sample: pooling (full), Alg. 1 budgets of every
-    head (full), proxy scores + selection of 3 block rows (scaled by logit / row count),
-    block-sparse attention of 4 (head, row) items of the two densest heads (scaled by the
-    layer's selected-block count under the oracle's own budgets)."""
+    extrapolate to the full layer (ms).  Sample: pooling (full); Alg. 1 budgets of a head
+    subset (scaled by the head count); proxy scores + selection of sampled block rows (scaled
+    by logit / row count); block-sparse attention of sampled (head, row) items of the densest
+    heads (scaled by the layer's selected-block count under the oracle's own budgets).
+    `threads` pins the OpenMP thread count (1 = the single-core baseline); `scale` < 1 shrinks
+    the sample (fewer heads / rows / items) for slow configurations."""
     import oracle
 
     oc = oracle.Cfg(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"],
                     w["block_size"], w["stride"], w["n_groups"], w["gamma"],
                     w["min_budget_tokens"], round_bf16=True)
-    M, bs, Ns = oc.M, oc.block_size // oc.stride, oc.Ns
-    Qf = Q.float().cpu().numpy()
-    Kf = K.float().cpu().numpy()
-    Vf = V.float().cpu().numpy()
-    t = {}
-    t0 = time.perf_counter()
-    Pq, Pk, scale = oracle.pool(oc, Qf, Kf)
-    t["pool_s"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    kst, _, _, _ = oracle.budgets(oc, Qf, Kf)
-    t["budget_s"] = time.perf_counter() - t0
-    rows = [M // 8, M // 2, M - 1]
-    t0 = time.perf_counter()
-    _, L = oracle.proxy_scores(oc, Pq, Pk, scale, rows=rows)
-    t_rows = time.perf_counter() - t0
-    logits_rows = sum(bs * (m * bs) + bs * (bs + 1) / 2 for m in rows)
-    logits_all = oc.n_groups * Ns * (Ns + 1) / 2
-    t["proxy_s"] = t_rows * logits_all / logits_rows
-    t0 = time.perf_counter()
-    cnt, idx, _ = oracle.select(oc, np.nan_to_num(L, nan=-np.inf), kst, rows=rows)
-    t["select_s"] = (time.perf_counter() - t0) * M / len(rows)
-    dense_heads = [int(h) for h in np.argsort(-kst, kind="stable")[:2]]
-    items = [(h, m) for h in dense_heads for m in (M // 2, M - 1)]
-    t0 = time.perf_counter()
-    oracle.attention(oc, Qf, Kf, Vf, cnt, idx, items=items)
-    t_att_s = time.perf_counter() - t0
-    sel_blocks = sum(int(cnt[h, m]) for h, m in items)
-    total_blocks = sum(oracle.row_count(oc, int(k), m) for k in kst for m in range(M))
-    t["attention_s"] = t_att_s * total_blocks / max(sel_blocks, 1)
-    total = sum(t.values())
-    sample = (f"pool and Alg. 1 of all {oc.n_q_heads} heads in full; proxy scores of block "
-              f"rows {rows} of {M} (x{logits_all / logits_rows:.0f} by logit count) and their "
-              f"selection (x{M / len(rows):.0f}); attention of {len(items)} (head,row) items of "
-              f"the densest heads, {sel_blocks} blocks (x{total_blocks / max(sel_blocks, 1):.0f} "
-              f"to the layer's {total_blocks} selected blocks); extrapolated to one layer")
-    return total * 1e3, sample, oracle.num_threads(), t
+    all_threads = oracle.num_threads()
+    if threads:
+        oracle.set_num_threads(threads)
+    try:
+        M, bs, Ns, H = oc.M, oc.block_size // oc.stride, oc.Ns, oc.n_q_heads
+        Qf = Q.float().cpu().numpy()
+        Kf = K.float().cpu().numpy()
+        Vf = V.float().cpu().numpy()
+        t = {}
+        t0 = time.perf_counter()
+        Pq, Pk, sc = oracle.pool(oc, Qf, Kf)
+        t["pool_s"] = time.perf_counter() - t0
+        nh = max(1, min(H, int(round(H * scale))))
+        heads = [int(h) for h in np.linspace(0, H - 1, nh).round()]
+        t0 = time.perf_counter()
+        kst, _, _, _ = oracle.budgets(oc, Qf, Kf, heads=heads)
+        t["budget_s"] = (time.perf_counter() - t0) * H / len(heads)
+        if len(heads) < H:   # budgets of the other heads (for the selection / block counts), untimed
+            rest = [h for h in range(H) if h not in heads]
+            k2, _, _, _ = oracle.budgets(oc, Qf, Kf, heads=rest)
+            kst[rest] = k2[rest]
+        nr = max(2, int(round(8 * scale)))
+        rows = sorted({int(x) for x in np.linspace(M // 8, M - 1, nr).round()})
+        t0 = time.perf_counter()
+        _, L = oracle.proxy_scores(oc, Pq, Pk, sc, rows=rows)
+        t_rows = time.perf_counter() - t0
+        logits_rows = sum(bs * (m * bs) + bs * (bs + 1) / 2 for m in rows)
+        logits_all = oc.n_groups * Ns * (Ns + 1) / 2
+        t["proxy_s"] = t_rows * logits_all / logits_rows
+        t0 = time.perf_counter()
+        cnt, idx, _ = oracle.select(oc, np.nan_to_num(L, nan=-np.inf), kst, rows=rows)
+        t["select_s"] = (time.perf_counter() - t0) * M / len(rows)
+        ni = max(2, int(round(8 * scale)))
+        dense_heads = [int(h) for h in np.argsort(-kst, kind="stable")[:2]]
+        items = [(h, m) for h in dense_heads for m in rows[-(ni // 2):]]
+        t0 = time.perf_counter()
+        oracle.attention(oc, Qf, Kf, Vf, cnt, idx, items=items)
+        t_att_s = time.perf_counter() - t0
+        sel_blocks = sum(int(cnt[h, m]) for h, m in items)
+        total_blocks = sum(oracle.row_count(oc, int(k), m) for k in kst for m in range(M))
+        t["attention_s"] = t_att_s * total_blocks / max(sel_blocks, 1)
+        total = sum(t.values())
+        cores = oracle.num_threads()
+    finally:
+        oracle.set_num_threads(all_threads)
+    sample = (f"pool in full; Alg. 1 of {len(heads)} of {H} heads (x{H / len(heads):.0f}); proxy scores of "
+              f"block rows {rows} of {M} (x{logits_all / logits_rows:.0f} by logit count) and their selection "
+              f"(x{M / len(rows):.0f}); attention of {len(items)} (head,row) items of the densest heads, "
+              f"{sel_blocks} blocks (x{total_blocks / max(sel_blocks, 1):.0f} to the layer's {total_blocks} "
+              f"selected blocks); extrapolated to one layer")
+    return total * 1e3, sample, cores, t
+
+
+def bench_config(w, ws=1, parallelism=None):
+    """The `config` object of both arms' JSON lines (identical for the same workload)."""
+    return {"workload": w["name"], "n_q_heads": w["n_q_heads"], "n_kv_heads": w["n_kv_heads"],
+            "head_dim": w["head_dim"], "seq_len": w["seq_len"], "block_size": w["block_size"],
+            "stride": w["stride"], "n_groups": w["n_groups"], "gamma": w["gamma"],
+            "min_budget_tokens": w["min_budget_tokens"], "seed": w["seed"], "preset": w["preset"],
+            "parallelism": parallelism or ("single GPU" if ws == 1 else f"x{ws}"),
+            "l2": "flushed (256 MiB write) before every timed step"}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    w = dict(WORKLOADS[args.workload])
+    w = workload_of(args)
     Q, K, V, meta = gen_inputs(w, "cpu")
     vals = []
     sample = cores = None
     for i in range(args.warmup + args.steps):
-        ms, sample, cores, parts = oracle_sample(w, Q, K, V)
+        ms, sample, cores, parts = oracle_sample(w, Q, K, V, scale=0.25)
         if i >= args.warmup:
             vals.append(ms)
-    v = float(np.mean(vals))
+    v = float(np.median(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w["name"], **{k: w[k] for k in w if k != "name"}},
+        "config": bench_config(w, args.gpus, parallelism_of(args.gpus, args.shard, args.alg1)),
         "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample + " (median over steps)"},
         "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------- ours --
-def run_ours(args):
-    import paper_2509_24745_b200 as pa
+def parallelism_of(ws, sharding, alg1):
+    if ws <= 1:
+        return "single GPU"
+    if sharding == "rows":
+        return f"zig-zag block rows x{ws}" + (", Alg. 1 head-sharded + all-gather of K*" if alg1 == "sharded" else "")
+    return f"kv-head groups x{ws}"
 
-    ws, rank, local = dist_env()
-    # BENCH_SAME_DEVICE=1 (testing only): every rank on cuda:0, gloo only -> exercises the
-    # multi-rank code path on a one-GPU box (its timings are meaningless).
-    same_dev = os.environ.get("BENCH_SAME_DEVICE") == "1"
-    if same_dev:
-        local = 0
-    cpu_group = None
-    if ws > 1:
-        import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("gloo" if same_dev else "nccl")
-        cpu_group = dist.new_group(backend="gloo")      # timing / bookkeeping collectives
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
+def workload_of(args):
     w = dict(WORKLOADS[args.workload])
     if args.gamma:
         w["gamma"] = args.gamma
@@ -334,6 +351,34 @@ def run_ours(args):
         cand = w["preset"].rsplit("-", 1)[0] + f"-{args.seq_len // 1024}k"
         if cand in workloads.PRESETS:      # per-length calibration to Table 8
             w["preset"] = cand
+    return w
+
+
+# ---------------------------------------------------------------------------- ours --
+def run_ours(args):
+    import paper_2509_24745_b200 as pa
+    from paper_2509_24745_b200 import shard
+
+    ws, rank, local = dist_env()
+    # BENCH_SAME_DEVICE=1 (testing only): every rank on cuda:0, gloo only -> exercises the
+    # multi-rank code path on a one-GPU box (its timings are meaningless).
+    same_dev = os.environ.get("BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
+    cpu_group = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        # NCCL's init log (communicator size, transports) on stderr, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo" if same_dev else "nccl")
+        cpu_group = dist.new_group(backend="gloo")      # timing / bookkeeping collectives
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = workload_of(args)
     sharding = args.shard if ws > 1 else "rows"
     cfg = build_config(pa, rank, ws, w, sharding)
     Q, K, V, meta = gen_inputs(w, dev)
@@ -351,11 +396,10 @@ def run_ours(args):
     idx = torch.empty(Hl, M, M, dtype=torch.int32, device=dev)
     O = torch.empty_like(Ql)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    from paper_2509_24745_b200 import shard
 
     my_rows = shard.zigzag_rows(M, ws, rank, shard.row_align(cfg)) if sharding == "rows" else [(0, M)]
 
-    def gather_kstar(dst, src):     # Alg. 1's K* of every head (Hq int32) from all ranks
+    def gather_small(dst, src):      # Alg. 1's K* / budgets of every head (Hq x 4 B) from all ranks
         import torch.distributed as dist
 
         if same_dev:                 # gloo-only test mode: through host memory
@@ -366,46 +410,45 @@ def run_ours(args):
             dist.all_gather_into_tensor(dst, src)
 
     alg1_sharded = sharding == "rows" and ws > 1 and args.alg1 == "sharded"
-
-    # Alg. 1 has its own workspace: it runs concurrently with the chunks' score passes
+    # Alg. 1 has its own workspace: it runs concurrently with the chunks' score passes; the
+    # rank's two row chunks are estimated concurrently (own workspace and stream each)
     alg1_ws = pa.alloc_workspace(cfg, dev) if alg1_sharded else None
-
-    def alg1():                      # head-sharded Alg. 1 + all-gather of K* (eager: a collective)
-        shard.budgets_sharded(cfg, Ql, Kl, ws, rank, alg1_ws, all_gather=gather_kstar, out=(kstar, budget))
-
-    # the rank's two row chunks are estimated concurrently (own workspace and stream each)
     est_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if alg1_sharded else None
     est_ws = [wsp, pa.alloc_workspace(cfg, dev)] if alg1_sharded else None
+    aux_st = torch.cuda.Stream(dev) if alg1_sharded else None
+    outs = (kstar, budget, cnt, idx)
+
+    def estimate_overlapped(run_scores=None, run_select=None):
+        shard.estimate_rows_overlapped(cfg, Ql, Kl, my_rows, ws, rank, est_ws, outs, alg1_workspace=alg1_ws,
+                                       aux_stream=aux_st, streams=est_streams, all_gather=gather_small,
+                                       run_scores=run_scores, run_select=run_select)
 
     def scores():                    # alg1_sharded: the chunks' A1-A3, K* not needed yet
-        shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx), kstar_given=True,
+        shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=outs, kstar_given=True,
                             streams=est_streams, workspaces=est_ws, scores_only=True)
 
     def select_lists():              # alg1_sharded: A5-A6 of the chunks once K* is gathered
         shard.select_rows(cfg, my_rows, est_ws, kstar, (cnt, idx))
 
-    aux_st = torch.cuda.Stream(dev) if alg1_sharded else None
-
-    def estimate_overlapped(run_scores, run_select):
-        # the chunks' score passes on a side stream while this stream runs the head-sharded
-        # Alg. 1 and the K* all-gather; selection after both
-        cur = torch.cuda.current_stream(dev)
-        aux_st.wait_stream(cur)
-        with torch.cuda.stream(aux_st):
-            run_scores()
-        alg1()
-        cur.wait_stream(aux_st)
-        run_select()
-
     def estimate():
         if alg1_sharded:
-            estimate_overlapped(scores, select_lists)
+            estimate_overlapped()
         elif sharding == "rows" and ws > 1:   # lists of this rank's rows only
-            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=(kstar, budget, cnt, idx))
+            shard.estimate_rows(cfg, Ql, Kl, my_rows, wsp, out=outs)
         elif sharding == "rows":
-            pa.estimate(cfg, Ql, Kl, wsp, out=(kstar, budget, cnt, idx))
+            pa.estimate(cfg, Ql, Kl, wsp, out=outs)
         else:                    # g < #ranks: pool -> NCCL all-reduce of pooled sums
-            shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=(kstar, budget, cnt, idx))
+            shard.estimate_sharded(cfg, Ql, Kl, ws, wsp, out=outs, all_reduce=all_reduce)
+
+    def all_reduce(t):
+        import torch.distributed as dist
+
+        if same_dev:                 # gloo-only test mode: through host memory
+            c = t.cpu()
+            dist.all_reduce(c)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t)
 
     def prefill():
         if sharding == "rows" and ws > 1:
@@ -469,14 +512,13 @@ def run_ours(args):
     est_ms = [e[0].elapsed_time(e[1]) for e in ev]
     att_ms = [e[1].elapsed_time(e[2]) for e in ev]
     step_ms = [a + b for a, b in zip(est_ms, att_ms)]
-    total_ms = float(np.sum(step_ms))
 
     # dense baseline (same run, same inputs), fewer iterations
     # (launched on `st`, the stream the events are recorded on)
     dense_ms = []
     Od = torch.empty_like(Ql)
     with torch.cuda.stream(st):
-        for i in range(args.warmup + max(2, args.steps // 2)):
+        for i in range(args.warmup + max(3, args.steps // 2)):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
@@ -489,18 +531,25 @@ def run_ours(args):
             torch.cuda.synchronize()
             if i >= args.warmup:
                 dense_ms.append(e0.elapsed_time(e1))
-    dense = float(np.mean(dense_ms))
+    dense = float(np.median(dense_ms))
 
-    # context only: a library dense kernel on the same inputs (torch SDPA, cuDNN backend
-    # first, then FlashAttention), so "speedup vs dense" can be read against a vendor kernel
+    # a library dense kernel on the same inputs (torch SDPA, cuDNN backend first, then
+    # FlashAttention): the speedup is quoted against the faster of it and our own dense
     lib_dense = None
     if ws == 1 and not args.no_lib_dense:
-        lib_dense = library_dense(Ql, Kl, Vl, cfg.r, st, flush, args.warmup, max(2, args.steps // 2))
+        lib_dense = library_dense(Ql, Kl, Vl, cfg.r, st, flush, args.warmup, max(3, args.steps // 2))
     del Od
 
-    # max over ranks
-    vec = torch.tensor([total_ms / args.steps, float(np.mean(est_ms)), float(np.mean(att_ms)), dense],
-                       dtype=torch.float64)
+    # estimation-latency comparison (Fig. 6b analogue): the seq-avgpool
+    # comparator's estimate (same Alg. 1 and Eq. 3 selection, per-head
+    # avgpool maps) against the proxy estimate timed above, both over the same-run dense time
+    est_cmp = None
+    if ws == 1 and not args.no_comparator:
+        est_cmp = comparator_latency(pa, cfg, Ql, Kl, st, flush, args.warmup, max(3, args.steps // 2))
+
+    # max over ranks of the per-rank medians (device-timed, CUDA events)
+    vec = torch.tensor([float(np.median(step_ms)), float(np.median(est_ms)), float(np.median(att_ms)), dense,
+                        float(np.mean(step_ms))], dtype=torch.float64)
     sel_blocks = float(sum(cnt[:, b:e].sum().item() for b, e in my_rows))
     blocks_t = torch.tensor([sel_blocks], dtype=torch.float64)
     per_rank_blocks = [sel_blocks]
@@ -511,8 +560,15 @@ def run_ours(args):
         parts = [torch.empty_like(blocks_t) for _ in range(ws)]
         dist.all_gather(parts, blocks_t, group=cpu_group)
         per_rank_blocks = [float(p.item()) for p in parts]
-    layer_ms, est_m, att_m, dense_m = vec.tolist()
+    layer_ms, est_m, att_m, dense_m, layer_mean = vec.tolist()
     total_blocks = float(sum(per_rank_blocks))
+
+    # N > 1: gather every rank's outputs over NCCL and compare them with a single-GPU run of
+    # the same layer on rank 0 (after timing; not part of the step)
+    verified = None
+    if ws > 1:
+        verified = verify_sharded(pa, shard, cfg, w, sharding, Q, K, V, outs, O, my_rows, ws, rank, dev,
+                                  same_dev)
 
     # e2e through the C-ABI host path (H2D of Q/K/V and D2H of O inside the timed region)
     e2e = None
@@ -527,14 +583,14 @@ def run_ours(args):
         dws = torch.empty(pa.forward_host_workspace_bytes(cfg), dtype=torch.uint8, device=dev)
         pa.forward_host(cfg, Qh, Kh, Vh, Oh, dws, ksh)
         ts = []
-        for _ in range(max(2, args.steps // 2)):
+        for _ in range(max(3, args.steps // 2)):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             pa.forward_host(cfg, Qh, Kh, Vh, Oh, dws, ksh)
             ts.append((time.perf_counter() - t0) * 1e3)
         h2d = (Qh.numel() + Kh.numel() + Vh.numel()) * 2
         d2h = Oh.numel() * 2 + ksh.numel() * 4
-        e2e = {"value": float(np.mean(ts)), "unit": "ms", "h2d_bytes_per_step": h2d,
+        e2e = {"value": float(np.median(ts)), "unit": "ms", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
         del dws
     elif ws > 1 and not args.no_e2e and w["n_kv_heads"] % ws == 0:
@@ -552,23 +608,14 @@ def run_ours(args):
         del wsp
         torch.cuda.empty_cache()
         hws = pa.alloc_workspace(hcfg, dev)
-
-        def ar(t):
-            if same_dev:            # gloo-only test mode: through host memory
-                c = t.cpu()
-                dist.all_reduce(c)
-                t.copy_(c)
-            else:
-                dist.all_reduce(t)
-
-        shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=ar)
+        shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=all_reduce)
         ts = []
-        for _ in range(max(2, args.steps // 2)):
+        for _ in range(max(3, args.steps // 2)):
             barrier()
             t0 = time.perf_counter()
-            shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=ar)
+            shard.forward_host_sharded(hcfg, Qh, Kh, Vh, Oh, ws, hws, all_reduce=all_reduce)
             ts.append((time.perf_counter() - t0) * 1e3)
-        tv = torch.tensor([float(np.mean(ts))], dtype=torch.float64)
+        tv = torch.tensor([float(np.median(ts))], dtype=torch.float64)
         dist.all_reduce(tv, op=dist.ReduceOp.MAX, group=cpu_group)
         h2d = (Qh.numel() + Kh.numel() + Vh.numel()) * 2 * ws
         d2h = Oh.numel() * 2 * ws
@@ -590,11 +637,10 @@ def run_ours(args):
     b, d = w["block_size"], w["head_dim"]
     flops_exec = 4.0 * b * b * d * max(per_rank_blocks)    # the slowest rank's attention
     pk = peaks()
-    peak_t = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak_burst = pk["bf16_tflops"]
+    peak_sus = pk.get("bf16_tflops_sustained", peak_burst)
     achieved = flops_exec / (att_m * 1e-3) / 1e12
-    kname = {"3": "attn_tc_kernel", "4": "attn_tc4_kernel", "5": "attn_tc5_kernel",
-             "6": "attn_tc6_kernel", "7": "attn_tc7_kernel", "8": "attn_tc8_kernel"}.get(
-                 os.environ.get("PROXYATTN_ATTN", "8")[:1], "attn_tc8_kernel")
+    kname = "attn_tc8_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
@@ -605,8 +651,17 @@ def run_ours(args):
     cpu = None
     if ws == 1 and not args.no_cpu:
         ms, sample, cores, parts = oracle_sample(w, Q.cpu(), K.cpu(), V.cpu())
-        cpu = {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample}
+        ms1, sample1, _, _ = oracle_sample(w, Q.cpu(), K.cpu(), V.cpu(), threads=1, scale=0.125)
+        cpu = {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle", "sample": sample,
+               "value_1thread": ms1, "sample_1thread": sample1, "host_cpu": host_cpu()}
     clocks = getattr(clk, "result", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []})
+    # the dense denominator: the faster of our dense kernel (A8) and the library's
+    dense_ref, dense_ref_kernel = dense_m, "proxyattn_dense_prefill (A8, this library)"
+    if lib_dense and lib_dense["ms"] < dense_ref:
+        dense_ref, dense_ref_kernel = lib_dense["ms"], lib_dense["kernel"]
+    n_units = len(my_rows)
+    launches_pre = 2 + (1 if cfg.Hl // cfg.r > 1 else 0) + (1 if b == 64 else 0)   # fast + exact (+ kv order, pair union)
+    launches_est = ESTIMATE_KERNELS + 4 * (n_units - 1 if ws > 1 and sharding == "rows" else 0)
     line = {
         "metric": METRIC,
         "value": layer_ms,
@@ -620,44 +675,43 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (structured generator, SURVEY §8d; seed 0; inputs resident in HBM)",
-        "config": {"workload": w["name"], "heads": f"{w['n_q_heads']}/{w['n_kv_heads']}",
-                   "preset": w["preset"],
-                   "head_dim": d, "seq_len": w["seq_len"], "block": b, "stride": w["stride"],
-                   "proxy_groups": w["n_groups"], "gamma": w["gamma"],
-                   "min_budget_tokens": w["min_budget_tokens"],
-                   "parallelism": (f"zig-zag block rows x{ws}" + (", Alg. 1 head-sharded + all-gather of K*"
-                                                                  if alg1_sharded else "")
-                                   if sharding == "rows" else f"kv-head groups x{ws}") if ws > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "launch": "CUDA graphs (estimate, prefill)" if use_graph else "eager"},
-        "speedup_vs_dense": dense_m / layer_ms,
+        "config": bench_config(w, ws, parallelism_of(ws, sharding, args.alg1)),
+        "statistic": "median of the timed steps (max over ranks); mean_ms alongside",
+        "mean_ms": layer_mean,
+        "launch": "CUDA graphs (estimate, prefill)" if use_graph else "eager",
+        # speedup against the faster dense kernel of the same run (ours or the library's)
+        "speedup_vs_dense": dense_ref / layer_ms,
+        "dense_baseline": {"ms": dense_ref, "kernel": dense_ref_kernel},
         "dense_ms": dense_m,
+        "speedup_vs_own_dense": dense_m / layer_ms,
         # A8's algorithmic FLOP (every causal block whole) over the library kernel's time
         "dense_library": (dict(lib_dense, speedup_vs_library=lib_dense["ms"] / layer_ms,
                                tflops=4.0 * b * b * d * dense_blocks / (lib_dense["ms"] * 1e-3) / 1e12)
                           if lib_dense else None),
+        "dense_tflops": 4.0 * b * b * d * dense_blocks / ws / (dense_m * 1e-3) / 1e12,
         "estimate_ms": est_m,
         "prefill_ms": att_m,
         # estimation cost relative to the same-run dense attention (the paper's "< 10 %",
         # P:614-615; cost model g/(n s^2) = 0.20 % here, Alg. 1 adds about as much, Z22)
         "estimate_over_dense": est_m / dense_m,
+        "estimation_latency": est_cmp,
         "sparsity": sparsity,
         "tflops_exec": achieved,
         "roofline": {"bound": "tensor", "kernel": f"{kname} (A7)", "achieved": achieved,
-                     "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
+                     "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst,
                      "traffic": traffic,
-                     "peak_source": pk["_source"] + " bf16_tflops_sustained",
+                     "peak_source": pk["_source"] + " bf16_tflops (burst)",
+                     "frac_sustained": achieved / peak_sus, "peak_sustained": peak_sus,
                      "algorithmic": f"4*b^2*d FLOP per executed (head,row,block) = {4 * b * b * d / 1e6:.2f} MFLOP"},
         "work_share": [x / total_blocks for x in per_rank_blocks],
+        "verified": verified,
         "cpu_baseline": cpu,
         "e2e": e2e,
         # attn_tc8 is two launches per prefill call: the fast pass and the exact re-run of
-        # the rows it flagged (an empty list at these inputs)
-        # estimate: 8 kernels (4 of them Alg. 1); a row-range estimate adds 4 per extra range
-        "gpu_launches": (ESTIMATE_KERNELS + 4 * (len(my_rows) - 1 if ws > 1 and sharding == "rows" else 0)
-                         + len(my_rows) * ((2 if kname == "attn_tc8_kernel" else 1)
-                                           + (1 if kname == "attn_tc8_kernel" and cfg.Hl // cfg.r > 1 else 0)  # kv order
-                                           + (1 if b == 64 else 0))) * args.steps,   # + pair union
+        # the rows it flagged (an empty list at these inputs), plus the KV-head order
+        # (and the row-pair union at b = 64); estimate: 8 kernels (4 of them Alg. 1), a
+        # row-range estimate adds 4 per extra range
+        "gpu_launches": (launches_est + n_units * launches_pre) * args.steps,
         "clocks": clocks,
         # the paper's own numbers, other hardware and workloads: context only
         "paper_context": {"attention_speedup_vs_flashattention": "up to 10.3x at 256K, H800 (P:586)",
@@ -669,6 +723,132 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def host_cpu() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs"
+
+
+def comparator_latency(pa, cfg, Q, K, st, flush, warmup, iters):
+    """Estimation latency of the seq-avgpool comparator (proxyattn_avgpool_estimate: block-mean
+    pooling of Q and K, per-head M x M score maps, the same Alg. 1 budgets and Eq. 3 selection)
+    and of its score map alone, on the same inputs and stream, CUDA-graph replay, median."""
+    ws = torch.empty(pa.avgpool_workspace_bytes(cfg), dtype=torch.uint8, device=Q.device)
+    Hl, M = cfg.Hl, cfg.M
+    out = (torch.empty(Hl, dtype=torch.int32, device=Q.device), torch.empty(Hl, device=Q.device),
+           torch.empty(Hl, M, dtype=torch.int32, device=Q.device),
+           torch.empty(Hl, M, M, dtype=torch.int32, device=Q.device))
+    res = {}
+    with torch.cuda.stream(st):
+        for name, fn in (("avgpool_estimate_ms", lambda: pa.avgpool_estimate(cfg, Q, K, ws, out)),
+                         ("avgpool_scores_ms", lambda: pa.avgpool_scores(cfg, Q, K, ws))):
+            fn()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                fn()
+            ts = []
+            for i in range(warmup + iters):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                g.replay()
+                e1.record(st)
+                torch.cuda.synchronize()
+                if i >= warmup:
+                    ts.append(e0.elapsed_time(e1))
+            res[name] = float(np.median(ts))
+            del g
+    sel = float(out[2].sum().item())
+    res["avgpool_sparsity"] = 1.0 - sel / (Hl * M * (M + 1) / 2)
+    res["note"] = ("seq-avgpool comparator (SPEC S:365-373) vs the proxy estimate; same Alg. 1 and "
+                   "Eq. 3 selection, per-head block-mean score maps (Fig. 6b analogue, P:615-652)")
+    del ws
+    torch.cuda.empty_cache()
+    return res
+
+
+def verify_sharded(pa, shard, cfg, w, sharding, Q, K, V, outs, O, my_rows, ws, rank, dev, same_dev):
+    """N > 1 verification (north_star: NCCL "to gather outputs for verification"): every
+    rank's K*, block lists and O are gathered to rank 0 over the default (NCCL) group and
+    compared with a single-GPU estimate + prefill of the whole layer on rank 0."""
+    import torch.distributed as dist
+
+    kstar, budget, cnt, idx = outs
+    M = cfg.M
+    H = w["n_q_heads"]
+    torch.cuda.synchronize()
+
+    def to_root(t):                   # sum-reduce (integer views: x + 0 == x bit for bit)
+        if same_dev:
+            c = t.cpu()
+            dist.reduce(c, 0)
+            t.copy_(c)
+        else:
+            dist.reduce(t, 0)
+    if sharding == "rows":
+        mask = torch.zeros(M, dtype=torch.bool, device=dev)
+        for b, e in my_rows:
+            mask[b:e] = True
+        c_full = torch.where(mask[None, :], cnt, torch.zeros_like(cnt))
+        valid = torch.arange(M, device=dev)[None, None, :] < cnt[:, :, None]
+        i_full = torch.where(mask[None, :, None] & valid, idx, torch.zeros_like(idx))
+        tok = mask.repeat_interleave(cfg.block_size)[:cfg.seq_len]
+        o_full = torch.where(tok[None, :, None], O, torch.zeros_like(O)).view(torch.int16).to(torch.int32)
+        k_all = kstar.clone()
+        for t in (c_full, i_full, o_full):
+            to_root(t)
+        parts = [torch.empty_like(k_all) for _ in range(ws)]
+        if same_dev:
+            cp = [p.cpu() for p in parts]
+            dist.all_gather(cp, k_all.cpu())
+            parts = [p.to(dev) for p in cp]
+        else:
+            dist.all_gather(parts, k_all)
+        kstar_ranks_equal = all(torch.equal(p, parts[0]) for p in parts)
+    else:                              # head shards: equal-size slices, all_gather
+        def gather(t):
+            ps = [torch.empty_like(t) for _ in range(ws)]
+            if same_dev:
+                cp = [p.cpu() for p in ps]
+                dist.all_gather(cp, t.cpu())
+                ps = [p.to(dev) for p in cp]
+            else:
+                dist.all_gather(ps, t.contiguous())
+            return torch.cat(ps, 0)
+        k_all = gather(kstar)
+        c_full = gather(cnt)
+        valid = torch.arange(M, device=dev)[None, None, :] < cnt[:, :, None]
+        i_full = gather(torch.where(valid, idx, torch.zeros_like(idx)))
+        o_full = gather(O.view(torch.int16).to(torch.int32))
+        kstar_ranks_equal = True
+    if rank != 0:
+        return None
+    full = cfg.replace(q_head_begin=0, q_head_end=0, row_begin=0, row_end=0)
+    k1, _, c1, i1 = pa.estimate(full, Q, K)
+    O1 = pa.prefill(full, Q, K, V, c1, i1)
+    v1 = torch.arange(M, device=dev)[None, None, :] < c1[:, :, None]
+    i1 = torch.where(v1, i1, torch.zeros_like(i1))
+    o1 = O1.view(torch.int16).to(torch.int32)
+    res = {"method": f"{'zig-zag rows' if sharding == 'rows' else 'head shards'}: rank outputs gathered to rank 0 "
+                     f"({'gloo' if same_dev else 'NCCL'}), compared with a 1-GPU run of the whole layer",
+           "nranks": ws, "kstar_equal": bool(torch.equal(k_all, k1)) and kstar_ranks_equal,
+           "lists_equal": bool(torch.equal(c_full, c1)) and bool(torch.equal(i_full, i1)),
+           "O_bitwise_equal": bool(torch.equal(o_full, o1))}
+    if not res["O_bitwise_equal"]:
+        of = o_full.to(torch.int16).view(torch.bfloat16).float()
+        res["O_max_abs_diff"] = float((of - O1.float()).abs().max().item())
+    res["list_rows_mismatched"] = int(((c_full != c1) | (i_full != i1).any(dim=2)).sum().item())
+    res["ok"] = res["kstar_equal"] and res["lists_equal"] and (res["O_bitwise_equal"] or
+                                                               res.get("O_max_abs_diff", 1.0) <= 2e-2)
+    del O1, i1, o1, o_full, i_full
+    torch.cuda.empty_cache()
+    return res
 
 
 def library_dense(Q, K, V, r, st, flush, warmup, iters):
@@ -695,7 +875,7 @@ def library_dense(Q, K, V, r, st, flush, warmup, iters):
                     torch.cuda.synchronize()
                     if i >= warmup:
                         ts.append(e0.elapsed_time(e1))
-            out = {"kernel": name, "ms": float(np.mean(ts))}
+            out = {"kernel": name, "ms": float(np.median(ts))}
             break
         except Exception as ex:   # backend unavailable for this shape / build
             out = {"kernel": name, "error": str(ex).splitlines()[0][:160]}
@@ -707,7 +887,7 @@ def library_dense(Q, K, V, r, st, flush, warmup, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seq-len", type=int, default=0, help="override N (sweep)")
@@ -724,6 +904,8 @@ def main():
     ap.add_argument("--no-lib-dense", action="store_true",
                     help="skip the library dense context timing (torch SDPA)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graphs)")
+    ap.add_argument("--no-comparator", action="store_true",
+                    help="skip the seq-avgpool comparator's estimation-latency record")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

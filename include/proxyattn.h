@@ -18,17 +18,22 @@
  *  - Element type: bf16 (__nv_bfloat16) by default; fp32 when PROXYATTN_FLAG_FP32_DEBUG.
  *  - Per-head outputs (kstar, budget, block_cnt, block_idx) are indexed by local head.
  *  - All work is enqueued on `stream` (a cudaStream_t, passed as void*); no call
- *    synchronises the host except proxyattn_forward_host.  proxyattn_estimate forks
- *    Alg. 1 onto a library-owned per-device stream and joins it back to `stream` by
- *    events before returning, so its completion is still ordered on `stream` (and the
- *    call is capturable in a CUDA graph); PROXYATTN_SERIAL_ESTIMATE=1 disables the fork.
+ *    synchronises the host except proxyattn_forward_host and the validation flags
+ *    (PROXYATTN_FLAG_CHECK, PROXYATTN_FLAG_CHECK_FINITE).  proxyattn_estimate forks Alg. 1
+ *    onto a library-owned helper stream and joins it back to `stream` by events before
+ *    returning, so its completion is still ordered on `stream` and the call is capturable
+ *    in a CUDA graph.  Helper streams are created once per (device, caller stream): calls
+ *    from different threads on different streams never share one.
  *  - Scratch comes from the caller's workspace.  The only memory the library allocates is
  *    the attention launch's scheduler state, once per (device, stream) on the first
  *    prefill / forward on that stream (work counter, KV-head order, the exact-launch row
- *    list: 20 bytes per work item, grown when a larger launch comes, kept until exit).
- *    Hence CUDA-graph capture: make one call on the capture stream first (as bench.py
- *    and tests/test_gpu_graphs.py do); every call is then asynchronous and capturable,
- *    including proxyattn_forward_varlen.
+ *    list: 20 bytes per work item).  When a later launch on that stream needs more items,
+ *    new arrays are made and the old ones are kept (never freed while the process lives),
+ *    so a graph captured earlier keeps valid pointers.  Hence CUDA-graph capture: make one
+ *    call on the capture stream first (as bench.py and tests/test_gpu_graphs.py do); every
+ *    call is then asynchronous and capturable, including proxyattn_forward_varlen.  Graphs
+ *    captured on one stream share its work counter: replay them in that stream's order, not
+ *    concurrently on other streams.
  *  - Return codes: PROXYATTN_OK or one of the negative PROXYATTN_E_* codes; a
  *    human-readable reason is available from proxyattn_last_error() (thread-local).
  *    Validation errors are raised before anything is enqueued.
@@ -98,6 +103,10 @@ typedef struct {
  * scores L stay in the workspace for proxyattn_select_ws (block_cnt / block_idx may be NULL).
  * Lets a caller overlap the scores with a K* exchange (multi-GPU) and select afterwards. */
 #define PROXYATTN_FLAG_SCORES_ONLY 0x80u
+/* Validation ("all values finite"; S:49 / S:319 "non-finite input -> validation error"):
+ * every call that reads Q / K / V first counts their NaN / Inf elements on the device,
+ * synchronises `stream` and returns PROXYATTN_E_NONFINITE (nothing else enqueued) if any. */
+#define PROXYATTN_FLAG_CHECK_FINITE 0x100u
 
 #define PROXYATTN_OK               0
 #define PROXYATTN_E_CONFIG        -1  /* divisibility, gamma range, shard alignment */
@@ -105,6 +114,7 @@ typedef struct {
 #define PROXYATTN_E_SHAPE         -3  /* invalid block list (empty, unsorted, out of range, acausal) */
 #define PROXYATTN_E_WORKSPACE     -4  /* workspace missing or too small                             */
 #define PROXYATTN_E_CUDA          -5  /* CUDA launch / runtime failure                              */
+#define PROXYATTN_E_NONFINITE     -6  /* NaN / Inf input, only with PROXYATTN_FLAG_CHECK_FINITE */
 
 /* ------------------------------------------------------------- workspace -- */
 
@@ -215,6 +225,31 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
                              void* workspace, size_t workspace_bytes, int32_t* kstar,
                              void* stream);
 
+/* ------------------------------------------------- seq-avgpool comparator -- */
+
+/* The coarse estimator the paper's granularity argument is measured against (SURVEY §8(f)
+ * rank 4; SPEC S:365-373 seq_avgpool_scores; paper §1 / §2.1 "pooling ... along the
+ * sequence dimension", Fig. 6b's estimation-latency comparison).  Per LOCAL
+ * query head h and block rows m, n (n <= m):
+ *   qbar_m = mean of block m's (real) query rows of head h, kbar_n = mean of block n's key
+ *   rows of kv(h); S_h[m][n] = log softmax_{n' <= m}(qbar_m . kbar_n' / sqrt(d)) at n,
+ *   -inf for n > m.
+ * The block sums are rounded once to bf16 (RNE of the exact sum; fp32 with FP32_DEBUG), the
+ * dots accumulate in fp32.  No row range (E_CONFIG); head_dim % 32 == 0; any GQA ratio; the
+ * shard may split proxy groups (everything is per head).  Workspace:
+ * proxyattn_avgpool_workspace_bytes.  S_out: DEVICE float [Hl][M][M]. */
+int proxyattn_avgpool_workspace_bytes(const proxyattn_cfg* cfg, size_t* out_bytes);
+int proxyattn_avgpool_scores(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                             void* workspace, size_t workspace_bytes, float* S_out, void* stream);
+/* The comparator's full estimate: the same Alg. 1 budgets as proxyattn_estimate (kstar an
+ * input with KSTAR_GIVEN; static_kstar honoured) and the same Eq. 3 row counts / selection
+ * rule (diagonal forced, ties to the lower index, ascending lists), but each head ranks the
+ * columns of its OWN map S_h.  Outputs as proxyattn_estimate. */
+int proxyattn_avgpool_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K,
+                               void* workspace, size_t workspace_bytes,
+                               int32_t* kstar, float* budget, int32_t* block_cnt, int32_t* block_idx,
+                               void* stream);
+
 /* ----------------------------------------------------------------- misc -- */
 
 /* §3.1 cost model: g / (Hq * s^2). */
@@ -232,11 +267,6 @@ const char* proxyattn_build_info(void);
  *   C_ts [128][128] = A · B    (A staged in TMEM via tcgen05.st, B MN-major in shared memory)
  * fp32 outputs.  Used by the GPU tests to pin the descriptor encodings. */
 int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream);
-
-/* Diagnostic: copies the per-event clock64 timeline recorded for one CTA of the last
- * attention launch when the process runs with PROXYATTN_TRACE=<cta index> (n entries of
- * [2 sides][256 iterations][2 slots][8 events]).  E_CONFIG when tracing is off. */
-int proxyattn_debug_trace(long long* host_out, size_t n);
 
 #ifdef __cplusplus
 }

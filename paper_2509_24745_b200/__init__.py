@@ -9,6 +9,9 @@ from ._lib import (  # noqa: F401
     Config,
     ProxyAttnError,
     alloc_workspace,
+    avgpool_estimate,
+    avgpool_scores,
+    avgpool_workspace_bytes,
     budgets,
     build_info,
     cost_ratio,

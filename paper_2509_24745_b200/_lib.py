@@ -23,6 +23,7 @@ FLAG_DESIGNATED_HEAD = 0x10
 FLAG_TOKEN_MAJOR = 0x20
 FLAG_KSTAR_GIVEN = 0x40
 FLAG_SCORES_ONLY = 0x80
+FLAG_CHECK_FINITE = 0x100
 
 OK = 0
 E_CONFIG = -1
@@ -30,6 +31,7 @@ E_UNSUPPORTED = -2
 E_SHAPE = -3
 E_WORKSPACE = -4
 E_CUDA = -5
+E_NONFINITE = -6
 
 
 class ProxyAttnError(RuntimeError):
@@ -88,6 +90,7 @@ class Config:
     token_major: bool = False       # Q/K/V/O as [N][heads][d] with token strides (0 = packed)
     q_token_stride: int = 0
     kv_token_stride: int = 0
+    check_finite: bool = False      # validate Q/K/V (NaN / Inf -> E_NONFINITE, S:49 / S:319)
 
     @property
     def M(self) -> int:
@@ -124,7 +127,8 @@ class Config:
                  | (FLAG_DESIGNATED_HEAD if self.designated_head else 0)
                  | (FLAG_TOKEN_MAJOR if self.token_major else 0)
                  | (FLAG_KSTAR_GIVEN if self.kstar_given else 0)
-                 | (FLAG_SCORES_ONLY if self.scores_only else 0))
+                 | (FLAG_SCORES_ONLY if self.scores_only else 0)
+                 | (FLAG_CHECK_FINITE if self.check_finite else 0))
         return _CCfg(self.n_q_heads, self.n_kv_heads, self.head_dim, self.seq_len,
                      self.block_size, self.stride, self.n_groups, float(self.gamma),
                      self.min_budget_tokens, flags, self.q_head_begin, self.q_head_end,
@@ -152,7 +156,9 @@ _SIGS = {
     "proxyattn_last_error": ([], ctypes.c_char_p),
     "proxyattn_build_info": ([], ctypes.c_char_p),
     "proxyattn_debug_umma": ([_P, _P, _P, _P, _P], ctypes.c_int),
-    "proxyattn_debug_trace": ([_P, ctypes.c_size_t], ctypes.c_int),
+    "proxyattn_avgpool_workspace_bytes": ([_CP, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "proxyattn_avgpool_scores": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P], ctypes.c_int),
+    "proxyattn_avgpool_estimate": ([_CP, _P, _P, _P, ctypes.c_size_t, _P, _P, _P, _P, _P], ctypes.c_int),
     "proxyattn_varlen_workspace_bytes": ([_CP, ctypes.c_int32, _P, ctypes.POINTER(ctypes.c_size_t)],
                                          ctypes.c_int),
     "proxyattn_forward_varlen": ([_CP, ctypes.c_int32, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P, _P],
@@ -184,21 +190,34 @@ def _check(rc: int) -> None:
         raise ProxyAttnError(rc, lib().proxyattn_last_error().decode())
 
 
-def _ptr(t: torch.Tensor | None):
+def _ptr(t: torch.Tensor | None, dtype: torch.dtype | None = None, cuda: bool = True):
     if t is None:
         return None
     if not t.is_contiguous():
         raise ValueError("tensors must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"expected a {dtype} tensor, got {t.dtype}")
+    if cuda and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _tptr(t: torch.Tensor | None, cfg: "Config"):
-    """Pointer of a Q/K/V/O tensor: contiguous head-major, or token-major [N][heads][d]
-    whose token stride is the one in cfg (rows of d contiguous elements)."""
-    if t is None or not cfg.token_major:
-        return _ptr(t)
+def _tptr(t: torch.Tensor | None, cfg: "Config", role: str = "q"):
+    """Pointer of a Q/K/V/O tensor (role "q" for Q / O, "kv" for K / V) in cfg's element type:
+    contiguous head-major, or token-major [N][heads][d] whose token stride is the one in cfg
+    (0 = packed: local heads x d) with rows of d contiguous elements."""
+    if t is None:
+        return None
+    if not cfg.token_major:
+        return _ptr(t, cfg.dtype)
+    if t.dtype != cfg.dtype or not t.is_cuda:
+        raise ValueError(f"expected a CUDA {cfg.dtype} tensor, got {t.dtype} on {t.device}")
     if t.dim() != 3 or t.stride(2) != 1 or (t.shape[1] > 1 and t.stride(1) != t.shape[2]):
         raise ValueError("token-major tensors must be [N][heads][d] with contiguous heads x d rows")
+    heads = cfg.Hl if role == "q" else cfg.Hl // cfg.r
+    want = (cfg.q_token_stride if role == "q" else cfg.kv_token_stride) or heads * cfg.head_dim
+    if t.shape[0] > 1 and t.stride(0) != want:
+        raise ValueError(f"{role} token stride {t.stride(0)} != the config's {want} (use with_strides)")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -235,6 +254,17 @@ def alloc_workspace(cfg: Config, device) -> torch.Tensor:
     return torch.empty(workspace_bytes(cfg), dtype=torch.uint8, device=device)
 
 
+def _check_out(cfg: Config, out, lists: bool = True) -> None:
+    """Shapes / dtypes / device of (kstar, budget, block_cnt, block_idx) output tensors."""
+    Hl, M = cfg.Hl, cfg.M
+    want = [((Hl,), torch.int32), ((Hl,), torch.float32), ((Hl, M), torch.int32), ((Hl, M, M), torch.int32)]
+    for k, (t, (shape, dt)) in enumerate(zip(out, want)):
+        if t is None and k >= 2 and not lists:
+            continue
+        if t is None or tuple(t.shape) != shape or t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"output {k} must be a contiguous CUDA {dt} tensor of shape {shape}")
+
+
 def estimate(cfg: Config, Q: torch.Tensor, K: torch.Tensor, workspace: torch.Tensor | None = None,
              out: tuple | None = None):
     """proxyattn_estimate -> (kstar [Hl] i32, budget [Hl] f32, block_cnt [Hl][M] i32,
@@ -248,8 +278,9 @@ def estimate(cfg: Config, Q: torch.Tensor, K: torch.Tensor, workspace: torch.Ten
                torch.empty(Hl, dtype=torch.float32, device=dev),
                torch.empty(Hl, M, dtype=torch.int32, device=dev),
                torch.empty(Hl, M, M, dtype=torch.int32, device=dev))
+    _check_out(cfg, out, lists=not cfg.scores_only)
     kstar, budget, cnt, idx = out
-    _check(lib().proxyattn_estimate(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(workspace),
+    _check(lib().proxyattn_estimate(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _ptr(workspace),
                                     workspace.numel(), _ptr(kstar), _ptr(budget), _ptr(cnt),
                                     _ptr(idx), _stream(dev)))
     return kstar, budget, cnt, idx
@@ -259,8 +290,11 @@ def prefill(cfg: Config, Q, K, V, block_cnt, block_idx, O=None):
     """proxyattn_prefill -> O [Hl][N][d]."""
     if O is None:
         O = _like_q(cfg, Q)
-    _check(lib().proxyattn_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg),
-                                   _ptr(block_cnt), _ptr(block_idx), _tptr(O, cfg), _stream(Q.device)))
+    if tuple(block_cnt.shape) != (cfg.Hl, cfg.M) or tuple(block_idx.shape) != (cfg.Hl, cfg.M, cfg.M):
+        raise ValueError("block lists must be [Hl][M] and [Hl][M][M]")
+    _check(lib().proxyattn_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _tptr(V, cfg, "kv"),
+                                   _ptr(block_cnt, torch.int32), _ptr(block_idx, torch.int32), _tptr(O, cfg),
+                                   _stream(Q.device)))
     return O
 
 
@@ -268,7 +302,7 @@ def dense_prefill(cfg: Config, Q, K, V, O=None):
     """proxyattn_dense_prefill -> O [Hl][N][d]."""
     if O is None:
         O = _like_q(cfg, Q)
-    _check(lib().proxyattn_dense_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg),
+    _check(lib().proxyattn_dense_prefill(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _tptr(V, cfg, "kv"),
                                          _tptr(O, cfg), _stream(Q.device)))
     return O
 
@@ -279,7 +313,7 @@ def pool(cfg: Config, Q, K):
     shape = (gl, cfg.Ns, cfg.head_dim)
     qsum = torch.empty(shape, dtype=torch.float32, device=Q.device)
     ksum = torch.empty_like(qsum)
-    _check(lib().proxyattn_pool(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(qsum), _ptr(ksum),
+    _check(lib().proxyattn_pool(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _ptr(qsum), _ptr(ksum),
                                 _stream(Q.device)))
     return qsum, ksum
 
@@ -300,7 +334,7 @@ def budgets(cfg: Config, Q, K, workspace=None):
         workspace = alloc_workspace(cfg, Q.device)
     kstar = torch.empty(cfg.Hl, dtype=torch.int32, device=Q.device)
     budget = torch.empty(cfg.Hl, dtype=torch.float32, device=Q.device)
-    _check(lib().proxyattn_budgets(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg), _ptr(workspace),
+    _check(lib().proxyattn_budgets(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _ptr(workspace),
                                    workspace.numel(), _ptr(kstar), _ptr(budget),
                                    _stream(Q.device)))
     return kstar, budget
@@ -318,6 +352,7 @@ def select(cfg: Config, L, kstar):
 def select_ws(cfg: Config, workspace, kstar, out):
     """proxyattn_select_ws: A5-A6 of rows [row_begin, row_end) from the L a scores_only
     estimate left in `workspace`; writes out = (block_cnt, block_idx)."""
+    _check_out(cfg, (kstar, torch.empty(cfg.Hl, device=kstar.device)) + tuple(out))
     cnt, idx = out
     _check(lib().proxyattn_select_ws(_cfg_ref(cfg), _ptr(workspace), workspace.numel(), _ptr(kstar),
                                      _ptr(cnt), _ptr(idx), _stream(workspace.device)))
@@ -332,8 +367,9 @@ def forward_host_workspace_bytes(cfg: Config) -> int:
 
 def forward_host(cfg: Config, Qh, Kh, Vh, Oh, device_ws, kstar_h=None):
     """proxyattn_forward_host on host (CPU, ideally pinned) tensors; synchronises."""
-    _check(lib().proxyattn_forward_host(_cfg_ref(cfg), _ptr(Qh), _ptr(Kh), _ptr(Vh), _ptr(Oh),
-                                        _ptr(kstar_h), _ptr(device_ws), device_ws.numel(),
+    h = dict(dtype=cfg.dtype, cuda=False)
+    _check(lib().proxyattn_forward_host(_cfg_ref(cfg), _ptr(Qh, **h), _ptr(Kh, **h), _ptr(Vh, **h), _ptr(Oh, **h),
+                                        _ptr(kstar_h, torch.int32, cuda=False), _ptr(device_ws), device_ws.numel(),
                                         _stream(device_ws.device)))
     return Oh
 
@@ -368,10 +404,45 @@ def forward_varlen(cfg: Config, cu_seqlens, Q, K, V, O=None, workspace=None, kst
     if kstar is None:
         kstar = torch.zeros(max(n, 1), cfg.Hl, dtype=torch.int32, device=Q.device)
     _check(lib().proxyattn_forward_varlen(_cfg_ref(cfg), n, ctypes.c_void_p(cu.data_ptr()),
-                                          _tptr(Q, cfg), _tptr(K, cfg), _tptr(V, cfg), _tptr(O, cfg),
+                                          _tptr(Q, cfg), _tptr(K, cfg, "kv"), _tptr(V, cfg, "kv"), _tptr(O, cfg),
                                           _ptr(workspace), workspace.numel(), _ptr(kstar),
                                           _stream(Q.device)))
     return O, kstar[:n]
+
+
+def avgpool_workspace_bytes(cfg: Config) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().proxyattn_avgpool_workspace_bytes(_cfg_ref(cfg), ctypes.byref(n)))
+    return n.value
+
+
+def avgpool_scores(cfg: Config, Q, K, workspace=None):
+    """proxyattn_avgpool_scores -> S [Hl][M][M] fp32: the seq-avgpool comparator's per-head
+    log-domain block scores, -inf above the diagonal."""
+    if workspace is None:
+        workspace = torch.empty(avgpool_workspace_bytes(cfg), dtype=torch.uint8, device=Q.device)
+    S = torch.empty(cfg.Hl, cfg.M, cfg.M, dtype=torch.float32, device=Q.device)
+    _check(lib().proxyattn_avgpool_scores(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _ptr(workspace),
+                                          workspace.numel(), _ptr(S), _stream(Q.device)))
+    return S
+
+
+def avgpool_estimate(cfg: Config, Q, K, workspace=None, out: tuple | None = None):
+    """proxyattn_avgpool_estimate -> (kstar, budget, block_cnt, block_idx), the comparator's
+    selection (the same Alg. 1 budgets and Eq. 3 rule on per-head avgpool maps)."""
+    dev = Q.device
+    if workspace is None:
+        workspace = torch.empty(avgpool_workspace_bytes(cfg), dtype=torch.uint8, device=dev)
+    if out is None:
+        Hl, M = cfg.Hl, cfg.M
+        out = (torch.empty(Hl, dtype=torch.int32, device=dev), torch.empty(Hl, dtype=torch.float32, device=dev),
+               torch.empty(Hl, M, dtype=torch.int32, device=dev), torch.empty(Hl, M, M, dtype=torch.int32, device=dev))
+    _check_out(cfg, out)
+    kstar, budget, cnt, idx = out
+    _check(lib().proxyattn_avgpool_estimate(_cfg_ref(cfg), _tptr(Q, cfg), _tptr(K, cfg, "kv"), _ptr(workspace),
+                                            workspace.numel(), _ptr(kstar), _ptr(budget), _ptr(cnt), _ptr(idx),
+                                            _stream(dev)))
+    return kstar, budget, cnt, idx
 
 
 def cost_ratio(cfg: Config) -> float:

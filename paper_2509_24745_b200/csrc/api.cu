@@ -5,12 +5,16 @@
 #include <algorithm>
 #include <climits>
 #include <cstdarg>
+#include <initializer_list>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/proxyattn.h"
 #include "common.cuh"
@@ -19,6 +23,16 @@
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range per method stage: host-side ranges around each stage's launches, so
+// a profiler attributes kernels to A1-A8 (nvtx3 is header-only and costs nothing when no
+// tool is attached).
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -43,7 +57,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 constexpr int kMaxBlocks = 16384;
 
 // O1: validate the config and derive every size the kernels need.
-int derive(const proxyattn_cfg* c, pa::Dims& D) {
+int derive(const proxyattn_cfg* c, pa::Dims& D, bool limit_m = true) {
     if (!c) return fail(PROXYATTN_E_CONFIG, "cfg is NULL");
     if (c->n_q_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 || c->seq_len <= 0 ||
         c->block_size <= 0 || c->stride <= 0 || c->n_groups <= 0)
@@ -69,7 +83,7 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
     }
     // A4/A6 sort one head's / one row's M block scores in shared memory (next_pow2(M) x 12 B
     // <= 227 KB): M <= 16384, i.e. N <= 2M tokens at b = 128, 1M at b = 64
-    if ((c->seq_len + c->block_size - 1) / c->block_size > kMaxBlocks)
+    if (limit_m && (c->seq_len + c->block_size - 1) / c->block_size > kMaxBlocks)
         return fail(PROXYATTN_E_UNSUPPORTED, "seq_len / block_size > %d blocks", kMaxBlocks);
     D.Hq = c->n_q_heads;
     D.Hkv = c->n_kv_heads;
@@ -125,24 +139,6 @@ int derive(const proxyattn_cfg* c, pa::Dims& D) {
 
 }  // namespace
 
-namespace pa {
-// A7 kernel variant.  Sparse prefill: 8 = attn_tc8 (persistent attn_tc7: rows pulled from
-// an atomic counter, next row's loads/S/softmax overlapping the previous row's tail; default),
-// 7 = attn_tc7 (one row per CTA, two key-block streams sharing one O under a fixed per-row
-// softmax reference), 6 = attn_tc6 (two independent streams with online rescaling), 3 =
-// attn_tc (two rows per CTA sharing K/V tiles), 4 / 5 = experimental.  Dense prefill: 3.
-// PROXYATTN_ATTN=3..8 overrides both.
-int attn_variant(bool dense) {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PROXYATTN_ATTN");
-        v = (e && e[0] >= '3' && e[0] <= '8') ? e[0] - '0' : 0;
-    }
-    if (v) return v;
-    return dense ? 3 : 8;
-}
-}  // namespace pa
-
 namespace {
 
 bool groups_complete(const pa::Dims& D) { return D.qb % D.gq == 0 && D.qe % D.gq == 0; }
@@ -184,14 +180,28 @@ int run_budgets(const pa::Dims& D, const void* Q, const void* K, void* ws, const
     return PROXYATTN_OK;
 }
 
-// Per-device auxiliary stream of proxyattn_estimate (non-blocking, created once): Alg. 1
-// runs on it concurrently with A1-A3 (fork / join by events, so the pair stays capturable
-// in a CUDA graph).  PROXYATTN_SERIAL_ESTIMATE=1 keeps everything on the caller's stream.
+// Library-owned helper streams (non-blocking), one set per (device, CALLER stream): work a
+// call forks onto them is joined back to the caller's stream by events, so a graph captured
+// on one caller stream never pulls in work of another thread using another stream.  Kinds:
+// 0 = Alg. 1 of proxyattn_estimate (concurrent with A1-A3), 1 / 2 = the host path's upload /
+// download streams, 3 = the second estimate stream of the packed varlen path.
+int helper_stream(cudaStream_t caller, int kind, cudaStream_t* out) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, int>, cudaStream_t> streams;
+    int dev = 0;
+    PA_CUDA(cudaGetDevice(&dev), "get device");
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& s = streams[{dev, caller, kind}];
+    if (!s) PA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    *out = s;
+    return PROXYATTN_OK;
+}
+
+// fork / join events of the calling thread on the current device (reused: record -> wait
+// pairs are ordered on the host, and nothing is created or destroyed inside a capture)
 struct AuxEvents {
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-// fork / join events of the calling thread on the current device (reused: record -> wait
-// pairs are ordered on the host, and nothing is created or destroyed inside a capture)
 int estimate_events(AuxEvents* out) {
     thread_local std::map<int, AuxEvents> per_dev;
     int dev = 0;
@@ -205,24 +215,31 @@ int estimate_events(AuxEvents* out) {
     return PROXYATTN_OK;
 }
 
-int estimate_aux(cudaStream_t* aux) {
-    static std::mutex mu;
-    static std::map<int, cudaStream_t> per_dev;
-    static int serial = -1;
-    if (serial < 0) {
-        const char* e = getenv("PROXYATTN_SERIAL_ESTIMATE");
-        serial = (e && e[0] == '1') ? 1 : 0;
+// CHECK_FINITE ("all values finite"; "non-finite input -> validation error"):
+// counts NaN / Inf elements of the listed tensors on the device, synchronises the stream and
+// returns E_NONFINITE when any is found.  `q_role` tensors use the Q / O layout, the others K / V.
+int check_finite(const pa::Dims& D, cudaStream_t st, std::initializer_list<std::pair<const void*, bool>> ts) {
+    if (!(D.flags & PROXYATTN_FLAG_CHECK_FINITE)) return PROXYATTN_OK;
+    int* bad = nullptr;
+    PA_CUDA(cudaMallocAsync(&bad, sizeof(int), st), "check alloc");
+    PA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st), "check memset");
+    for (const auto& t : ts) {
+        if (!t.first) continue;
+        const bool q = t.second;
+        const long long heads = q ? D.Hl : D.Hkvl;
+        cudaError_t e = D.tok ? pa::launch_count_nonfinite(t.first, D.fp32, D.N, heads * D.d, q ? D.q_ts : D.kv_ts,
+                                                           bad, st)
+                              : pa::launch_count_nonfinite(t.first, D.fp32, 1, heads * D.N * D.d, 0, bad, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(bad, st);
+            return cuda_fail(e, "count_nonfinite");
+        }
     }
-    if (serial) {
-        *aux = nullptr;
-        return PROXYATTN_OK;
-    }
-    int dev = 0;
-    PA_CUDA(cudaGetDevice(&dev), "get device");
-    std::lock_guard<std::mutex> lock(mu);
-    cudaStream_t& s = per_dev[dev];
-    if (!s) PA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
-    *aux = s;
+    int hbad = 0;
+    PA_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "check copy");
+    PA_CUDA(cudaFreeAsync(bad, st), "check free");
+    PA_CUDA(cudaStreamSynchronize(st), "check sync");
+    if (hbad) return fail(PROXYATTN_E_NONFINITE, "%d non-finite input elements (S:49, S:319)", hbad);
     return PROXYATTN_OK;
 }
 
@@ -245,6 +262,7 @@ int proxyattn_pool(const proxyattn_cfg* cfg, const void* Q, const void* K, float
     int rc = derive(cfg, D);
     if (rc) return rc;
     if (!Q || !K || !qsum || !ksum) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    if ((rc = check_finite(D, S(stream), {{Q, true}, {K, false}}))) return rc;
     PA_CUDA(pa::launch_pool(D, Q, K, qsum, ksum, nullptr, nullptr, S(stream)), "pool");
     return PROXYATTN_OK;
 }
@@ -271,6 +289,7 @@ int proxyattn_budgets(const proxyattn_cfg* cfg, const void* Q, const void* K, vo
     const pa::Workspace W = pa::workspace_layout(D);
     if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
     if (!Q || !K || !kstar || !budget) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    if ((rc = check_finite(D, S(stream), {{Q, true}, {K, false}}))) return rc;
     return run_budgets(D, Q, K, ws, W, kstar, budget, S(stream));
 }
 
@@ -301,6 +320,7 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
     if (!Q || !K || !kstar || !budget || (!scores_only && (!block_cnt || !block_idx)))
         return fail(PROXYATTN_E_SHAPE, "NULL pointer");
     cudaStream_t st = S(stream);
+    if ((rc = check_finite(D, st, {{Q, true}, {K, false}}))) return rc;
     void* Pq = at<char>(ws, W.pq);
     void* Pk = at<char>(ws, W.pk);
     float* L = at<float>(ws, W.L);
@@ -322,27 +342,36 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, v
     const bool alg1 = !(D.flags & PROXYATTN_FLAG_KSTAR_GIVEN);
     cudaStream_t aux = nullptr;
     if (alg1 && pa::score_tc_supported(D) && D.static_kstar == 0) {
-        if ((rc = estimate_aux(&aux))) return rc;
+        if ((rc = helper_stream(st, 0, &aux))) return rc;
     }
     AuxEvents ev{};
     if (aux) {
         if ((rc = estimate_events(&ev))) return rc;
         PA_CUDA(cudaEventRecord(ev.fork, st), "record");
         PA_CUDA(cudaStreamWaitEvent(aux, ev.fork, 0), "wait");
+        Nvtx r("A4 Alg. 1 budgets");
         rc = run_budgets(D, Q, K, ws, W, kstar, budget, aux);
         if (rc) return rc;
         PA_CUDA(cudaEventRecord(ev.join, aux), "record");
     }
-    PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st, q_i0, i_end), "pool");
-    rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st, tr0, tr1);
-    if (rc) return rc;
+    {
+        Nvtx r("A1 pool + stride");
+        PA_CUDA(pa::launch_pool(D, Q, K, nullptr, nullptr, Pq, Pk, st, q_i0, i_end), "pool");
+    }
+    {
+        Nvtx r("A2-A3 proxy scores");
+        rc = run_proxy_from_pooled(D, Pq, Pk, ws, W, L, st, tr0, tr1);
+        if (rc) return rc;
+    }
     if (aux) {
         PA_CUDA(cudaStreamWaitEvent(st, ev.join, 0), "wait");
     } else if (alg1) {
+        Nvtx r("A4 Alg. 1 budgets");
         rc = run_budgets(D, Q, K, ws, W, kstar, budget, st);
         if (rc) return rc;
     }
     if (scores_only) return PROXYATTN_OK;   // L stays in the workspace (proxyattn_select_ws)
+    Nvtx r("A5-A6 select");
     PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, st), "select");
     return PROXYATTN_OK;
 }
@@ -355,6 +384,7 @@ int proxyattn_select_ws(const proxyattn_cfg* cfg, const void* ws, size_t ws_byte
     const pa::Workspace W = pa::workspace_layout(D);
     if (!ws || ws_bytes < W.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", W.total);
     if (!kstar || !block_cnt || !block_idx) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    Nvtx r("A5-A6 select");
     const float* L = reinterpret_cast<const float*>(static_cast<const char*>(ws) + W.L);
     PA_CUDA(pa::launch_select(D, L, kstar, block_cnt, block_idx, S(stream)), "select");
     return PROXYATTN_OK;
@@ -378,34 +408,14 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
         PA_CUDA(cudaStreamSynchronize(st), "check sync");
         if (hbad) return fail(PROXYATTN_E_SHAPE, "%d block rows violate the list contract (S:319)", hbad);
     }
-    if (D.fp32) {
+    if ((rc = check_finite(D, st, {{Q, true}, {K, false}, {V, false}}))) return rc;
+    Nvtx r(block_cnt ? "A7 block-sparse attention" : "A8 dense attention");
+    if (D.fp32)
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
-    } else {
-        int variant = pa::attn_variant(block_cnt == nullptr);
-        // only the persistent kernel reads token-major tensors (3-D TMA maps) and has the
-        // d = 64 / b = 64 instantiations
-        const bool only8 = D.tok || D.d != 128 || D.b != 128;
-        if (only8) {
-            if (block_cnt == nullptr) variant = 8;
-            if (variant != 8)
-                return fail(PROXYATTN_E_UNSUPPORTED,
-                            "token-major layouts and head_dim / block_size 64 need attention variant 8");
-        }
-        if ((variant == 4 || variant == 5) && (D.N % D.b || D.rb != 0 || D.re != D.M))
-            return fail(PROXYATTN_E_UNSUPPORTED, "attention variants 4/5 need seq_len %% 128 == 0 and all rows");
-        if (variant == 4)
-            PA_CUDA(pa::launch_attn_tc4(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc4");
-        else if (variant == 5)
-            PA_CUDA(pa::launch_attn_tc5(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc5");
-        else if (variant == 6)
-            PA_CUDA(pa::launch_attn_tc6(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc6");
-        else if (variant == 7)
-            PA_CUDA(pa::launch_attn_tc7(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc7");
-        else if (variant == 8)
-            PA_CUDA(pa::launch_attn_tc8(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc8");
-        else
-            PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc");
-    }
+    else if (block_cnt == nullptr && !D.tok && D.d == 128 && D.b == 128)
+        PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc dense");
+    else
+        PA_CUDA(pa::launch_attn_tc8(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc8");
     return PROXYATTN_OK;
 }
 
@@ -459,26 +469,6 @@ int proxyattn_forward_host_workspace_bytes(const proxyattn_cfg* cfg, size_t* out
     return PROXYATTN_OK;
 }
 
-// Auxiliary streams of the host path (created once per device, non-blocking): one for the
-// V uploads, one for the O downloads, so PCIe traffic in both directions overlaps compute.
-struct HostStreams {
-    cudaStream_t up = nullptr, down = nullptr;
-};
-static int host_streams(HostStreams& hs) {
-    static std::mutex mu;
-    static std::map<int, HostStreams> per_dev;
-    int dev = 0;
-    PA_CUDA(cudaGetDevice(&dev), "get device");
-    std::lock_guard<std::mutex> lock(mu);
-    HostStreams& h = per_dev[dev];
-    if (!h.up) {
-        PA_CUDA(cudaStreamCreateWithFlags(&h.up, cudaStreamNonBlocking), "stream create");
-        PA_CUDA(cudaStreamCreateWithFlags(&h.down, cudaStreamNonBlocking), "stream create");
-    }
-    hs = h;
-    return PROXYATTN_OK;
-}
-
 int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void* Kh, const void* Vh,
                            void* Oh, int32_t* kstar_h, void* dws, size_t dws_bytes, void* stream) {
     pa::Dims D;
@@ -490,6 +480,8 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     const HostLayout H = host_layout(D);
     if (!dws || dws_bytes < H.total) return fail(PROXYATTN_E_WORKSPACE, "device workspace needs %zu bytes", H.total);
     if (!Qh || !Kh || !Vh || !Oh) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    if (D.flags & PROXYATTN_FLAG_CHECK_FINITE)
+        return fail(PROXYATTN_E_CONFIG, "forward_host: validate the inputs with a device call (CHECK_FINITE)");
     cudaStream_t st = S(stream);
     const size_t el = D.fp32 ? 4 : 2;
     const size_t kb = kv_bytes(D);
@@ -503,33 +495,37 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     // pairs), so every chunk's lists and outputs equal the one-shot call's bit for bit.
     const int align = std::max(D.b == 64 ? 2 : 1, std::max(1, 128 / D.bs));
     const int units = (D.M + align - 1) / align;
-    static int want = -1;          // PROXYATTN_HOST_CHUNKS overrides the 16 row chunks (128K:
-    if (want < 0) {                // 1 / 4 / 8 / 16 / 24 chunks -> 63.5 / 41.2 / 37.3 / 35.8 / 35.8 ms)
-        const char* e = getenv("PROXYATTN_HOST_CHUNKS");
-        want = e ? std::max(1, atoi(e)) : 16;
-    }
-    const int n_ch = std::max(1, std::min(want, units));
-    // order: PROXYATTN_HOST_ORDER=fwd processes the FIRST rows first (K and the last Q block
-    // up front for Alg. 1, then V and Q chunk by chunk in row order: each chunk needs only the
-    // keys / values before its rows); the default processes the last (heaviest) rows first
-    static int fwd = -1;
-    if (fwd < 0) {
-        const char* e = getenv("PROXYATTN_HOST_ORDER");
-        fwd = (e && e[0] == 'f') ? 1 : 0;
-    }
-    std::vector<std::pair<int, int>> ch;                  // [r0, r1) block rows in processing order
+    // 16 row chunks (128K: 1 / 4 / 8 / 16 / 24 chunks -> 63.5 / 41.2 / 37.3 / 35.8 / 35.8 ms)
+    const int n_ch = std::max(1, std::min(16, units));
+    std::vector<std::pair<int, int>> ch;                  // [r0, r1) block rows, last rows first
     for (int k = 0; k < n_ch; ++k) {
-        const int c = fwd ? k : n_ch - 1 - k;
+        const int c = n_ch - 1 - k;
         const int r0 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * c) / n_ch));
         const int r1 = std::min(D.M, align * static_cast<int>((static_cast<long long>(units) * (c + 1)) / n_ch));
         if (r1 > r0) ch.emplace_back(r0, r1);
     }
-    HostStreams hs;
-    if ((rc = host_streams(hs))) return rc;
+    cudaStream_t up = nullptr, down = nullptr;
+    if ((rc = helper_stream(st, 1, &up)) || (rc = helper_stream(st, 2, &down))) return rc;
     const int nc = static_cast<int>(ch.size());
-    std::vector<cudaEvent_t> ev(2 * nc + 3);
+    // Every exit path goes through the guard: on an error it drains the helper streams and the
+    // caller's stream (no async copy into the caller's host buffers is left in flight), and it
+    // always destroys the per-call events.
+    struct Guard {
+        std::vector<cudaEvent_t> ev;
+        cudaStream_t st, up, down;
+        bool ok;
+        ~Guard() {
+            if (!ok) {
+                cudaStreamSynchronize(up);
+                cudaStreamSynchronize(down);
+                cudaStreamSynchronize(st);
+            }
+            for (auto& e : ev)
+                if (e) cudaEventDestroy(e);
+        }
+    } guard{std::vector<cudaEvent_t>(2 * nc + 3, nullptr), st, up, down, false};
+    std::vector<cudaEvent_t>& ev = guard.ev;
     for (auto& e : ev) PA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
-    auto cleanup = [&]() { for (auto& e : ev) cudaEventDestroy(e); };
     cudaEvent_t ev_k = ev[0], ev_v = ev[1], ev_done = ev[2];
     // token range [t0, t1) of Q / O between host and device, in the configured layout
     auto copy_rows = [&](void* dst, const void* src, int r0, int r1, cudaMemcpyKind kind, cudaStream_t s) -> int {
@@ -546,42 +542,17 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
         }
         return PROXYATTN_OK;
     };
-    // value rows [t0, t1) of V (head-major [Hkv_l][N][d] or token-major)
-    auto copy_v = [&](int r0, int r1) -> int {
-        const long long t0 = static_cast<long long>(r0) * D.b, t1 = std::min<long long>(static_cast<long long>(r1) * D.b, D.N);
-        if (t1 <= t0) return PROXYATTN_OK;
-        if (D.tok) {
-            const size_t off = static_cast<size_t>(t0) * D.kv_ts * el, n = static_cast<size_t>(t1 - t0) * D.kv_ts * el;
-            PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v) + off, static_cast<const char*>(Vh) + off, n,
-                                    cudaMemcpyHostToDevice, hs.up), "H2D V rows");
-        } else {
-            const size_t pitch = static_cast<size_t>(D.N) * D.d * el, off = static_cast<size_t>(t0) * D.d * el;
-            PA_CUDA(cudaMemcpy2DAsync(at<char>(dws, H.v) + off, pitch, static_cast<const char*>(Vh) + off, pitch,
-                                      static_cast<size_t>(t1 - t0) * D.d * el, D.Hkvl, cudaMemcpyHostToDevice, hs.up),
-                    "H2D V rows");
-        }
-        return PROXYATTN_OK;
-    };
-    // uploads — reverse: K, Q chunk 0 (the last rows), V, the other Q chunks; forward: K, the
-    // last Q block (Alg. 1), then per chunk its V rows and Q rows
+    // uploads: K, Q chunk 0 (the last rows), V, the other Q chunks
     PA_CUDA(cudaEventRecord(ev[0], st), "record");                 // after the caller's prior work
-    PA_CUDA(cudaStreamWaitEvent(hs.up, ev[0], 0), "wait");
-    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, hs.up), "H2D K");
-    if (fwd && (rc = copy_rows(at<char>(dws, H.q), Qh, D.M - 1, D.M, cudaMemcpyHostToDevice, hs.up))) {
-        cleanup();
-        return rc;
-    }
-    PA_CUDA(cudaEventRecord(ev_k, hs.up), "record");
+    PA_CUDA(cudaStreamWaitEvent(up, ev[0], 0), "wait");
+    PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.k), Kh, kb, cudaMemcpyHostToDevice, up), "H2D K");
+    PA_CUDA(cudaEventRecord(ev_k, up), "record");
     for (int c = 0; c < nc; ++c) {
-        if (fwd && (rc = copy_v(ch[c].first, ch[c].second))) { cleanup(); return rc; }
-        if ((rc = copy_rows(at<char>(dws, H.q), Qh, ch[c].first, ch[c].second, cudaMemcpyHostToDevice, hs.up))) {
-            cleanup();
-            return rc;
-        }
-        PA_CUDA(cudaEventRecord(ev[3 + c], hs.up), "record");
-        if (!fwd && c == 0) {
-            PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, hs.up), "H2D V");
-            PA_CUDA(cudaEventRecord(ev_v, hs.up), "record");
+        if ((rc = copy_rows(at<char>(dws, H.q), Qh, ch[c].first, ch[c].second, cudaMemcpyHostToDevice, up))) return rc;
+        PA_CUDA(cudaEventRecord(ev[3 + c], up), "record");
+        if (c == 0) {
+            PA_CUDA(cudaMemcpyAsync(at<char>(dws, H.v), Vh, kb, cudaMemcpyHostToDevice, up), "H2D V");
+            PA_CUDA(cudaEventRecord(ev_v, up), "record");
         }
     }
     // compute: Alg. 1 once, then per chunk estimate (K* given) + attention; O chunks down
@@ -589,11 +560,10 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     for (int c = 0; c < nc; ++c) {
         PA_CUDA(cudaStreamWaitEvent(st, c == 0 ? ev_k : ev[3 + c], 0), "wait");
         if (c == 0) {
-            if (!fwd) PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");   // the last rows' Q
+            PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");   // the last rows' Q
             rc = proxyattn_budgets(cfg, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws), dws_bytes - H.ws,
                                    at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), stream);
-            if (rc) { cleanup(); return rc; }
-            if (fwd) PA_CUDA(cudaStreamWaitEvent(st, ev[3], 0), "wait");      // the first chunk's V / Q
+            if (rc) return rc;
         }
         cc.row_begin = ch[c].first;
         cc.row_end = ch[c].second;
@@ -601,26 +571,23 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
         rc = proxyattn_estimate(&cc, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.ws), dws_bytes - H.ws,
                                 at<int32_t>(dws, H.kstar), at<float>(dws, H.budget), at<int32_t>(dws, H.cnt),
                                 at<int32_t>(dws, H.idx), stream);
-        if (rc) { cleanup(); return rc; }
-        if (!fwd && c == 0) PA_CUDA(cudaStreamWaitEvent(st, ev_v, 0), "wait");
+        if (rc) return rc;
+        if (c == 0) PA_CUDA(cudaStreamWaitEvent(st, ev_v, 0), "wait");
         cc.flags = cfg->flags;
         rc = proxyattn_prefill(&cc, at<char>(dws, H.q), at<char>(dws, H.k), at<char>(dws, H.v),
                                at<int32_t>(dws, H.cnt), at<int32_t>(dws, H.idx), at<char>(dws, H.o), stream);
-        if (rc) { cleanup(); return rc; }
+        if (rc) return rc;
         PA_CUDA(cudaEventRecord(ev[3 + nc + c], st), "record");
-        PA_CUDA(cudaStreamWaitEvent(hs.down, ev[3 + nc + c], 0), "wait");
-        if ((rc = copy_rows(Oh, at<char>(dws, H.o), ch[c].first, ch[c].second, cudaMemcpyDeviceToHost, hs.down))) {
-            cleanup();
-            return rc;
-        }
+        PA_CUDA(cudaStreamWaitEvent(down, ev[3 + nc + c], 0), "wait");
+        if ((rc = copy_rows(Oh, at<char>(dws, H.o), ch[c].first, ch[c].second, cudaMemcpyDeviceToHost, down))) return rc;
     }
-    PA_CUDA(cudaEventRecord(ev_done, hs.down), "record");
+    PA_CUDA(cudaEventRecord(ev_done, down), "record");
     PA_CUDA(cudaStreamWaitEvent(st, ev_done, 0), "wait");
     if (kstar_h)
         PA_CUDA(cudaMemcpyAsync(kstar_h, at<char>(dws, H.kstar), (size_t)D.Hl * 4, cudaMemcpyDeviceToHost, st),
                 "D2H kstar");
     PA_CUDA(cudaStreamSynchronize(st), "forward_host sync");
-    cleanup();
+    guard.ok = true;
     return PROXYATTN_OK;
 }
 
@@ -636,7 +603,7 @@ struct VarlenLayout {
     bool packed;
 };
 static bool varlen_packed(const pa::Dims& D) {
-    return !D.fp32 && D.b == 128 && pa::attn_variant(false) == 8;
+    return !D.fp32 && D.b == 128;
 }
 static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu, VarlenLayout& L,
                          int64_t& max_len) {
@@ -678,19 +645,6 @@ static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu,
         L.ws2 = off;     off = pa::align256(off + pa::workspace_layout(D).total);
     }
     L.total = off;
-    return PROXYATTN_OK;
-}
-
-// Per-device second stream of the packed varlen path (created once, non-blocking).
-static int varlen_stream(cudaStream_t* out) {
-    static std::mutex mu;
-    static std::map<int, cudaStream_t> per_dev;
-    int dev = 0;
-    PA_CUDA(cudaGetDevice(&dev), "get device");
-    std::lock_guard<std::mutex> lock(mu);
-    cudaStream_t& s = per_dev[dev];
-    if (!s) PA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
-    *out = s;
     return PROXYATTN_OK;
 }
 
@@ -762,7 +716,7 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
     cudaStream_t st2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (L.packed && !descs.empty()) {
-        if ((rc = varlen_stream(&st2))) return rc;
+        if ((rc = helper_stream(st, 3, &st2))) return rc;
         PA_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
         PA_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event create");
         PA_CUDA(cudaEventRecord(ev_fork, st), "record");
@@ -802,14 +756,99 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
     }
     if (L.packed && !descs.empty()) {
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
-        pa::Dims D;
-        if ((rc = derive(&c, D))) return rc;
+        pa::Dims D;               // (each sequence's M was checked by varlen_layout; the packed
+        if ((rc = derive(&c, D, false))) return rc;   // total may exceed one sequence's limit)
         const int n_items = descs.back().item0 + D.Hl * descs.back().M;
         PA_CUDA(pa::launch_attn_tc8_varlen(D, Q, K, V, at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), O,
                                            at<pa::SeqDesc>(ws, L.descs), static_cast<int>(descs.size()),
                                            n_items, st),
                 "attn_tc8 varlen");
     }
+    return PROXYATTN_OK;
+}
+
+// ------------------------------------------------------ seq-avgpool comparator --
+// SPEC S:365-373 (seq_avgpool_scores): the per-head sequence-pooled
+// estimator; the same Alg. 1 budgets and Eq. 3 selection then run on its score maps.
+struct AvgLayout {
+    size_t qb, kb, z, lse, ws, total;
+};
+static AvgLayout avg_layout(const pa::Dims& D) {
+    AvgLayout A{};
+    const size_t el = D.fp32 ? 4 : 2;
+    size_t off = 0;
+    A.qb = off;  off = pa::align256(off + (size_t)D.Hl * D.M * D.d * el);
+    A.kb = off;  off = pa::align256(off + (size_t)D.Hkvl * D.M * D.d * el);
+    A.z = off;   off = pa::align256(off + (size_t)D.Hl * D.M * D.M * 4);
+    A.lse = off; off = pa::align256(off + (size_t)D.Hl * D.M * 4);
+    A.ws = off;  off = pa::align256(off + pa::workspace_layout(D).total);   // Alg. 1 scratch
+    A.total = off;
+    return A;
+}
+
+static int avg_derive(const proxyattn_cfg* cfg, pa::Dims& D) {
+    int rc = derive(cfg, D);
+    if (rc) return rc;
+    if (D.rb != 0 || D.re != D.M) return fail(PROXYATTN_E_CONFIG, "the avgpool comparator takes no row range");
+    if (D.d % 32) return fail(PROXYATTN_E_UNSUPPORTED, "the avgpool comparator needs head_dim %% 32 == 0");
+    return PROXYATTN_OK;
+}
+
+int proxyattn_avgpool_workspace_bytes(const proxyattn_cfg* cfg, size_t* out) {
+    pa::Dims D;
+    int rc = avg_derive(cfg, D);
+    if (rc) return rc;
+    if (!out) return fail(PROXYATTN_E_CONFIG, "out is NULL");
+    *out = avg_layout(D).total;
+    return PROXYATTN_OK;
+}
+
+int proxyattn_avgpool_scores(const proxyattn_cfg* cfg, const void* Q, const void* K, void* ws, size_t ws_bytes,
+                             float* S_out, void* stream) {
+    pa::Dims D;
+    int rc = avg_derive(cfg, D);
+    if (rc) return rc;
+    const AvgLayout A = avg_layout(D);
+    if (!ws || ws_bytes < A.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", A.total);
+    if (!Q || !K || !S_out) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    cudaStream_t st = S(stream);
+    if ((rc = check_finite(D, st, {{Q, true}, {K, false}}))) return rc;
+    PA_CUDA(pa::launch_block_pool(D, Q, K, at<char>(ws, A.qb), at<char>(ws, A.kb), st), "block_pool");
+    PA_CUDA(pa::launch_avgpool_scores(D, at<char>(ws, A.qb), at<char>(ws, A.kb), S_out, at<float>(ws, A.lse), true, st),
+            "avgpool_scores");
+    return PROXYATTN_OK;
+}
+
+int proxyattn_avgpool_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K, void* ws, size_t ws_bytes,
+                               int32_t* kstar, float* budget, int32_t* block_cnt, int32_t* block_idx, void* stream) {
+    pa::Dims D;
+    int rc = avg_derive(cfg, D);
+    if (rc) return rc;
+    const AvgLayout A = avg_layout(D);
+    if (!ws || ws_bytes < A.total) return fail(PROXYATTN_E_WORKSPACE, "workspace needs %zu bytes", A.total);
+    if (!Q || !K || !kstar || !budget || !block_cnt || !block_idx) return fail(PROXYATTN_E_SHAPE, "NULL pointer");
+    cudaStream_t st = S(stream);
+    if ((rc = check_finite(D, st, {{Q, true}, {K, false}}))) return rc;
+    const pa::Workspace W = pa::workspace_layout(D);
+    void* wsb = at<char>(ws, A.ws);
+    Nvtx r("seq-avgpool comparator estimate");
+    const bool alg1 = !(D.flags & PROXYATTN_FLAG_KSTAR_GIVEN);
+    // Alg. 1 forked onto the helper stream, as in proxyattn_estimate (it reads only Q and K)
+    cudaStream_t aux = nullptr;
+    AuxEvents ev{};
+    if (alg1) {
+        if ((rc = helper_stream(st, 0, &aux)) || (rc = estimate_events(&ev))) return rc;
+        PA_CUDA(cudaEventRecord(ev.fork, st), "record");
+        PA_CUDA(cudaStreamWaitEvent(aux, ev.fork, 0), "wait");
+        if ((rc = run_budgets(D, Q, K, wsb, W, kstar, budget, aux))) return rc;
+        PA_CUDA(cudaEventRecord(ev.join, aux), "record");
+    }
+    PA_CUDA(pa::launch_block_pool(D, Q, K, at<char>(ws, A.qb), at<char>(ws, A.kb), st), "block_pool");
+    // raw logits suffice for the selection: z - lse_m has the order of z within a row
+    PA_CUDA(pa::launch_avgpool_scores(D, at<char>(ws, A.qb), at<char>(ws, A.kb), at<float>(ws, A.z), nullptr, false,
+                                      st), "avgpool_scores");
+    if (alg1) PA_CUDA(cudaStreamWaitEvent(st, ev.join, 0), "wait");
+    PA_CUDA(pa::launch_select(D, at<float>(ws, A.z), kstar, block_cnt, block_idx, st, true), "select per head");
     return PROXYATTN_OK;
 }
 
@@ -823,13 +862,6 @@ const char* proxyattn_last_error(void) { return g_err.c_str(); }
 
 const char* proxyattn_build_info(void) {
     return "libproxyattn sm_100a (tcgen05/TMEM/TMA attention and estimation)";
-}
-
-int proxyattn_debug_trace(long long* host_out, size_t n) {
-    long long* d = pa::attn_trace_ptr();
-    if (!d || !host_out) return fail(PROXYATTN_E_CONFIG, "no trace (set PROXYATTN_TRACE=<cta>)");
-    PA_CUDA(cudaMemcpy(host_out, d, n * sizeof(long long), cudaMemcpyDeviceToHost), "trace copy");
-    return PROXYATTN_OK;
 }
 
 int proxyattn_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts, void* stream) {

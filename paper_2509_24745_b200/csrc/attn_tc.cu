@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O,
                const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
-               int r, int Hl, int pair_mode, float scale_log2, long long* trace, int trace_bid,
+               int r, int Hl, int pair_mode, float scale_log2,
                int row_lo, int row_hi) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -242,13 +242,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     if (!(f_cur & (1 << slot))) continue;
                     const uint32_t tP = tbase + slot * 128;
                     const uint32_t tO = tbase + 256 + slot * 128;
-                    long long* tr = (trace && blockIdx.x == trace_bid && u < 256 && leader)
-                                        ? trace + (u * 2 + slot) * 8 : nullptr;
-                    if (tr) tr[0] = clock64();                 // MMA: start waiting for P
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {   // PV over keys [64 half, 64 half + 64)
                         mbar_wait(&bars->p_half[slot][half], jn[slot] & 1);
-                        if (tr) tr[1 + half] = clock64();      // MMA: P half ready
                         tc_fence_after();
                         if (leader) {
                             const uint64_t b0 = dv + (st * kTile >> 4);
@@ -265,7 +261,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     __syncwarp();
                     ++jn[slot];
                     if (has_nxt && (f_nxt & (1 << slot))) issue_s(slot, u + 1);
-                    if (tr) tr[3] = clock64();                 // MMA: PV + next S issued
                 }
                 if (leader) tc_commit(&bars->v_empty[st]);
                 __syncwarp();
@@ -300,12 +295,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         for (int j = 0; j < my_cnt; ++j) {
             const int n = n_next;
             if (j + 1 < my_cnt) n_next = my_list ? __ldg(my_list + j + 1) : j + 1;  // prefetch
-            long long* tr = (trace && blockIdx.x == trace_bid && lane == 0 && quarter == 2 && j < 256)
-                                ? trace + 256 * 16 + (j * 2 + slot) * 8 : nullptr;
-            if (tr) tr[0] = clock64();                         // SM: start waiting for S
             mbar_wait(&bars->s_full[slot], j & 1);
             tc_fence_after();
-            if (tr) tr[1] = clock64();                         // SM: S ready
             uint32_t raw[4][32];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, raw[c]);
@@ -331,7 +322,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 }
             const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-            if (tr) tr[2] = clock64();                         // SM: S loaded + row max
             const float m_new = fmaxf(m_used, rmax * scale_log2);
             const bool need = (m_new > m_used + kRescaleThreshold);
             const bool any = __any_sync(0xffffffffu, need);
@@ -365,11 +355,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     ls[c & 3] = f2_add(ls[c & 3], f2_pack(p0, p1));
                     pk[c] = pack_bf16(p0, p1);
                 }
-                if (tr) tr[5 + half] = clock64();              // SM: exps of this half done
                 tmem_st32(tS + half * 32, pk);
                 if (half == 0 && j > 0) {
                     mbar_wait(&bars->o_done[slot], (j - 1) & 1);  // PV_{j-1} finished writing O
-                    if (tr) tr[7] = clock64();                 // SM: O ready for correction
                     tc_fence_after();
                     if (any) {
 #pragma unroll
@@ -387,7 +375,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&bars->p_half[slot][half]);
-                if (tr) tr[3 + half] = clock64();              // SM: P half released
             }
             {
                 const uint64_t t = f2_add(f2_add(ls[0], ls[1]), f2_add(ls[2], ls[3]));
@@ -431,37 +418,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
 }
 
-// Slot pairing: 0 = two heads of one kv head at the same row, 1 = one head at two adjacent
-// rows (default; adjacent rows' lists overlap strongly, independent of per-head budgets).
-// PROXYATTN_PAIR_MODE overrides it (for measurements).
-constexpr size_t kTraceBytes = 2 * 256 * 2 * 8 * sizeof(long long);
-
-int attn_pair_mode() {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("PROXYATTN_PAIR_MODE");
-        mode = (e && e[0] == '0') ? 0 : 1;
-    }
-    return mode;
-}
-
-// Fraction (x/4) of the softmax exponentials computed on the FMA pipe instead of MUFU
-// (FA4-style balance of the two pipes).  PROXYATTN_EXP_EMU=0..3 overrides the default.
-int attn_exp_emu() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PROXYATTN_EXP_EMU");
-        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
-    }
-    return v;
-}
-
 }  // namespace
-
-long long*& attn_trace_ptr() {
-    static long long* p = nullptr;
-    return p;
-}
 
 cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {
@@ -470,36 +427,16 @@ cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const vo
         !make_map_bf16_sw128(&mk, K, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128) ||
         !make_map_bf16_sw128(&mv, V, static_cast<uint64_t>(D.Hkvl) * D.N, 128, 128))
         return cudaErrorInvalidValue;
-    const int emu = attn_exp_emu();
-    auto kern = emu == 0 ? attn_tc_kernel<0> : emu == 1 ? attn_tc_kernel<1> : emu == 2 ? attn_tc_kernel<2>
-              : attn_tc_kernel<3>;
-    static bool attr_set[4] = {false, false, false, false};
-    if (!attr_set[emu]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBytes));
-        if (e != cudaSuccess) return e;
-        attr_set[emu] = true;
-    }
+    auto kern = attn_tc_kernel<0>;   // all exponentials on MUFU
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
-    const int mode = attn_pair_mode();
+    const int mode = 1;   // slot pairing: one head at two adjacent rows (dense lists nest exactly)
     const int nrows = D.re - D.rb;
-    const unsigned grid = mode == 0
-        ? static_cast<unsigned>(D.Hkvl * ((D.r + 1) / 2)) * static_cast<unsigned>(nrows)
-        : static_cast<unsigned>(D.Hl) * static_cast<unsigned>((nrows + 1) / 2);
-    // PROXYATTN_TRACE=<cta>: per-event clock64 timeline of one CTA (diagnostics only), read
-    // back with proxyattn_debug_trace().
-    static long long* trace = nullptr;
-    static int trace_bid = -1;
-    if (trace_bid < 0) {
-        const char* e = getenv("PROXYATTN_TRACE");
-        trace_bid = e ? atoi(e) : 1 << 30;
-        if (e && cudaMalloc(&trace, kTraceBytes) != cudaSuccess) trace = nullptr;
-    }
-    if (trace) cudaMemsetAsync(trace, 0, kTraceBytes, st);
-    attn_trace_ptr() = trace;
+    const unsigned grid = static_cast<unsigned>(D.Hl) * static_cast<unsigned>((nrows + 1) / 2);
     kern<<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
-        D.M, D.r, D.Hl, mode, scale_log2, trace, trace_bid, D.rb, D.re);
+        D.M, D.r, D.Hl, mode, scale_log2, D.rb, D.re);
     return cudaGetLastError();
 }
 

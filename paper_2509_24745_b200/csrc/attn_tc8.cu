@@ -42,6 +42,8 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -143,7 +145,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int* __restrict__ block_cnt, const int* __restrict__ block_idx, int N, int M,
                 int r, float scale_log2, int row_lo, int row_hi, int n_total, Sched* sched,
                 int* flagged, int exact, long long o_hs, long long o_ts, const int* __restrict__ ucnt,
-                int diag_noload, const int* __restrict__ kvperm, const SeqDesc* __restrict__ seqs,
+                const int* __restrict__ kvperm, const SeqDesc* __restrict__ seqs,
                 int n_seqs) {
     using Sh = Shape<kD, kB>;
     constexpr bool kPair = (kB == 64);
@@ -309,10 +311,6 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             int mem;
                             const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
-                            if (diag_noload && gk >= kKStages) {   // diagnostics: stale tile, no L2 traffic
-                                mbar_arrive(&bars->k_full[st]);
-                                continue;
-                            }
                             mbar_expect_tx(&bars->k_full[st], Sh::kKTile);
 #pragma unroll
                             for (int ch = 0; ch < kD / 64; ++ch)
@@ -339,10 +337,6 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         int mem;
                         const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
-                        if (diag_noload && gv >= kVStages) {
-                            mbar_arrive(&bars->v_full[st]);
-                            continue;
-                        }
                         mbar_expect_tx(&bars->v_full[st], Sh::kKTile);
 #pragma unroll
                         for (int ch = 0; ch < kD / 64; ++ch)
@@ -816,8 +810,11 @@ __global__ void __launch_bounds__(1024) kv_order_kernel(const int* __restrict__ 
     if (threadIdx.x == 0) *done = 0;
 }
 
-// Per-stream scheduler state + flagged-row list + kB = 64 union counts (grown on demand,
-// never freed).
+// Per-(device, stream) scheduler state + flagged-row list + kB = 64 union counts.  A launch
+// captured into a CUDA graph keeps these pointers in its kernel parameters, so a buffer is
+// NEVER freed: when a larger launch needs more room, the old arrays are retired (kept
+// allocated until exit) and new ones are made.  Graphs captured on one stream share the
+// `sched` counters: replay them one at a time on that stream (stream order serialises them).
 struct SchedBuf {
     Sched* sched = nullptr;
     int* flagged = nullptr;
@@ -831,8 +828,9 @@ struct SchedBuf {
 SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
     static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, SchedBuf> bufs;
+    static std::vector<void*> retired;   // superseded arrays a captured graph may still use
     int dev = 0;
-    cudaGetDevice(&dev);
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
     SchedBuf& b = bufs[{dev, st}];
     if (!b.sched && cudaMalloc(&b.sched, sizeof(Sched)) != cudaSuccess) return nullptr;
@@ -843,30 +841,32 @@ SchedBuf* sched_for(cudaStream_t st, size_t n_items) {
         if (cudaMemset(b.kvdone, 0, sizeof(int)) != cudaSuccess) return nullptr;
     }
     if (b.cap < n_items) {   // each row can be appended by up to 4 epilogue warps
-        if (b.flagged) cudaFree(b.flagged);
-        if (b.ucnt) cudaFree(b.ucnt);
-        b.flagged = b.ucnt = nullptr;
-        b.cap = 0;
-        if (cudaMalloc(&b.flagged, 4 * n_items * sizeof(int)) != cudaSuccess) return nullptr;
-        if (cudaMalloc(&b.ucnt, n_items * sizeof(int)) != cudaSuccess) return nullptr;
-        b.cap = n_items;
+        int* fl = nullptr;
+        int* uc = nullptr;
+        const size_t cap = std::max(n_items, 2 * b.cap);
+        if (cudaMalloc(&fl, 4 * cap * sizeof(int)) != cudaSuccess) return nullptr;
+        if (cudaMalloc(&uc, cap * sizeof(int)) != cudaSuccess) {
+            cudaFree(fl);
+            return nullptr;
+        }
+        if (b.flagged) retired.push_back(b.flagged);
+        if (b.ucnt) retired.push_back(b.ucnt);
+        b.flagged = fl;
+        b.ucnt = uc;
+        b.cap = cap;
     }
     return &b;
 }
 
 using AttnKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, __nv_bfloat16*,
                             const int*, const int*, int, int, int, float, int, int, int, Sched*, int*,
-                            int, long long, long long, const int*, int, const int*, const SeqDesc*, int);
+                            int, long long, long long, const int*, const int*, const SeqDesc*, int);
 
 template <int kD, int kB, int kEmu, bool kVar = false>
 AttnKernel kernel_with_attr() {
-    static bool set = false;
-    if (!set) {
-        if (cudaFuncSetAttribute(attn_tc8_kernel<kEmu, kD, kB, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Shape<kD, kB>::kSmem)) != cudaSuccess)
-            return nullptr;
-        set = true;
-    }
+    if (ensure_smem_attr(reinterpret_cast<const void*>(attn_tc8_kernel<kEmu, kD, kB, kVar>),
+                         static_cast<int>(Shape<kD, kB>::kSmem)) != cudaSuccess)
+        return nullptr;
     return attn_tc8_kernel<kEmu, kD, kB, kVar>;
 }
 
@@ -883,35 +883,17 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
         !make_map_bf16_sw128_3d(&mk, K, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d) ||
         !make_map_bf16_sw128_3d(&mv, V, D.Hkvl, D.N, D.kv_ts, D.kv_hs, D.b, D.d))
         return cudaErrorInvalidValue;
-    static int emu = -1;
-    // PROXYATTN_EXP_EMU=0..4: x/8 of the exponentials on the FMA pipe (d = b = 128).  Default 0:
-    // under the power cap all-MUFU measured best (128K prefill 18.84-18.94 ms vs 18.85-19.06 at
-    // 1/8 and 19.18-19.28 at 2/8, three alternating runs; 2/8 was best before the barrier fix)
-    if (emu < 0) {
-        const char* e = getenv("PROXYATTN_EXP_EMU");
-        emu = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 0;
-    }
+    // Exp2 split (of every 8 key-column pairs, kEmu on the FMA-pipe polynomial), measured at
+    // 128K: d = 128 all-MUFU (under the power cap 18.84-18.94 ms vs 18.85-19.06 at 1/8 and
+    // 19.18-19.28 at 2/8); d = 64 (exp-bound: half the tensor work per exp2) 2/8 (13.2-13.3 ms
+    // vs 13.4-13.6 at 3/8 and 13.8 at 4/8); b = 64 all-MUFU.
     AttnKernel kern = nullptr;
-    if (n_seqs > 0) {          // varlen instantiations (b = 128; the default exp2 split per d)
+    if (n_seqs > 0)            // varlen instantiations (b = 128)
         kern = D.d == 128 ? kernel_with_attr<128, 128, 0, true>() : kernel_with_attr<64, 128, 2, true>();
-    } else if (D.d == 128 && D.b == 128) {
-        kern = emu == 0 ? kernel_with_attr<128, 128, 0>() : emu == 1 ? kernel_with_attr<128, 128, 1>()
-             : emu == 2 ? kernel_with_attr<128, 128, 2>() : emu == 3 ? kernel_with_attr<128, 128, 3>()
-                                                          : kernel_with_attr<128, 128, 4>();
-    } else if (D.d == 128) {   // b = 64: 0 or 2 (PROXYATTN_EXP_EMU)
-        kern = emu == 2 ? kernel_with_attr<128, 64, 2>() : kernel_with_attr<128, 64, 0>();
-    } else if (D.b == 128) {   // d = 64 (exp-bound: half the tensor work per exp2)
-        static int emu64 = -1;   // PROXYATTN_EXP_EMU64=2..4; 2/8 measured best at 128K
-        if (emu64 < 0) {         // (13.2-13.3 ms vs 13.4-13.6 at 3/8 and 13.8 at 4/8)
-            const char* e = getenv("PROXYATTN_EXP_EMU64");
-            emu64 = (e && e[0] >= '0' && e[0] <= '4') ? e[0] - '0' : 2;
-        }
-        kern = emu64 == 0 ? kernel_with_attr<64, 128, 0>() : emu64 == 1 ? kernel_with_attr<64, 128, 1>()
-             : emu64 == 2 ? kernel_with_attr<64, 128, 2>() : emu64 == 3 ? kernel_with_attr<64, 128, 3>()
-                                                                         : kernel_with_attr<64, 128, 4>();
-    } else {
-        kern = kernel_with_attr<64, 64, 2>();
-    }
+    else if (D.d == 128)
+        kern = D.b == 128 ? kernel_with_attr<128, 128, 0>() : kernel_with_attr<128, 64, 0>();
+    else
+        kern = D.b == 128 ? kernel_with_attr<64, 128, 2>() : kernel_with_attr<64, 64, 2>();
     if (!kern) return cudaErrorInvalidValue;
     int dev = 0, n_sm = 0;
     cudaGetDevice(&dev);
@@ -943,13 +925,6 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
         kvperm = sb->kvperm;
     }
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D.d));
-    // PROXYATTN_DIAG_NOLOAD=1 (diagnostics only, WRONG results): K/V TMA loads after the
-    // first ring fill are skipped, so the launch time excludes the L2 -> SMEM traffic
-    static int noload = -1;
-    if (noload < 0) {
-        const char* e = getenv("PROXYATTN_DIAG_NOLOAD");
-        noload = (e && e[0] == '1') ? 1 : 0;
-    }
     const size_t smem = D.d == 128 ? (D.b == 128 ? Shape<128, 128>::kSmem : Shape<128, 64>::kSmem)
                                    : (D.b == 128 ? Shape<64, 128>::kSmem : Shape<64, 64>::kSmem);
     // fast launch over every row, then the exact launch over the rows it flagged (usually
@@ -959,7 +934,7 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
         kern<<<grid, kThreads, smem, st>>>(
             mq, mk, mv, static_cast<__nv_bfloat16*>(O), block_cnt, block_idx, static_cast<int>(D.N),
             D.M, D.r, scale_log2, D.rb, D.re, static_cast<int>(n_items), sb->sched, sb->flagged, exact,
-            D.q_hs, D.q_ts, sb->ucnt, noload, kvperm, seqs, n_seqs);
+            D.q_hs, D.q_ts, sb->ucnt, kvperm, seqs, n_seqs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -12,6 +12,7 @@
 // estimate_tc.cu for A2-A4 when the shapes allow.
 #include <cfloat>
 #include <climits>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -396,8 +397,9 @@ __global__ void budget_finalize_kernel(Dims D, const float* __restrict__ bmass,
 // One CTA per (local group c, block row m).  Sorts columns 0..m-1 of the shared score row
 // by (L desc, index asc) once, then each head of the group keeps the first K_{h,m}-1 of
 // that order plus the diagonal, emitted ascending (nested prefixes).
+// per_head (the seq-avgpool comparator): L holds one score map per LOCAL head, c = local head.
 __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __restrict__ kstar,
-                              int* __restrict__ block_cnt, int* __restrict__ block_idx) {
+                              int* __restrict__ block_cnt, int* __restrict__ block_idx, int per_head) {
     extern __shared__ unsigned char sm[];
     const int nr = D.re - D.rb;                  // block rows [rb, re) (all by default)
     const int c = blockIdx.x / nr;
@@ -418,7 +420,8 @@ __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __
     __syncthreads();
 
     const int grp = D.gb + c;
-    const int h0 = max(grp * D.gq, D.qb), h1 = min((grp + 1) * D.gq, D.qe);
+    const int h0 = per_head ? D.qb + c : max(grp * D.gq, D.qb);
+    const int h1 = per_head ? h0 + 1 : min((grp + 1) * D.gq, D.qe);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // One warp per head: ballot compaction of {n <= m : n == m or rank[n] < K - 1}.
     for (int h = h0 + wid; h < h1; h += nw) {
@@ -583,7 +586,7 @@ cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar
 }
 
 cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* block_cnt,
-                          int* block_idx, cudaStream_t st) {
+                          int* block_idx, cudaStream_t st, bool per_head) {
     const int P = next_pow2(D.M);
     const size_t sm = static_cast<size_t>(P) * 4 * 3;
     if (sm > 48 * 1024) {
@@ -591,14 +594,61 @@ cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* 
                                              static_cast<int>(sm));
         if (e != cudaSuccess) return e;
     }
-    select_kernel<<<D.gl * (D.re - D.rb), 512, sm, st>>>(D, L, kstar, block_cnt, block_idx);
+    select_kernel<<<(per_head ? D.Hl : D.gl) * (D.re - D.rb), 512, sm, st>>>(D, L, kstar, block_cnt, block_idx,
+                                                                           per_head ? 1 : 0);
     return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ CHECK_FINITE --
+// S:37 ("all values finite"), S:49 / S:319 ("non-finite input -> validation error"): counts
+// the elements whose exponent field is all ones (NaN or +-Inf).  Element e of run r lives at
+// p[r * row_stride + e].  Grid-stride, 8 bf16 / 4 fp32 per 16-byte load when aligned.
+template <bool kF32>
+__global__ void count_nonfinite_kernel(const void* __restrict__ p, long long rows, long long row_elems,
+                                       long long row_stride, int* __restrict__ bad) {
+    constexpr int kVec = kF32 ? 4 : 8;
+    const bool vec = (row_elems % kVec == 0) && (row_stride % kVec == 0) &&
+                     (reinterpret_cast<uintptr_t>(p) % 16 == 0);
+    const long long per_row = vec ? row_elems / kVec : row_elems;
+    const long long total = rows * per_row;
+    int n = 0;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = i / per_row, c = i % per_row;
+        if (vec) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + (r * row_stride) / kVec + c);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (kF32) n += (w[k] & 0x7f800000u) == 0x7f800000u;
+                else n += ((w[k] & 0x7f80u) == 0x7f80u) + ((w[k] & 0x7f800000u) == 0x7f800000u);
+            }
+        } else if (kF32) {
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(p) + r * row_stride + c);
+            n += (w & 0x7f800000u) == 0x7f800000u;
+        } else {
+            const unsigned short w = __ldg(reinterpret_cast<const unsigned short*>(p) + r * row_stride + c);
+            n += (w & 0x7f80u) == 0x7f80u;
+        }
+    }
+    n = __reduce_add_sync(0xffffffffu, n);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(bad, n);
 }
 
 cudaError_t launch_check_lists(const Dims& D, const int* block_cnt, const int* block_idx,
                                int* bad_out, cudaStream_t st) {
     const long long n = static_cast<long long>(D.Hl) * D.M;
     check_lists_kernel<<<blocks_for(n, 256), 256, 0, st>>>(D, block_cnt, block_idx, bad_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonfinite(const void* p, bool fp32, long long rows, long long row_elems,
+                                   long long row_stride, int* bad, cudaStream_t st) {
+    if (rows <= 0 || row_elems <= 0) return cudaSuccess;
+    const long long n = rows * row_elems;
+    const unsigned grid = static_cast<unsigned>(std::min<long long>((n + 2047) / 2048, 148 * 16));
+    if (fp32) count_nonfinite_kernel<true><<<grid, 256, 0, st>>>(p, rows, row_elems, row_stride, bad);
+    else count_nonfinite_kernel<false><<<grid, 256, 0, st>>>(p, rows, row_elems, row_stride, bad);
     return cudaGetLastError();
 }
 

@@ -30,8 +30,9 @@ cudaError_t launch_static_budget(const Dims& D, int* kstar, float* budget, cudaS
 cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar, float* budget,
                                    cudaStream_t st);
 // A5-A6: per (group, row) ordering, per head compaction.
+// per_head: L is [Hl][M][M] (one score map per local head, the seq-avgpool comparator).
 cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* block_cnt,
-                          int* block_idx, cudaStream_t st);
+                          int* block_idx, cudaStream_t st, bool per_head = false);
 // A7/A8 fp32 debug (SIMT) attention; block lists null => dense.
 cudaError_t launch_attn_simt(const Dims& D, const void* Q, const void* K, const void* V,
                              const int* block_cnt, const int* block_idx, void* O,
@@ -39,14 +40,6 @@ cudaError_t launch_attn_simt(const Dims& D, const void* Q, const void* K, const 
 // A7/A8 bf16 tcgen05 attention; block lists null => dense.
 cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
-cudaError_t launch_attn_tc4(const Dims& D, const void* Q, const void* K, const void* V,
-                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
-cudaError_t launch_attn_tc5(const Dims& D, const void* Q, const void* K, const void* V,
-                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
-cudaError_t launch_attn_tc6(const Dims& D, const void* Q, const void* K, const void* V,
-                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
-cudaError_t launch_attn_tc7(const Dims& D, const void* Q, const void* K, const void* V,
-                            const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 // Varlen (one packed launch over several sequences, token-major, b = 128): sequence s owns the
 // tokens [tok0, tok0 + N) of the packed tensors, its block lists start at cnt_off / idx_off
 // ([Hl][M] / [Hl][M][M] of its own M), and its work items are [item0, item0 + Hl * M).
@@ -63,7 +56,6 @@ cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, 
                                    const SeqDesc* seqs, int n_seqs, int n_items, cudaStream_t st);
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
-long long*& attn_trace_ptr();
 // tcgen05 estimation (bf16, d = b = 128, s = 4): A2+A3 and A4 (see score_tc.cu).
 bool score_tc_supported(const Dims& D);
 size_t score_tc_scratch_bytes(const Dims& D);
@@ -75,6 +67,19 @@ cudaError_t launch_budget_tc(const Dims& D, const void* Q, const void* K, float*
 // Device-side validation of block lists; *bad_out (device int) receives the violation count.
 cudaError_t launch_check_lists(const Dims& D, const int* block_cnt, const int* block_idx,
                                int* bad_out, cudaStream_t st);
+// Number of non-finite elements (NaN / Inf) of a tensor laid out as `rows` runs of
+// `row_elems` contiguous elements, `row_stride` elements apart, added to *bad (device int).
+cudaError_t launch_count_nonfinite(const void* p, bool fp32, long long rows, long long row_elems,
+                                   long long row_stride, int* bad, cudaStream_t st);
+// Seq-avgpool comparator: per-block means of Q (per local head) and of K (per
+// local kv head), bf16 RNE of the exact sums (fp32 in FP32_DEBUG) into Qb [Hl][M][d], Kb
+// [Hkvl][M][d] and the real row count of each block into cnt [M].
+cudaError_t launch_block_pool(const Dims& D, const void* Q, const void* K, void* Qb, void* Kb,
+                              cudaStream_t st);
+// z[hl][m][n] = Qb_m . Kb_n / (c_m c_n sqrt(d)) for n <= m (-inf above), lse[hl][m] over n <= m
+// (natural log); with normalize, z -= lse (log-domain scores, the comparator's map).
+cudaError_t launch_avgpool_scores(const Dims& D, const void* Qb, const void* Kb, float* z, float* lse,
+                                  bool normalize, cudaStream_t st);
 // Diagnostic GEMM tile (see proxyattn_debug_umma).
 cudaError_t launch_debug_umma(const void* A, const void* B, float* C_ss, float* C_ts,
                               cudaStream_t st);

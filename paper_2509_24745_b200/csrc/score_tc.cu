@@ -488,16 +488,9 @@ __global__ void __launch_bounds__(256) budget_mass_kernel(int M, int n_chunks, c
     }
 }
 
-// Exp2 split between MUFU and the FMA pipe in the score epilogues (x/4 of the column
-// pairs on the FMA pipe); PROXYATTN_SCORE_EMU=0..3 overrides the default.
-int score_emu() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PROXYATTN_SCORE_EMU");
-        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;   // 1/4 on the FMA pipe: A2 pass 213 -> 198 us
-    }
-    return v;
-}
+// Exp2 split between MUFU and the FMA pipe in the score epilogues: 1/4 of the column pairs
+// on the FMA-pipe polynomial (A2 pass 213 -> 198 us, Alg. 1 pass 178 -> 166 us at 128K).
+constexpr int kScoreEmu = 1;
 
 // Key tiles per CTA of the score passes; PROXYATTN_SCORE_CHUNK=16/32/64 overrides.
 // Key tiles per CTA of the proxy (A2) pass: the default unless the causal grid of this
@@ -517,48 +510,25 @@ int proxy_chunk(const Dims& D, int base) {
     return c;
 }
 
-int score_chunk() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PROXYATTN_SCORE_CHUNK");
-        const int x = e ? atoi(e) : 0;
-        v = (x == 16 || x == 32 || x == 64) ? x : kChunk;
-    }
-    return v;
-}
+constexpr int score_chunk() { return kChunk; }
 
 
 using ScoreKernel = void (*)(const CUtensorMap, const CUtensorMap, ScoreParams);
 
 // mode: kLse (the A2 pass) or kBudget (Alg. 1; b64 = block size 64)
 ScoreKernel score_kernel(int d, int mode, bool b64 = false) {
-    if (mode == kLse) {
-        if (d == 64) return score_tc_kernel<0, false, 64, kLse>;
-        const int e = score_emu();
-        return e == 0 ? score_tc_kernel<0, false, 128, kLse> : e == 1 ? score_tc_kernel<1, false, 128, kLse>
-             : e == 2 ? score_tc_kernel<2, false, 128, kLse> : score_tc_kernel<3, false, 128, kLse>;
-    }
+    if (mode == kLse) return d == 64 ? score_tc_kernel<0, false, 64, kLse> : score_tc_kernel<kScoreEmu, false, 128, kLse>;
     if (d == 64) return b64 ? score_tc_kernel<0, true, 64, kBudget> : score_tc_kernel<0, false, 64, kBudget>;
-    if (b64) return score_tc_kernel<0, true, 128, kBudget>;
-    static int eb = -1;   // PROXYATTN_BUDGET_EMU=0/1: the same split for the Alg. 1 pass (1: 178 -> 166 us)
-    if (eb < 0) {
-        const char* e = getenv("PROXYATTN_BUDGET_EMU");
-        eb = (e && e[0] == '0') ? 0 : 1;
-    }
-    return eb ? score_tc_kernel<1, false, 128, kBudget> : score_tc_kernel<0, false, 128, kBudget>;
+    return b64 ? score_tc_kernel<0, true, 128, kBudget> : score_tc_kernel<kScoreEmu, false, 128, kBudget>;
 }
 
 bool set_smem_attr() {
-    static bool done = false;
-    if (!done) {
-        for (int d : {64, 128})
-            for (int mode : {static_cast<int>(kLse), static_cast<int>(kBudget)})
-                for (bool b64 : {false, true})
-                    if (cudaFuncSetAttribute(score_kernel(d, mode, b64), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmem)) != cudaSuccess)
-                        return false;
-        done = true;
-    }
+    for (int d : {64, 128})
+        for (int mode : {static_cast<int>(kLse), static_cast<int>(kBudget)})
+            for (bool b64 : {false, true})
+                if (ensure_smem_attr(reinterpret_cast<const void*>(score_kernel(d, mode, b64)),
+                                     static_cast<int>(kSmem)) != cudaSuccess)
+                    return false;
     return true;
 }
 
@@ -571,7 +541,7 @@ bool score_tc_supported(const Dims& D) {
 
 size_t score_tc_scratch_bytes(const Dims& D) {
     const int n_tr = static_cast<int>((D.Ns + 127) / 128);
-    const int chunk = proxy_chunk(D, score_chunk() < kChunk ? score_chunk() : kChunk);
+    const int chunk = proxy_chunk(D, kChunk);
     const int n_chunks = (n_tr + chunk - 1) / chunk;
     // A2/A3: lse partials, lse2, window maxima W [gl][Ns][M]
     const size_t nwin = 128 / (D.bs > 0 ? D.bs : 1);

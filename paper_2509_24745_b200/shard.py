@@ -235,11 +235,11 @@ def budgets_sharded(cfg, Q, K, world: int, rank: int, workspace=None, budgets=No
     b, e = head_shard(Hq, Hkv, world, rank)
     r = Hq // Hkv
     loc = cfg.replace(q_head_begin=b, q_head_end=e, row_begin=0, row_end=0)
-    ks_loc, _ = budgets(loc, Q[b:e], K[b // r:e // r], workspace)
+    ks_loc, bu_loc = budgets(loc, Q[b:e], K[b // r:e // r], workspace)
     kstar = out[0] if out is not None else torch.empty(Hq, dtype=torch.int32, device=ks_loc.device)
-    all_gather(kstar, ks_loc.contiguous())
     budget = out[1] if out is not None else torch.empty(Hq, dtype=torch.float32, device=ks_loc.device)
-    torch.div(kstar.float(), float(cfg.M), out=budget)       # b_h = K*_h / M (Alg. 1 line 4)
+    all_gather(kstar, ks_loc.contiguous())                 # K*_h and b_h = K*_h / M, both as
+    all_gather(budget, bu_loc.contiguous())                # the library computed them
     return kstar, budget
 
 
@@ -261,3 +261,39 @@ def row_work_share(block_cnt_full: torch.Tensor, world: int, align: int = 1) -> 
     M = per_row.numel()
     return [sum(float(per_row[b:e].sum()) for b, e in zigzag_rows(M, world, r, align)) / tot
             for r in range(world)]
+
+
+def estimate_rows_overlapped(cfg, Q, K, ranges, world: int, rank: int, workspaces, out, alg1_workspace=None,
+                             aux_stream=None, streams=None, estimate=None, select_ws=None, budgets=None,
+                             all_gather=None, run_scores=None, run_select=None):
+    """The row-sharded estimate with its one collective overlapped (bench.py's step at N > 1):
+    the score passes (A1-A3, SCORES_ONLY, K* not needed yet) of the rank's row ranges run on
+    `aux_stream` while the current stream runs the head-sharded Alg. 1 and the K* / budget
+    all-gather (budgets_sharded); the selection (A5-A6, select_rows) follows both.  `out` =
+    (kstar, budget, block_cnt, block_idx) for all heads; only the ranges' rows are written.
+    run_scores / run_select replace the two phases (bench.py passes CUDA-graph replays).
+    Without a CUDA stream (aux_stream None: CPU tests with injected ops) the phases run in
+    program order."""
+    kstar, budget, cnt, idx = out
+    if run_scores is None:
+        def run_scores():
+            estimate_rows(cfg, Q, K, ranges, out=out, estimate=estimate, kstar_given=True, streams=streams,
+                          workspaces=workspaces, scores_only=True)
+    if run_select is None:
+        def run_select():
+            select_rows(cfg, ranges, workspaces, kstar, (cnt, idx), select_ws=select_ws)
+    if aux_stream is None:
+        run_scores()
+        budgets_sharded(cfg, Q, K, world, rank, alg1_workspace, budgets=budgets, all_gather=all_gather,
+                        out=(kstar, budget))
+        run_select()
+        return out
+    cur = torch.cuda.current_stream()
+    aux_stream.wait_stream(cur)
+    with torch.cuda.stream(aux_stream):
+        run_scores()
+    budgets_sharded(cfg, Q, K, world, rank, alg1_workspace, budgets=budgets, all_gather=all_gather,
+                    out=(kstar, budget))
+    cur.wait_stream(aux_stream)
+    run_select()
+    return out

@@ -286,3 +286,84 @@ def test_head_sharded_alg1_gathers_the_replicated_kstar():
     ref, _, _, _ = oracle.budgets(oc, Q.float().numpy(), K.float().numpy())
     assert np.array_equal(ks, ref)                           # every head, bit for bit
     assert np.allclose(bu, ref / oc.M)
+
+
+# ---------------------- bench.py's N > 1 estimate: scores | Alg. 1 + all-gather | select --
+def _overlap_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oc = oracle.Cfg(8, 4, 16, 2048, 64, 4, 1, 0.9, round_bf16=True)
+        Q, K, V, _ = workloads.structured(8, 4, 2048, 16, seed=19, dtype=torch.bfloat16)
+        Qf, Kf = Q.float().numpy(), K.float().numpy()
+        M = oc.M
+        phases = []
+
+        def estimate(cfg, Q_, K_, ws, out):                # SCORES_ONLY: L of the rows -> ws
+            assert cfg.scores_only and cfg.kstar_given
+            phases.append(("scores", cfg.row_begin, cfg.row_end))
+            rows = list(range(cfg.row_begin, cfg.row_end))
+            Pq, Pk, sc = oracle.pool(oc, Qf, Kf)
+            _, L = oracle.proxy_scores(oc, Pq, Pk, sc, rows=rows)
+            ws["L"] = L
+            return out
+
+        def select_ws(cfg, ws, kstar, out):
+            phases.append(("select", cfg.row_begin, cfg.row_end))
+            rows = list(range(cfg.row_begin, cfg.row_end))
+            cnt, idx, _ = oracle.select(oc, np.nan_to_num(ws["L"], nan=-np.inf), kstar.numpy(), rows=rows)
+            out[0][:, rows] = torch.from_numpy(cnt[:, rows])
+            out[1][:, rows] = torch.from_numpy(idx[:, rows])
+            return out
+
+        def budgets(cfg, Q_, K_, workspace=None):
+            phases.append(("alg1", cfg.q_head_begin, cfg.q_head_end))
+            b, e = cfg.q_head_begin, cfg.q_head_end
+            ks, bu, _, _ = oracle.budgets(oc, Qf, Kf, heads=list(range(b, e)))
+            return torch.tensor(ks[b:e], dtype=torch.int32), torch.tensor(bu[b:e], dtype=torch.float32)
+
+        def all_gather(dst, src):
+            phases.append(("all_gather",))
+            parts = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(parts, src)
+            dst.copy_(torch.cat(parts))
+
+        cfg = Config(8, 4, 16, 2048, 64, 4, 1, 0.9)
+        ranges = shard.zigzag_rows(M, world, rank, shard.row_align(cfg))
+        out = (torch.zeros(8, dtype=torch.int32), torch.zeros(8), torch.zeros(8, M, dtype=torch.int32),
+               torch.full((8, M, M), -1, dtype=torch.int32))
+        wss = [dict() for _ in ranges]
+        shard.estimate_rows_overlapped(cfg, Q, K, ranges, world, rank, wss, out, estimate=estimate,
+                                       select_ws=select_ws, budgets=budgets, all_gather=all_gather)
+        kinds = [p[0] for p in phases]
+        # scores of every range precede the selection, which follows the K* exchange
+        assert kinds.index("all_gather") < kinds.index("select")
+        assert max(i for i, k in enumerate(kinds) if k == "scores") < kinds.index("select")
+        q.put((rank, ranges, out[0].numpy(), out[1].numpy(), out[2].numpy(), out[3].numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_row_sharded_estimate_equals_unsharded_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    oc = oracle.Cfg(8, 4, 16, 2048, 64, 4, 1, 0.9, round_bf16=True)
+    Q, K, _, _ = workloads.structured(8, 4, 2048, 16, seed=19, dtype=torch.bfloat16)
+    est = oracle.estimate(oc, Q.float().numpy(), K.float().numpy())
+    covered = np.zeros(oc.M, bool)
+    for rank, ranges, ks, bu, cnt, idx in res:
+        assert np.array_equal(ks, est["kstar"]) and np.allclose(bu, est["kstar"] / oc.M)
+        for b, e in ranges:
+            assert not covered[b:e].any()
+            covered[b:e] = True
+            assert np.array_equal(cnt[:, b:e], est["block_cnt"][:, b:e])
+            assert np.array_equal(idx[:, b:e], est["block_idx"][:, b:e])
+    assert covered.all()

@@ -40,25 +40,47 @@ def np32(t):
     return t.float().cpu().numpy()
 
 
-def check_masks(ocfg, L_ref, kstar_gpu, cnt, idx, rows=None):
-    """Stage 4: oracle selection from the oracle's L with the GPU budgets injected."""
-    ocnt, oidx, cmg = oracle.select(ocfg, L_ref, kstar_gpu, rows=rows)
+def check_masks(ocfg, L_ref, kstar_gpu, cnt, idx, rows=None, per_head=False):
+    """Stage 4: oracle selection from the oracle's L (per_head: the comparator's per-head
+    maps) with the GPU budgets injected.  Every (head, row) is checked:
+    * the counts are equal (A5 is integer arithmetic);
+    * rows whose cut margin > 1e-4: the ascending lists are identical;
+    * near-tie rows: the GPU list is valid (ascending, in range, diagonal last) and may differ
+      from the oracle's only in blocks whose oracle score lies within 1e-4 of the cut (the
+      lowest kept non-diagonal score): a block only the GPU kept scores >= cut - 1e-4, a
+      block only the oracle kept scores <= cut + 1e-4, and there are as many of each.
+    Returns (exact rows, near-tie rows); prints the near-tie fraction."""
+    sel = oracle.select_heads if per_head else oracle.select
+    if per_head:
+        ocnt, oidx, cmg = sel(ocfg, L_ref, kstar_gpu)
+    else:
+        ocnt, oidx, cmg = sel(ocfg, L_ref, kstar_gpu, rows=rows)
     cnt, idx = cnt.cpu().numpy(), idx.cpu().numpy()
     rows = range(ocfg.M) if rows is None else rows
-    checked = skipped = 0
+    checked = near = 0
     for h in range(ocfg.n_q_heads):
+        grp = h if per_head else oracle.group_of_q(ocfg, h)
         for m in rows:
             assert cnt[h, m] == ocnt[h, m], (h, m)
+            c = ocnt[h, m]
+            got, ref = idx[h, m, :c], oidx[h, m, :c]
             if cmg[h, m] > MARGIN:
-                c = ocnt[h, m]
-                assert np.array_equal(idx[h, m, :c], oidx[h, m, :c]), (h, m, idx[h, m, :c], oidx[h, m, :c])
+                assert np.array_equal(got, ref), (h, m, got, ref)
                 checked += 1
-            else:
-                skipped += 1
-                c = cnt[h, m]
-                lst = idx[h, m, :c]                      # still a valid list
-                assert lst[-1] == m and np.all(np.diff(lst) > 0) and lst[0] >= 0
-    return checked, skipped
+                continue
+            near += 1
+            assert got[-1] == m and np.all(np.diff(got) > 0) and got[0] >= 0, (h, m, got)
+            lr = L_ref[grp, m, :m + 1]
+            kept = [n for n in ref[:-1] if not (ocfg.force_sink and n == 0)]
+            cut = lr[kept].min()
+            only_gpu, only_ref = np.setdiff1d(got, ref), np.setdiff1d(ref, got)
+            assert len(only_gpu) == len(only_ref), (h, m)
+            assert np.all(lr[only_gpu] >= cut - MARGIN) and np.all(lr[only_ref] <= cut + MARGIN), \
+                (h, m, cut, lr[only_gpu], lr[only_ref])
+    total = checked + near
+    if total:
+        print(f"selection: {checked} rows exact, {near} near-tie rows ({near / total:.2%}) within 1e-4 of the cut")
+    return checked, near
 
 
 def check_out(O_gpu, O_ref, fp32):
@@ -245,7 +267,9 @@ def test_single_block_and_gamma_one_equals_dense():
     assert torch.all(kstar == cfg1.M)
     O = pa.prefill(cfg1, Qd, Kd, Vd, cnt, idx)
     Od = pa.dense_prefill(cfg1, Qd, Kd, Vd)
-    # AC2: gamma = 1 -> dense (the sparse and dense launches may use different kernels)
+    # AC2: gamma = 1 -> dense.  The sparse launch (attn_tc8) and the dense baseline
+    # (attn_tc) are different kernels (different softmax reference points and P rounding),
+    # so they agree within the bf16 output tolerance, not bitwise.
     assert (O.float() - Od.float()).abs().max().item() <= 2e-2
     check_out(O, oracle.dense(ocfg_of(cfg1), np32(Q), np32(K), np32(V)), fp32=False)
     Os = pa.prefill(cfg1, Qd, Kd, Vd, cnt, idx)

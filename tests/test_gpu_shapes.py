@@ -177,14 +177,14 @@ def test_head_sharded_budgets_concat_equal_full(world):
     cfg = cfg_of(128, 128, 4096, heads=(8, 4))
     Q, K, V, _ = workloads.structured(8, 4, 4096, 128, seed=70)
     Qd, Kd, _ = to_dev(Q, K, V)
-    full, _ = pa.budgets(cfg, Qd, Kd)
-    parts = []
+    full, full_b = pa.budgets(cfg, Qd, Kd)
+    parts, bparts = [], []
     for rank in range(world):
-        def gather(dst, src, rank=rank):
-            parts.append(src.clone())
+        def gather(dst, src, rank=rank):       # K* (int32) and b_h = K*/M (fp32, from the library)
+            (parts if src.dtype == torch.int32 else bparts).append(src.clone())
             dst.zero_()
         shard.budgets_sharded(cfg, Qd, Kd, world, rank, all_gather=gather)
-    assert torch.equal(torch.cat(parts), full)
+    assert torch.equal(torch.cat(parts), full) and torch.equal(torch.cat(bparts), full_b)
 
 
 @pytest.mark.parametrize("d,b", SHAPES)
