@@ -50,6 +50,17 @@
 #include "sm100.cuh"
 #include "tma_host.h"
 
+// Energy-attribution experiments (never in the shipped build; scripts/attn_experiments.sh
+// builds them with PROXYATTN_NVCC_DEFINES and times the launch): each removes one component
+// of the per-block work and so produces WRONG outputs.  PA_X_NOMUFU: P = x instead of 2^x;
+// PA_X_NOLOAD: K/V TMA loads skipped after the rings are filled; PA_X_NOQK / PA_X_NOPV: the
+// S / PV tcgen05.mma skipped (commits kept); PA_X_EXBF16: ex2.approx.ftz.bf16x2 on a bf16
+// argument.  Any of them also disables the overflow flagging (no exact re-run).
+#if defined(PA_X_NOMUFU) || defined(PA_X_NOLOAD) || defined(PA_X_NOQK) || defined(PA_X_NOPV) || \
+    defined(PA_X_EXBF16)
+#define PA_X_ANY 1
+#endif
+
 namespace pa {
 namespace {
 
@@ -311,6 +322,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             int mem;
                             const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+#ifdef PA_X_NOLOAD
+                            if (gk >= kKStages) {
+                                mbar_arrive(&bars->k_full[st]);
+                                continue;
+                            }
+#endif
                             mbar_expect_tx(&bars->k_full[st], Sh::kKTile);
 #pragma unroll
                             for (int ch = 0; ch < kD / 64; ++ch)
@@ -337,6 +354,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         int mem;
                         const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+#ifdef PA_X_NOLOAD
+                        if (gv >= kVStages) {
+                            mbar_arrive(&bars->v_full[st]);
+                            continue;
+                        }
+#endif
                         mbar_expect_tx(&bars->v_full[st], Sh::kKTile);
 #pragma unroll
                         for (int ch = 0; ch < kD / 64; ++ch)
@@ -374,8 +397,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             for (int kk = 0; kk < kD / 16; ++kk) {
                                 const uint32_t offq = ((kk >> 2) * kBox + (kk & 3) * 32) >> 4;
                                 const uint32_t offk = ((kk >> 2) * Sh::kKBox + (kk & 3) * 32) >> 4;
+#ifndef PA_X_NOQK
                                 umma_ss(tbase + kColS + s * 128 + sb * 64, dq + offq, b0 + offk, idesc_qk,
                                         kk > 0 ? 1u : 0u);
+#endif
                             }
                             tc_commit(&bars->k_empty[st]);
                             tc_commit(&bars->s_full[s][sb]);
@@ -411,8 +436,10 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
                             for (int k4 = 0; k4 < 4; ++k4) {
                                 const int kk = half * 4 + k4;
+#ifndef PA_X_NOPV
                                 umma_ts(tbase + kColO, tbase + kColP + s * 64 + pb * 32 + kk * 8,
                                         b0 + (kk * 2048 >> 4), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+#endif
                             }
                         }
                         __syncwarp();
@@ -445,12 +472,14 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             mbar_wait(&bars->l_ready[it & 1], (it >> 1) & 1);
             const float l0 = bars->lsum[it & 1][0][rr], l1 = bars->lsum[it & 1][1][rr];
             const float inv = 1.f / (l0 + l1);
+#ifndef PA_X_ANY
             if (!exact) {   // a row whose P exceeded the bound (l = +inf marker): exact re-run
                 bool bad = !(l0 + l1 <= 2.f * exp2f(kOverflow));
                 if (kPair) bad = bad || (m >= 0 && l0 + l1 < exp2f(kUnderflow));
                 if (__any_sync(0xffffffffu, bad) && lane == 0)
                     flagged[atomicAdd(&sched->n_flagged, 1)] = x.item;   // <= 4 duplicates, benign
             }
+#endif
             mbar_wait(&bars->o_final, it & 1);
             tc_fence_after();
             const bool row_valid = m >= 0 && pos < c_N;
@@ -513,8 +542,21 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 } else {
                     float x0, x1;
                     f2_unpack(x2, x0, x1);
+#if defined(PA_X_NOMUFU)
+                    p0 = x0;
+                    p1 = x1;
+#elif defined(PA_X_EXBF16)
+                    uint32_t hb;
+                    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(hb) : "r"(pack_bf16(x0, x1)));
+                    p0 = __uint_as_float(hb << 16);
+                    p1 = __uint_as_float(hb & 0xffff0000u);
+                    ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
+                    pk[p] = hb;
+                    continue;
+#else
                     p0 = ex2(x0);
                     p1 = ex2(x1);
+#endif
                 }
                 ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
                 pk[p] = pack_bf16(p0, p1);
@@ -672,7 +714,9 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         l += block_exps(m_ref, n == m, true);
                     }
                 }
+#ifndef PA_X_ANY
                 if (!(l <= exp2f(kOverflow)) || xhi > kOverflow) l = INFINITY;   // flag the row
+#endif
             } else {
                 // exact: the row's true max over its own blocks first (S only), then the fixed pass
                 float tmax = -INFINITY;

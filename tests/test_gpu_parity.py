@@ -55,7 +55,8 @@ def check_masks(ocfg, L_ref, kstar_gpu, cnt, idx, rows=None, per_head=False):
         ocnt, oidx, cmg = sel(ocfg, L_ref, kstar_gpu)
     else:
         ocnt, oidx, cmg = sel(ocfg, L_ref, kstar_gpu, rows=rows)
-    cnt, idx = cnt.cpu().numpy(), idx.cpu().numpy()
+    cnt = cnt.cpu().numpy() if torch.is_tensor(cnt) else np.asarray(cnt)
+    idx = idx.cpu().numpy() if torch.is_tensor(idx) else np.asarray(idx)
     rows = range(ocfg.M) if rows is None else rows
     checked = near = 0
     for h in range(ocfg.n_q_heads):
