@@ -5,7 +5,7 @@ sweep lines; the same launch configuration bench.py times), checked against the 
 sampling of SURVEY §8(c).5: L rows first, last and 16 random per proxy group; Alg. 1 K* of
 EVERY head (margin-gated); the block lists of those rows for every head (margin-gated, near
 ties within 1e-4 of the cut); O on those rows for every head with the GPU mask injected.  At
-32K (config B) L and the lists are checked on EVERY row.  Plus properties at any size."""
+32K (config B) L, the lists and O are checked on EVERY row of every head.  Plus properties at any size."""
 import numpy as np
 import pytest
 import torch
@@ -112,7 +112,7 @@ def test_fullsize_sampled_parity(layer):
     assert checked >= 0.9 * (checked + near)
     del Lfull
     # stage 5: O on the sampled rows for EVERY head, GPU mask injected
-    orows = sample_rows(M, seed=1) if complete else rows
+    orows = rows                                             # config B: every row
     items = [(h, m) for h in range(H) for m in orows]
     cnt_h = layer["cnt"]
     idx = layer["idx"]
