@@ -55,9 +55,10 @@
 // of the per-block work and so produces WRONG outputs.  PA_X_NOMUFU: P = x instead of 2^x;
 // PA_X_NOLOAD: K/V TMA loads skipped after the rings are filled; PA_X_NOQK / PA_X_NOPV: the
 // S / PV tcgen05.mma skipped (commits kept); PA_X_EXBF16: ex2.approx.ftz.bf16x2 on a bf16
-// argument.  Any of them also disables the overflow flagging (no exact re-run).
+// argument; PA_X_HALFLOAD: every other K and V load skipped (half the L2 -> SMEM traffic);
+// PA_X_NOKLOAD / PA_X_NOVLOAD: only the K / only the V loads skipped.  Any of them also disables the overflow flagging (no exact re-run).
 #if defined(PA_X_NOMUFU) || defined(PA_X_NOLOAD) || defined(PA_X_NOQK) || defined(PA_X_NOPV) || \
-    defined(PA_X_EXBF16)
+    defined(PA_X_EXBF16) || defined(PA_X_HALFLOAD) || defined(PA_X_NOKLOAD) || defined(PA_X_NOVLOAD)
 #define PA_X_ANY 1
 #endif
 
@@ -322,8 +323,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             int mem;
                             const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
-#ifdef PA_X_NOLOAD
+#if defined(PA_X_NOLOAD) || defined(PA_X_NOKLOAD) || defined(PA_X_HALFLOAD)
+#ifdef PA_X_HALFLOAD
+                            if (gk >= kKStages && (j & 1)) {
+#else
                             if (gk >= kKStages) {
+#endif
                                 mbar_arrive(&bars->k_full[st]);
                                 continue;
                             }
@@ -354,8 +359,12 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         int mem;
                         const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
-#ifdef PA_X_NOLOAD
+#if defined(PA_X_NOLOAD) || defined(PA_X_NOVLOAD) || defined(PA_X_HALFLOAD)
+#ifdef PA_X_HALFLOAD
+                        if (gv >= kVStages && (j & 1)) {
+#else
                         if (gv >= kVStages) {
+#endif
                             mbar_arrive(&bars->v_full[st]);
                             continue;
                         }

@@ -296,26 +296,36 @@ __global__ void budget_mass_simt(Dims D, const T* __restrict__ Q, const T* __res
 }
 
 // Bitonic sort of (key, id) pairs in shared memory, order: key descending, id ascending.
-// A stage with stride <= 16 only pairs elements inside the 64-element segments a warp's 32
-// threads own (pair t: lo = 2t - t mod stride), so consecutive such stages need only a
-// __syncwarp; cross-warp stages (stride >= 32) and the end of every merge size keep the
-// block barrier.  Same comparisons, same result.
-__device__ __forceinline__ bool before(float ka, int ia, float kb, int ib) {
-    return ka > kb || (ka == kb && ia < ib);
+// Each pair is ONE 64-bit word: the high half is the key's bits mapped to an unsigned
+// integer of the same order (sign set: all bits flipped; else the sign bit set), the low
+// half ~id, so (key desc, id asc) is plain unsigned descending order and a compare-exchange
+// is one 64-bit compare plus two selects.  A stage with stride <= 16 only pairs elements
+// inside the 64-element segments a warp's 32 threads own (pair t: lo = 2t - t mod stride),
+// so consecutive such stages need only a __syncwarp; cross-warp stages (stride >= 32) and
+// the end of every merge size keep the block barrier.
+__device__ __forceinline__ unsigned long long sort_word(float key, int id) {
+    uint32_t u = __float_as_uint(key);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return (static_cast<unsigned long long>(u) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(id));
 }
-__device__ void bitonic_sort(float* key, int* id, int P) {
+__device__ __forceinline__ int word_id(unsigned long long w) {
+    return static_cast<int>(~static_cast<uint32_t>(w));
+}
+__device__ __forceinline__ float word_key(unsigned long long w) {
+    const uint32_t u = static_cast<uint32_t>(w >> 32);
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ void bitonic_sort(unsigned long long* v, int P) {
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
                 const int lo = 2 * t - (t & (stride - 1));
                 const int hi = lo + stride;
-                const bool asc = ((lo & size) == 0);  // "asc" = keep `before` order
-                const bool sw = asc ? before(key[hi], id[hi], key[lo], id[lo])
-                                    : before(key[lo], id[lo], key[hi], id[hi]);
-                if (sw) {
-                    const float tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
-                    const int ti = id[lo]; id[lo] = id[hi]; id[hi] = ti;
-                }
+                const unsigned long long a = v[lo], b = v[hi];
+                const unsigned long long mx = a > b ? a : b, mn = a > b ? b : a;
+                const bool desc = ((lo & size) == 0);   // this half of the merge runs descending
+                v[lo] = desc ? mx : mn;
+                v[hi] = desc ? mn : mx;
             }
             if (stride > 16) __syncthreads();
             else __syncwarp();
@@ -335,15 +345,15 @@ __global__ void budget_finalize_kernel(Dims D, const float* __restrict__ bmass,
                                        int* __restrict__ kstar, float* __restrict__ budget) {
     extern __shared__ unsigned char sm[];
     const int P = next_pow2(D.M);
-    float* key = reinterpret_cast<float*>(sm);
-    int* id = reinterpret_cast<int*>(key + P);
+    unsigned long long* v = reinterpret_cast<unsigned long long*>(sm);
+    float* key = reinterpret_cast<float*>(v + P);   // the masses in descending order
     const int hl = blockIdx.x;
-    for (int n = threadIdx.x; n < P; n += blockDim.x) {
-        key[n] = (n < D.M) ? bmass[static_cast<long long>(hl) * D.M + n] : -1.f;  // pads last
-        id[n] = n;
-    }
+    for (int n = threadIdx.x; n < P; n += blockDim.x)
+        v[n] = sort_word((n < D.M) ? bmass[static_cast<long long>(hl) * D.M + n] : -1.f, n);  // pads last
     __syncthreads();
-    bitonic_sort(key, id, P);
+    bitonic_sort(v, P);
+    for (int j = threadIdx.x; j < D.M; j += blockDim.x) key[j] = word_key(v[j]);
+    __syncthreads();
     // Alg. 1 lines 3-4 in parallel: contiguous chunks of the descending order per thread,
     // a deterministic block scan of the chunk sums (T = total), then the first prefix
     // k with P(k) >= gamma * T (a min-reduction over the threads' candidates).
@@ -405,18 +415,15 @@ __global__ void select_kernel(Dims D, const float* __restrict__ L, const int* __
     const int c = blockIdx.x / nr;
     const int m = D.re - 1 - (blockIdx.x % nr);  // long rows first
     const int P = next_pow2(max(m, 1));
-    float* key = reinterpret_cast<float*>(sm);
-    int* id = reinterpret_cast<int*>(key + next_pow2(D.M));
-    int* rank = id + next_pow2(D.M);
+    unsigned long long* v = reinterpret_cast<unsigned long long*>(sm);
+    int* rank = reinterpret_cast<int*>(v + next_pow2(D.M));
     const float* row = L + (static_cast<long long>(c) * D.M + m) * D.M;
     const bool sink = has_flag(D, PROXYATTN_FLAG_FORCE_SINK);
-    for (int n = threadIdx.x; n < P; n += blockDim.x) {
-        key[n] = (n < m) ? ((sink && n == 0) ? INFINITY : row[n]) : -INFINITY;  // forced sink first
-        id[n] = (n < m) ? n : INT_MAX;
-    }
+    for (int n = threadIdx.x; n < P; n += blockDim.x)   // forced sink first; pads (id INT_MAX) last
+        v[n] = (n < m) ? sort_word((sink && n == 0) ? INFINITY : row[n], n) : sort_word(-INFINITY, INT_MAX);
     __syncthreads();
-    if (m > 1) bitonic_sort(key, id, P);
-    for (int p = threadIdx.x; p < m; p += blockDim.x) rank[id[p]] = p;
+    if (m > 1) bitonic_sort(v, P);
+    for (int p = threadIdx.x; p < m; p += blockDim.x) rank[word_id(v[p])] = p;
     __syncthreads();
 
     const int grp = D.gb + c;
@@ -575,7 +582,7 @@ cudaError_t launch_budget_mass(const Dims& D, const void* Q, const void* K, cons
 cudaError_t launch_budget_finalize(const Dims& D, const float* bmass, int* kstar, float* budget,
                                    cudaStream_t st) {
     const int P = next_pow2(D.M);
-    const size_t sm = static_cast<size_t>(P) * 8;
+    const size_t sm = static_cast<size_t>(P) * 12;   // 64-bit sort words + the sorted masses
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(budget_finalize_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));

@@ -221,15 +221,16 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             if (c * 32 + e > thr) raw[c][e] = 0xff800000u;   // -inf
                 }
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    float m2[2] = {__uint_as_float(raw[g >> 1][(g & 1) * 16]),
-                                   __uint_as_float(raw[g >> 1][(g & 1) * 16 + 1])};
-#pragma unroll
-                    for (int e = 2; e < 16; ++e)
-                        m2[e & 1] = fmaxf(m2[e & 1], __uint_as_float(raw[g >> 1][(g & 1) * 16 + e]));
-                    h8[hf * 4 + g] = fmaxf(m2[0], m2[1]);
+                for (int g = 0; g < 4; ++g) {                // 16-column maxima: 8 FMNMX3 each
+                    const uint32_t* v = &raw[g >> 1][(g & 1) * 16];
+                    auto f = [&](int e) { return __uint_as_float(v[e]); };
+                    const float a0 = fmax3(f(0), f(1), f(2)), a1 = fmax3(f(3), f(4), f(5));
+                    const float a2 = fmax3(f(6), f(7), f(8)), a3 = fmax3(f(9), f(10), f(11));
+                    const float a4 = fmax3(f(12), f(13), f(14));
+                    h8[hf * 4 + g] = fmax3(fmax3(a0, a1, a2), fmax3(a3, a4, f(15)), -INFINITY);
                 }
-                const float hmax = fmaxf(fmaxf(h8[hf * 4], h8[hf * 4 + 1]), fmaxf(h8[hf * 4 + 2], h8[hf * 4 + 3])) * p.sc2;
+                const float hmax = fmax3(fmax3(h8[hf * 4], h8[hf * 4 + 1], h8[hf * 4 + 2]), h8[hf * 4 + 3],
+                                         -INFINITY) * p.sc2;
                 // exps of the half relative to ref (log2 units)
                 const float ref = (kMode == kLse) ? fmaxf(m_run, hmax) : hmax;
                 float acc = 0.f;
@@ -490,7 +491,10 @@ __global__ void __launch_bounds__(256) budget_mass_kernel(int M, int n_chunks, c
 
 // Exp2 split between MUFU and the FMA pipe in the score epilogues: 1/4 of the column pairs
 // on the FMA-pipe polynomial (A2 pass 213 -> 198 us, Alg. 1 pass 178 -> 166 us at 128K).
-constexpr int kScoreEmu = 1;
+#ifndef PA_SCORE_EMU
+#define PA_SCORE_EMU 1
+#endif
+constexpr int kScoreEmu = PA_SCORE_EMU;
 
 // Key tiles per CTA of the score passes; PROXYATTN_SCORE_CHUNK=16/32/64 overrides.
 // Key tiles per CTA of the proxy (A2) pass: the default unless the causal grid of this

@@ -309,6 +309,13 @@ __device__ __forceinline__ void ex2_poly2_d4(uint64_t x2, float& r0, float& r1) 
     r1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
 
+// Three-input max (sm_100 FMNMX3): one instruction where fmaxf(fmaxf(a, b), c) takes two.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
