@@ -7,7 +7,7 @@ on a short ragged sequence and synchronises, so an error is attributed to its ca
 the fp32 debug path, the bf16 tensor-core shapes d x b in {64, 128}^2, GQA ratios with an
 odd head count (b = 64 pairs with one head), token-major layouts, a zig-zag row range with
 kstar given, scores-only + select_ws, method variants, the varlen packed launch and the
-pipelined host path.  No oracle: this checks memory safety, not values (the parity tests do).
+pipelined host path, the seq-avgpool comparator and the CHECK_FINITE scan.  No oracle: this checks memory safety, not values (the parity tests do).
 """
 import sys
 
@@ -89,6 +89,27 @@ def main():
             cu.append(cu[-1] + n)
         pa.forward_varlen(pa.Config(8, 2, 128, 1, 128, 4, 1, 0.9, token_major=True), cu, *packed)
     case("varlen packed", varlen)
+
+    def avgpool():                                              # the seq-avgpool comparator (round 2)
+        for d, b in [(128, 128), (64, 64)]:
+            Q, K, V, _ = workloads.structured(8, 2, N, d, seed=9 + d, device=DEV)
+            cfg = pa.Config(8, 2, d, N, b, 4, 1, 0.9)
+            pa.avgpool_scores(cfg, Q, K)
+            pa.avgpool_estimate(cfg, Q, K)
+    case("seq-avgpool comparator scores + estimate", avgpool)
+
+    def check_finite():                                         # CHECK_FINITE scan, then a NaN (round 2)
+        Q, K, V, _ = workloads.structured(8, 2, N, 128, seed=10, device=DEV)
+        cfg = pa.Config(8, 2, 128, N, 128, 4, 1, 0.9, check_finite=True)
+        layer(cfg, Q, K, V)
+        Q[3, 100, 5] = float("nan")
+        try:
+            pa.estimate(cfg, Q, K)
+        except Exception:
+            pass
+        else:
+            raise AssertionError("NaN input not rejected")
+    case("CHECK_FINITE scan and rejection", check_finite)
 
     def host():
         cfg = pa.Config(8, 2, 128, 1000, 128, 4, 1, 0.9)
