@@ -74,6 +74,17 @@ constexpr float kUnderflow = -60.0f;       // log2 floor of a row sum under a no
 #ifndef PA_VSTAGES
 #define PA_VSTAGES 2
 #endif
+// exp2 split per shape (of every 8 key-column pairs, this many on the FMA-pipe cubic); build
+// defines so the split can be re-measured without editing the dispatch
+#ifndef PA_EMU_D128
+#define PA_EMU_D128 0
+#endif
+#ifndef PA_EMU_D64
+#define PA_EMU_D64 2
+#endif
+#ifndef PA_EMU_B64
+#define PA_EMU_B64 0
+#endif
 constexpr int kKStages = PA_KSTAGES;   // K ring (3) and V ring (2) stages of 32 KB tiles
 constexpr int kVStages = PA_VSTAGES;
 constexpr int kItemSlots = 4;
@@ -941,12 +952,13 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
     // 19.18-19.28 at 2/8); d = 64 (exp-bound: half the tensor work per exp2) 2/8 (13.2-13.3 ms
     // vs 13.4-13.6 at 3/8 and 13.8 at 4/8); b = 64 all-MUFU.
     AttnKernel kern = nullptr;
+    constexpr int e128 = PA_EMU_D128, e64 = PA_EMU_D64, eb64 = PA_EMU_B64;
     if (n_seqs > 0)            // varlen instantiations (b = 128)
-        kern = D.d == 128 ? kernel_with_attr<128, 128, 0, true>() : kernel_with_attr<64, 128, 2, true>();
+        kern = D.d == 128 ? kernel_with_attr<128, 128, e128, true>() : kernel_with_attr<64, 128, e64, true>();
     else if (D.d == 128)
-        kern = D.b == 128 ? kernel_with_attr<128, 128, 0>() : kernel_with_attr<128, 64, 0>();
+        kern = D.b == 128 ? kernel_with_attr<128, 128, e128>() : kernel_with_attr<128, 64, eb64>();
     else
-        kern = D.b == 128 ? kernel_with_attr<64, 128, 2>() : kernel_with_attr<64, 64, 2>();
+        kern = D.b == 128 ? kernel_with_attr<64, 128, e64>() : kernel_with_attr<64, 64, e64>();
     if (!kern) return cudaErrorInvalidValue;
     int dev = 0, n_sm = 0;
     cudaGetDevice(&dev);

@@ -6,9 +6,12 @@ same clocks), not a multi-GPU measurement.
 
     python scripts/rank_emulation.py [P] [N] [--graph] [--qwen]"""
 import json
+import os
 import sys
 
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2509_24745_b200 as pa
 from paper_2509_24745_b200 import shard
