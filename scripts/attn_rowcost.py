@@ -2,10 +2,12 @@
 per-head budgets: many short rows) against static top-K lists with the same total blocks
 (every row ~the same length), and dense.  Prints ms, blocks, ns per block, rows."""
 import json
+import os
 import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -2,10 +2,12 @@
 estimate's sparsity matches Table 8 (Llama gamma = 0.9): 16K 73.31 %, 32K 78.27 %,
 64K 83.19 %, 128K 83.86 %.  beta_hi = 3 beta_lo, sigma = 0.93, rho = 0.999."""
 import json
+import os
 import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -4,10 +4,12 @@ estimate's sparsity (gamma = 0.9, seed 0) matches a target, e.g. Table 8's Llama
 
     python scripts/calibrate_shape.py Hq Hkv d N b target [lo hi]"""
 import json
+import os
 import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -2,10 +2,12 @@
 against the same-run dense attention (Fig. 6b: estimation < 10 % of full attention, P:614;
 Table 5 stride cost side; cost model g/(n s^2)).  JSON lines."""
 import json
+import os
 import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -4,6 +4,9 @@ import json
 
 import torch
 
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

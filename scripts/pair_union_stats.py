@@ -3,10 +3,12 @@ on the bench inputs: (a) two heads of one KV head on the same block row, paired 
 (the kernel's plan), (b) two adjacent block rows (2p, 2p+1) of the same head.  Reports
 sum(union) / (sum(cnt) / 2): 1.0 = no waste."""
 import json
+import os
 import sys
 
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -3,6 +3,9 @@ the union of the two ascending block lists vs the sum of their lengths."""
 import numpy as np
 import torch
 
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E402
 import paper_2509_24745_b200 as pa
 import workloads
 

@@ -1,10 +1,13 @@
 """Packed variable-length batch through proxyattn_forward_varlen (one attention launch over all
 sequences) against one estimate + prefill call per sequence, same inputs; prints ms."""
 import json
+import os
 import sys
 
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2509_24745_b200 as pa
 import workloads
