@@ -3,7 +3,7 @@
  * (arXiv 2509.24745, "ProxyAttn: Guided Sparse Attention via Representative Heads").
  *
  * Citations: P:<line> = PAPER.md line (section / equation), S:<line> = SPEC.md line.
- * Steps A1-A8 are SURVEY.md §8(a); readings Z1-Z23 are listed in DESIGN.md.
+ * Steps A1-A8 are SURVEY.md §8(a); readings Z1-Z24 are listed in DESIGN.md.
  *
  * Conventions (every entry point):
  *  - All tensor pointers are caller-owned DEVICE memory (e.g. torch tensors), 16-byte
@@ -212,10 +212,12 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const v
  * the cfg's token strides); cfg->seq_len is ignored.  Each sequence is one ProxyAttn layer
  * of its own (estimate A1-A6 + prefill A7, the paper's method per sequence):
  * its pooling, budgets and selection see only its own tokens.  Empty sequences are skipped.
- * Everything is enqueued on `stream`; the estimate scratch is reused sequence after
- * sequence.  bf16 with b = 128: the sequences' block lists are kept side by side in the
- * workspace and ONE attention launch covers every sequence (longest first); otherwise one
- * prefill per sequence.  The sequence table travels as kernel parameters (no host copy), so
+ * Everything is ordered on `stream`.  bf16 with b = 128: the per-sequence estimates rotate
+ * over up to 8 lanes (`stream` plus library helper streams, forked and joined by events, each
+ * lane with its own scratch; fewer lanes when the longest sequence's scratch would exceed
+ * 1 GiB), the sequences' block lists are kept side by side in the workspace, and ONE
+ * attention launch covers every sequence (longest first); otherwise one estimate + prefill
+ * per sequence on `stream`.  The sequence table travels as kernel parameters (no host copy), so
  * the call is asynchronous.
  * kstar (optional, DEVICE [n_seqs][Hl] int32) receives each sequence's K*_h. */
 int proxyattn_varlen_workspace_bytes(const proxyattn_cfg* cfg, int32_t n_seqs,

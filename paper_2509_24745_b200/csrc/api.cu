@@ -597,9 +597,11 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
 // order).  bf16 with b = 128: every sequence's block lists are kept (packed, each with its own
 // M) and ONE persistent attention launch covers all sequences (work items of the longest
 // sequences first); otherwise one prefill per sequence.
+constexpr int kMaxLanes = 8;   // packed varlen: concurrent per-sequence estimates
 struct VarlenLayout {
-    size_t kstar, budget, cnt, idx, descs, ws, total;
-    size_t kstar2, budget2, ws2;   // packed: the second concurrent estimate's staging / scratch
+    size_t cnt, idx, descs, total;
+    int lanes;                                   // estimate lanes (streams), each with its own
+    size_t lane_kstar[kMaxLanes], lane_budget[kMaxLanes], lane_ws[kMaxLanes];   // staging / scratch
     bool packed;
 };
 static bool varlen_packed(const pa::Dims& D) {
@@ -632,17 +634,25 @@ static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu,
         }
     }
     size_t off = 0;
-    L.kstar = off;  off = pa::align256(off + (size_t)D.Hl * 4);
-    L.budget = off; off = pa::align256(off + (size_t)D.Hl * 4);
     L.cnt = off;    off = pa::align256(off + n_cnt * 4);
     L.idx = off;    off = pa::align256(off + n_idx * 4);
     L.descs = off;  off = pa::align256(off + (L.packed ? (size_t)n * sizeof(pa::SeqDesc) : 0));
-    L.ws = off;     off = pa::align256(off + pa::workspace_layout(D).total);
-    L.kstar2 = L.budget2 = L.ws2 = 0;
-    if (L.packed) {   // two sequences' estimates in flight (two streams)
-        L.kstar2 = off;  off = pa::align256(off + (size_t)D.Hl * 4);
-        L.budget2 = off; off = pa::align256(off + (size_t)D.Hl * 4);
-        L.ws2 = off;     off = pa::align256(off + pa::workspace_layout(D).total);
+    // packed: up to kMaxLanes sequences' estimates in flight on their own streams (short
+    // sequences' estimates are a few small, latency-bound launches each: concurrency fills the
+    // GPU), as many lanes as non-empty sequences, capped so the lanes' scratch stays <= 1 GiB
+    int nonempty = 0;
+    for (int32_t i = 0; i < n; ++i) nonempty += cu[i + 1] > cu[i];
+    const size_t scratch = pa::workspace_layout(D).total;
+    L.lanes = 1;
+    if (L.packed) {
+        const size_t cap = std::max<size_t>(2, (size_t(1) << 30) / std::max<size_t>(scratch, 1));
+        L.lanes = static_cast<int>(std::min<size_t>({static_cast<size_t>(kMaxLanes), cap,
+                                                     static_cast<size_t>(std::max(nonempty, 1))}));
+    }
+    for (int k = 0; k < L.lanes; ++k) {
+        L.lane_kstar[k] = off;  off = pa::align256(off + (size_t)D.Hl * 4);
+        L.lane_budget[k] = off; off = pa::align256(off + (size_t)D.Hl * 4);
+        L.lane_ws[k] = off;     off = pa::align256(off + scratch);
     }
     L.total = off;
     return PROXYATTN_OK;
@@ -711,16 +721,19 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
             PA_CUDA(pa::write_seq_descs(at<pa::SeqDesc>(ws, L.descs), descs.data(),
                                         static_cast<int>(descs.size()), st), "varlen descriptors");
     }
-    // packed: consecutive sequences' estimates alternate between `stream` and a second stream
-    // (each with its own scratch) so the short, latency-bound estimates overlap
-    cudaStream_t st2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (L.packed && !descs.empty()) {
-        if ((rc = helper_stream(st, 3, &st2))) return rc;
+    // packed: consecutive sequences' estimates rotate over L.lanes streams (`stream` and helper
+    // streams, each lane with its own scratch) so the short, latency-bound estimates overlap
+    cudaStream_t lane_st[kMaxLanes] = {st};
+    cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
+    const int lanes = (L.packed && !descs.empty()) ? L.lanes : 1;
+    if (lanes > 1) {
         PA_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
-        PA_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event create");
         PA_CUDA(cudaEventRecord(ev_fork, st), "record");
-        PA_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0), "wait");
+        for (int k = 1; k < lanes; ++k) {
+            if ((rc = helper_stream(st, 2 + k, &lane_st[k]))) return rc;   // kinds 3 ..
+            PA_CUDA(cudaEventCreateWithFlags(&ev_join[k], cudaEventDisableTiming), "event create");
+            PA_CUDA(cudaStreamWaitEvent(lane_st[k], ev_fork, 0), "wait");
+        }
     }
     int n_done = 0;
     for (int32_t i = 0; i < n_seqs; ++i) {
@@ -728,11 +741,11 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
         if (n == 0) continue;
         c.seq_len = n;
         const size_t qo = (size_t)cu[i] * D0.q_ts * el, ko = (size_t)cu[i] * D0.kv_ts * el;
-        const bool second = st2 && (n_done++ & 1);
-        cudaStream_t si = second ? st2 : st;
-        int32_t* ks = at<int32_t>(ws, second ? L.kstar2 : L.kstar);
-        float* bu = at<float>(ws, second ? L.budget2 : L.budget);
-        const size_t wo = second ? L.ws2 : L.ws;
+        const int lane = n_done++ % lanes;
+        cudaStream_t si = lane_st[lane];
+        int32_t* ks = at<int32_t>(ws, L.lane_kstar[lane]);
+        float* bu = at<float>(ws, L.lane_budget[lane]);
+        const size_t wo = L.lane_ws[lane];
         int32_t* cnt = at<int32_t>(ws, L.cnt) + cnt_off[i];
         int32_t* idx = at<int32_t>(ws, L.idx) + idx_off[i];
         rc = proxyattn_estimate(&c, static_cast<const char*>(Q) + qo, static_cast<const char*>(K) + ko,
@@ -748,11 +761,13 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
             PA_CUDA(cudaMemcpyAsync(kstar + (size_t)i * D0.Hl, ks, (size_t)D0.Hl * 4,
                                     cudaMemcpyDeviceToDevice, si), "varlen kstar");
     }
-    if (st2) {
-        PA_CUDA(cudaEventRecord(ev_join, st2), "record");
-        PA_CUDA(cudaStreamWaitEvent(st, ev_join, 0), "wait");
-        cudaEventDestroy(ev_fork);   // released once the recorded work completes
-        cudaEventDestroy(ev_join);
+    if (lanes > 1) {
+        for (int k = 1; k < lanes; ++k) {
+            PA_CUDA(cudaEventRecord(ev_join[k], lane_st[k]), "record");
+            PA_CUDA(cudaStreamWaitEvent(st, ev_join[k], 0), "wait");
+            cudaEventDestroy(ev_join[k]);   // released once the recorded work completes
+        }
+        cudaEventDestroy(ev_fork);
     }
     if (L.packed && !descs.empty()) {
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
