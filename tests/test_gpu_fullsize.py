@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 MARGIN = 1e-4
 
 
-# bench.py's workloads at full size: (Hq, Hkv, d, N, b, g, min budget, preset[, gamma])
+# bench.py's workloads at full size: (Hq, Hkv, d, N, b, g, min budget, preset[, gamma[, static K*]])
 WORKLOADS = {
     "llama3.1-8b-attn-128k": (32, 8, 128, 131072, 128, 1, 0, "llama-128k"),
     "llama3.1-8b-attn-128k-b64": (32, 8, 128, 131072, 64, 1, 0, "llama-128k"),
@@ -32,6 +32,7 @@ WORKLOADS = {
     "llama3.1-8b-attn-16k": (32, 8, 128, 16384, 128, 1, 0, "llama-16k"),     # bench --seq-len sweep
     "llama3.1-8b-attn-32k": (32, 8, 128, 32768, 128, 1, 0, "llama-32k"),     # BASELINE config B
     "llama3.1-8b-attn-64k": (32, 8, 128, 65536, 128, 1, 0, "llama-64k"),
+    "llama3.1-8b-attn-128k-fixed": (32, 8, 128, 131072, 128, 1, 0, "llama-128k", 0.9, 164),   # M-C-fixed
 }
 
 
@@ -40,7 +41,8 @@ def layer(request):
     dev = torch.device("cuda:0")
     Hq, Hkv, d, N, b, g, mb, preset, *rest = WORKLOADS[request.param]
     gamma = rest[0] if rest else 0.9
-    cfg = pa.Config(Hq, Hkv, d, N, b, 4, g, gamma, mb)
+    sk = rest[1] if len(rest) > 1 else 0                      # static K* (the M-C-fixed line)
+    cfg = pa.Config(Hq, Hkv, d, N, b, 4, g, gamma, mb, static_kstar=sk)
     Q, K, V, _ = workloads.structured(Hq, Hkv, N, d, seed=0, params=workloads.PRESETS[preset],
                                       device=dev)
     kstar, budget, cnt, idx = pa.estimate(cfg, Q, K)
@@ -48,7 +50,7 @@ def layer(request):
     qsum, ksum = pa.pool(cfg, Q, K)
     L = pa.proxy_scores(cfg, qsum, ksum)
     torch.cuda.synchronize()
-    oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, g, gamma, mb, round_bf16=True)
+    oc = oracle.Cfg(Hq, Hkv, d, N, b, 4, g, gamma, mb, round_bf16=True, static_kstar=sk)
     host = dict(Q=Q.float().cpu().numpy(), K=K.float().cpu().numpy(), V=V.float().cpu().numpy())
     return dict(name=request.param, cfg=cfg, oc=oc, kstar=kstar.cpu().numpy(), budget=budget.cpu().numpy(),
                 cnt=cnt.cpu().numpy(), idx=idx, O=O, L=L.cpu().numpy(), **host)
@@ -109,7 +111,10 @@ def test_fullsize_sampled_parity(layer):
     Lfull[:, rows] = Lref[:, rows]
     del Lref
     checked, near = check_masks(oc, Lfull, ks, layer["cnt"], layer["idx"], rows=rows)
-    assert checked >= 0.9 * (checked + near)
+    # a guard that the margin gate does not hide a systematic difference (near-tie rows are still
+    # validated by the near-tie rule above); with a static K* every head cuts the SAME shared
+    # order at the same rank, so one near-tie row counts once per head (2 of 18 rows at 128K)
+    assert checked >= (0.85 if cfg.static_kstar else 0.9) * (checked + near)
     del Lfull
     # stage 5: O on the sampled rows for EVERY head, GPU mask injected
     orows = rows                                             # config B: every row
