@@ -723,16 +723,32 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
     }
     // packed: consecutive sequences' estimates rotate over L.lanes streams (`stream` and helper
     // streams, each lane with its own scratch) so the short, latency-bound estimates overlap
-    cudaStream_t lane_st[kMaxLanes] = {st};
-    cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
+    // Every exit joins the forked lanes back into `stream` (an error path included: no helper
+    // stream is left running work the caller cannot order against) and destroys the events.
+    struct Lanes {
+        cudaStream_t st[kMaxLanes] = {};
+        cudaEvent_t fork = nullptr, join[kMaxLanes] = {};
+        int n = 1;
+        ~Lanes() {
+            for (int k = 1; k < n; ++k) {
+                if (st[k] && join[k] && cudaEventRecord(join[k], st[k]) == cudaSuccess)
+                    cudaStreamWaitEvent(st[0], join[k], 0);
+                if (join[k]) cudaEventDestroy(join[k]);   // released once the recorded work completes
+            }
+            if (fork) cudaEventDestroy(fork);
+        }
+    } lanes_g;
+    cudaStream_t* lane_st = lanes_g.st;
+    lane_st[0] = st;
     const int lanes = (L.packed && !descs.empty()) ? L.lanes : 1;
     if (lanes > 1) {
-        PA_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
-        PA_CUDA(cudaEventRecord(ev_fork, st), "record");
+        PA_CUDA(cudaEventCreateWithFlags(&lanes_g.fork, cudaEventDisableTiming), "event create");
+        PA_CUDA(cudaEventRecord(lanes_g.fork, st), "record");
         for (int k = 1; k < lanes; ++k) {
             if ((rc = helper_stream(st, 2 + k, &lane_st[k]))) return rc;   // kinds 3 ..
-            PA_CUDA(cudaEventCreateWithFlags(&ev_join[k], cudaEventDisableTiming), "event create");
-            PA_CUDA(cudaStreamWaitEvent(lane_st[k], ev_fork, 0), "wait");
+            PA_CUDA(cudaEventCreateWithFlags(&lanes_g.join[k], cudaEventDisableTiming), "event create");
+            lanes_g.n = k + 1;
+            PA_CUDA(cudaStreamWaitEvent(lane_st[k], lanes_g.fork, 0), "wait");
         }
     }
     int n_done = 0;
@@ -761,13 +777,14 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
             PA_CUDA(cudaMemcpyAsync(kstar + (size_t)i * D0.Hl, ks, (size_t)D0.Hl * 4,
                                     cudaMemcpyDeviceToDevice, si), "varlen kstar");
     }
-    if (lanes > 1) {
-        for (int k = 1; k < lanes; ++k) {
-            PA_CUDA(cudaEventRecord(ev_join[k], lane_st[k]), "record");
-            PA_CUDA(cudaStreamWaitEvent(st, ev_join[k], 0), "wait");
-            cudaEventDestroy(ev_join[k]);   // released once the recorded work completes
-        }
-        cudaEventDestroy(ev_fork);
+    for (int k = 1; k < lanes; ++k) {   // join the lanes (the guard then only destroys events)
+        PA_CUDA(cudaEventRecord(lanes_g.join[k], lane_st[k]), "record");
+        PA_CUDA(cudaStreamWaitEvent(st, lanes_g.join[k], 0), "wait");
+    }
+    lanes_g.n = 1;
+    for (int k = 1; k < lanes; ++k) {
+        cudaEventDestroy(lanes_g.join[k]);
+        lanes_g.join[k] = nullptr;
     }
     if (L.packed && !descs.empty()) {
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
