@@ -1,0 +1,22 @@
+# multicast K only (V per CTA): correctness at 48K / 128K, then interleaved A/B at 128K
+mkdir -p gpurun_out
+SO=paper_2509_24745_b200/libproxyattn.so
+python -m paper_2509_24745_b200.build --force > /dev/null && cp $SO /tmp/base.so
+PROXYATTN_NVCC_DEFINES="-DPA_MC=1" python -m paper_2509_24745_b200.build --force > /dev/null && cp $SO /tmp/mc.so
+for shape in "49152 32 8" "131072 32 8 llama-128k"; do
+  set -- $shape; pr=""; [ -n "$4" ] && pr="--preset $4"
+  cp /tmp/base.so $SO; timeout 120 python scripts/mc_check.py $1 $2 $3 $pr --save /tmp/O.pt > /dev/null 2>&1
+  cp /tmp/mc.so $SO; timeout 120 python scripts/mc_check.py $1 $2 $3 $pr --check /tmp/O.pt 2>&1 | tail -1
+done
+for rep in 1 2 3; do
+  for v in base mc; do
+    cp /tmp/$v.so $SO
+    timeout 200 python scripts/attn_time.py --tag "abk_$v" --steps 20 >> gpurun_out/r2_mck.jsonl 2>> gpurun_out/r2_mck.err
+  done
+done
+cp /tmp/base.so $SO
+python - <<'PY'
+import json
+for l in open("gpurun_out/r2_mck.jsonl"):
+    d = json.loads(l); print(d["tag"], round(d["ms"], 3), d["clocks"]["sm_mhz"])
+PY
