@@ -1,4 +1,6 @@
 # multicast debugging: which launch fails at 64K
+# (targets the round-2 row-pair multicast build, measured and reverted: see DESIGN.md §6 and
+# profiles/r02_attn_rowpair_multicast_ab.jsonl; PA_MC no longer exists in the tree)
 mkdir -p gpurun_out
 SO=paper_2509_24745_b200/libproxyattn.so
 PROXYATTN_NVCC_DEFINES="-DPA_MC=1" python -m paper_2509_24745_b200.build --force > /dev/null && cp $SO /tmp/mc.so
