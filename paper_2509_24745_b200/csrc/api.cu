@@ -412,9 +412,7 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     Nvtx r(block_cnt ? "A7 block-sparse attention" : "A8 dense attention");
     if (D.fp32)
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
-    else if (block_cnt == nullptr && !D.tok && D.d == 128 && D.b == 128)
-        PA_CUDA(pa::launch_attn_tc(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc dense");
-    else
+    else   // block-sparse (A7) or, with no lists, every causal block (A8): the same kernel
         PA_CUDA(pa::launch_attn_tc8(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc8");
     return PROXYATTN_OK;
 }

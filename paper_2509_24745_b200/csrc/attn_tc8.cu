@@ -333,7 +333,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             const int st = gk % kKStages;
                             if (gk >= kKStages) mbar_wait(&bars->k_empty[st], ((gk / kKStages) - 1) & 1);
                             int mem;
-                            const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                            const int n = kPair ? w.next(mem) : dense ? mA - j : __ldg(list + j);
 #if defined(PA_X_NOLOAD) || defined(PA_X_NOKLOAD) || defined(PA_X_HALFLOAD)
 #ifdef PA_X_HALFLOAD
                             if (gk >= kKStages && (j & 1)) {
@@ -369,7 +369,7 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         const int st = gv % kVStages;
                         if (gv >= kVStages) mbar_wait(&bars->v_empty[st], ((gv / kVStages) - 1) & 1);
                         int mem;
-                        const int n = kPair ? w.next(mem) : dense ? j : __ldg(list + j);
+                        const int n = kPair ? w.next(mem) : dense ? mA - j : __ldg(list + j);
 #if defined(PA_X_NOLOAD) || defined(PA_X_NOVLOAD) || defined(PA_X_HALFLOAD)
 #ifdef PA_X_HALFLOAD
                         if (gv >= kVStages && (j & 1)) {
@@ -701,7 +701,11 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 return n;
             };
             if (kPair && s == 1) w.next(dummy);
-            auto block_n = [&](int js) { return dense ? 2 * js + s : __ldg(list + 2 * js + s); };
+            // dense (b = 128): blocks in DESCENDING order, so the two streams' first blocks — the
+            // fixed softmax reference — are the diagonal and its neighbour, where a causal row's
+            // largest scores usually sit (ascending, the sink-side reference let rows overflow 2^32
+            // and re-run exactly: 11.7 of 117 ms at 128K)
+            auto block_n = [&](int js) { return dense ? m - (2 * js + s) : __ldg(list + 2 * js + s); };
             float l = 0.f;
             float m_ref;
             if (!exact) {

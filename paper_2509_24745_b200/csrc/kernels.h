@@ -37,9 +37,6 @@ cudaError_t launch_select(const Dims& D, const float* L, const int* kstar, int* 
 cudaError_t launch_attn_simt(const Dims& D, const void* Q, const void* K, const void* V,
                              const int* block_cnt, const int* block_idx, void* O,
                              cudaStream_t st);
-// A7/A8 bf16 tcgen05 attention; block lists null => dense.
-cudaError_t launch_attn_tc(const Dims& D, const void* Q, const void* K, const void* V,
-                           const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
 // Varlen (one packed launch over several sequences, token-major, b = 128): sequence s owns the
 // tokens [tok0, tok0 + N) of the packed tensors, its block lists start at cnt_off / idx_off
 // ([Hl][M] / [Hl][M][M] of its own M), and its work items are [item0, item0 + Hl * M).
