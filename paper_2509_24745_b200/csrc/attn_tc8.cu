@@ -146,9 +146,10 @@ struct PairWalk {
     int ca, cb, pa, pb, j;
     bool dense;
     __device__ __forceinline__ int next(int& mem) {
-        if (dense) {   // lists 0..ca-1 and 0..cb-1
-            mem = (j < ca ? 1 : 0) | (j < cb ? 2 : 0);
-            return j++;
+        if (dense) {   // lists 0..ca-1 and 0..cb-1, walked diagonal-first (see block_n below)
+            const int n = max(ca, cb) - 1 - j++;
+            mem = (n < ca ? 1 : 0) | (n < cb ? 2 : 0);
+            return n;
         }
         const int x = pa < ca ? __ldg(a + pa) : INT_MAX;
         const int y = pb < cb ? __ldg(b + pb) : INT_MAX;
