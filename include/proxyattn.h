@@ -214,8 +214,8 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Q_host, const v
  * its pooling, budgets and selection see only its own tokens.  Empty sequences are skipped.
  * Everything is ordered on `stream`.  bf16 with b = 128: the per-sequence estimates rotate
  * over up to 8 lanes (`stream` plus library helper streams, forked and joined by events, each
- * lane with its own scratch; fewer lanes when the longest sequence's scratch would exceed
- * 1 GiB), the sequences' block lists are kept side by side in the workspace, and ONE
+ * lane with its own scratch; fewer lanes — down to 2 — when the lanes' scratch would
+ * exceed 256 MiB), the sequences' block lists are kept side by side in the workspace, and ONE
  * attention launch covers every sequence (longest first); otherwise one estimate + prefill
  * per sequence on `stream`.  The sequence table travels as kernel parameters (no host copy), so
  * the call is asynchronous.

@@ -637,13 +637,14 @@ static int varlen_layout(const proxyattn_cfg* cfg, int32_t n, const int64_t* cu,
     L.descs = off;  off = pa::align256(off + (L.packed ? (size_t)n * sizeof(pa::SeqDesc) : 0));
     // packed: up to kMaxLanes sequences' estimates in flight on their own streams (short
     // sequences' estimates are a few small, latency-bound launches each: concurrency fills the
-    // GPU), as many lanes as non-empty sequences, capped so the lanes' scratch stays <= 1 GiB
+    // GPU), as many lanes as non-empty sequences, capped so the lanes' scratch stays <= 256 MiB
+    // (long sequences' estimates fill the GPU on their own: two lanes, as before)
     int nonempty = 0;
     for (int32_t i = 0; i < n; ++i) nonempty += cu[i + 1] > cu[i];
     const size_t scratch = pa::workspace_layout(D).total;
     L.lanes = 1;
     if (L.packed) {
-        const size_t cap = std::max<size_t>(2, (size_t(1) << 30) / std::max<size_t>(scratch, 1));
+        const size_t cap = std::max<size_t>(2, (size_t(256) << 20) / std::max<size_t>(scratch, 1));
         L.lanes = static_cast<int>(std::min<size_t>({static_cast<size_t>(kMaxLanes), cap,
                                                      static_cast<size_t>(std::max(nonempty, 1))}));
     }
