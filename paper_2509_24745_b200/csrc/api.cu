@@ -16,6 +16,12 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+// A7 at d = b = 128 runs the row-pair kernel (attn_tc9.cu); 0 selects attn_tc8 everywhere
+// (a build define for A/B timing, not a runtime switch)
+#ifndef PA_ATTN_V9
+#define PA_ATTN_V9 1
+#endif
+
 #include "../../include/proxyattn.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -412,6 +418,10 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     Nvtx r(block_cnt ? "A7 block-sparse attention" : "A8 dense attention");
     if (D.fp32)
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
+#if PA_ATTN_V9
+    else if (block_cnt && D.d == 128 && D.b == 128)   // A7 at d = b = 128: row-pair kernel
+        PA_CUDA(pa::launch_attn_tc9(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc9");
+#endif
     else   // block-sparse (A7) or, with no lists, every causal block (A8): the same kernel
         PA_CUDA(pa::launch_attn_tc8(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc8");
     return PROXYATTN_OK;
@@ -489,9 +499,10 @@ int proxyattn_forward_host(const proxyattn_cfg* cfg, const void* Qh, const void*
     // start), then V, then the remaining Q chunks in reverse order; each chunk's row-range
     // estimate (K* given) and attention run as soon as it has landed, and its O goes down on
     // a third stream.  The heaviest rows (the longest causal lists) thus compute while the rest
-    // of Q is still crossing PCIe.  Chunk edges sit on 128-row proxy tiles (and on b = 64 row
-    // pairs), so every chunk's lists and outputs equal the one-shot call's bit for bit.
-    const int align = std::max(D.b == 64 ? 2 : 1, std::max(1, 128 / D.bs));
+    // of Q is still crossing PCIe.  Chunk edges sit on 128-row proxy tiles (and on the block-row
+    // pairs of both attention kernels), so every chunk's lists and outputs equal the one-shot
+    // call's bit for bit.
+    const int align = std::max(2, 128 / D.bs);
     const int units = (D.M + align - 1) / align;
     // 16 row chunks (128K: 1 / 4 / 8 / 16 / 24 chunks -> 63.5 / 41.2 / 37.3 / 35.8 / 35.8 ms)
     const int n_ch = std::max(1, std::min(16, units));
@@ -711,7 +722,8 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
             sd.N = static_cast<int>(cu[i + 1] - cu[i]);
             sd.M = static_cast<int>((sd.N + D0.b - 1) / D0.b);
             sd.item0 = static_cast<int>(item0);
-            item0 += (long long)D0.Hl * sd.M;
+            item0 += (PA_ATTN_V9 && D0.d == 128) ? (long long)pa::attn_tc9_units(D0.Hl, sd.M)
+                                                 : (long long)D0.Hl * sd.M;
             descs.push_back(sd);
         }
         if (item0 > INT32_MAX || cu[n_seqs] > INT32_MAX)
@@ -789,11 +801,18 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
         pa::Dims D;               // (each sequence's M was checked by varlen_layout; the packed
         if ((rc = derive(&c, D, false))) return rc;   // total may exceed one sequence's limit)
-        const int n_items = descs.back().item0 + D.Hl * descs.back().M;
-        PA_CUDA(pa::launch_attn_tc8_varlen(D, Q, K, V, at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), O,
-                                           at<pa::SeqDesc>(ws, L.descs), static_cast<int>(descs.size()),
-                                           n_items, st),
-                "attn_tc8 varlen");
+        const bool v9 = PA_ATTN_V9 && D.d == 128;
+        const int n_items = descs.back().item0 + (v9 ? static_cast<int>(pa::attn_tc9_units(D.Hl, descs.back().M))
+                                                      : D.Hl * descs.back().M);
+        if (v9)
+            PA_CUDA(pa::launch_attn_tc9(D, Q, K, V, at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), O, st,
+                                        at<pa::SeqDesc>(ws, L.descs), static_cast<int>(descs.size()), n_items),
+                    "attn_tc9 varlen");
+        else
+            PA_CUDA(pa::launch_attn_tc8_varlen(D, Q, K, V, at<int32_t>(ws, L.cnt), at<int32_t>(ws, L.idx), O,
+                                               at<pa::SeqDesc>(ws, L.descs), static_cast<int>(descs.size()),
+                                               n_items, st),
+                    "attn_tc8 varlen");
     }
     return PROXYATTN_OK;
 }

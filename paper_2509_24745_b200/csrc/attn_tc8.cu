@@ -85,6 +85,10 @@ constexpr float kUnderflow = -60.0f;       // log2 floor of a row sum under a no
 #ifndef PA_EMU_B64
 #define PA_EMU_B64 0
 #endif
+// bf16 pack of P (build define for A/B timing): 0 F2FP (RNE)
+#ifndef PA_PACK
+#define PA_PACK 0
+#endif
 constexpr int kKStages = PA_KSTAGES;   // K ring (3) and V ring (2) stages of 32 KB tiles
 constexpr int kVStages = PA_VSTAGES;
 constexpr int kItemSlots = 4;
@@ -579,8 +583,19 @@ attn_tc8_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     p1 = ex2(x1);
 #endif
                 }
+#if PA_PACK == 1          // truncating pack (one PRMT), row sum of the fp32 values
+                ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
+                pk[p] = __byte_perm(__float_as_uint(p0), __float_as_uint(p1), 0x7632);
+#elif PA_PACK == 2        // round half up on the integer pipe (RNE except exact ties)
+                ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
+                pk[p] = __byte_perm(__float_as_uint(p0) + 0x8000u, __float_as_uint(p1) + 0x8000u, 0x7632);
+#elif PA_PACK == 3        // truncating pack, row sum of the truncated values
+                pk[p] = __byte_perm(__float_as_uint(p0), __float_as_uint(p1), 0x7632);
+                ls[p & 3] = f2_add(ls[p & 3], f2_pack(__uint_as_float(pk[p] << 16), __uint_as_float(pk[p] & 0xffff0000u)));
+#else
                 ls[p & 3] = f2_add(ls[p & 3], f2_pack(p0, p1));
                 pk[p] = pack_bf16(p0, p1);
+#endif
             }
             if (wait_free && gp >= kNB) {                // the PV kNB blocks back has read the buffer
                 mbar_wait(&bars->p_free[s][gp % kNB], ((gp / kNB) - 1) & 1);
@@ -1012,6 +1027,27 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
 }
 
 }  // namespace
+
+// Shared with attn_tc9.cu: the per-(device, stream) scheduler state for a launch pair of
+// n_items work units, zeroed on `st`, and (sparse, 1 < Hkvl <= 64) the KV-head order over the
+// launch's rows.  Returns the device pointers through the out-parameters.
+cudaError_t attn_sched_prepare(const Dims& D, const int* block_cnt, size_t n_items, cudaStream_t st,
+                               void** sched, int** flagged, const int** kvperm) {
+    SchedBuf* sb = sched_for(st, n_items);
+    if (!sb) return cudaErrorMemoryAllocation;
+    cudaError_t e = cudaMemsetAsync(sb->sched, 0, sizeof(Sched), st);
+    if (e != cudaSuccess) return e;
+    *kvperm = nullptr;
+    if (block_cnt && D.Hkvl > 1 && D.Hkvl <= 64) {
+        kv_order_kernel<<<D.Hkvl, 1024, 0, st>>>(block_cnt, D.M, D.r, D.rb, D.re, D.Hkvl, sb->kvsum,
+                                                 sb->kvdone, sb->kvperm);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        *kvperm = sb->kvperm;
+    }
+    *sched = sb->sched;
+    *flagged = sb->flagged;
+    return cudaSuccess;
+}
 
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st) {

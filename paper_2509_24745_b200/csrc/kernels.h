@@ -53,6 +53,15 @@ cudaError_t launch_attn_tc8_varlen(const Dims& D, const void* Q, const void* K, 
                                    const SeqDesc* seqs, int n_seqs, int n_items, cudaStream_t st);
 cudaError_t launch_attn_tc8(const Dims& D, const void* Q, const void* K, const void* V,
                             const int* block_cnt, const int* block_idx, void* O, cudaStream_t st);
+// Scheduler state of an attention launch pair (attn_tc8.cu), shared by attn_tc9.cu.
+cudaError_t attn_sched_prepare(const Dims& D, const int* block_cnt, size_t n_items, cudaStream_t st,
+                               void** sched, int** flagged, const int** kvperm);
+// A7 row-pair kernel (d = b = 128, sparse): work units = (head, block-row pair); varlen when
+// n_seqs > 0 (sequence s owns units [item0, item0 + attn_tc9_units(Hl, M_s))).
+size_t attn_tc9_units(int Hl, int M);
+cudaError_t launch_attn_tc9(const Dims& D, const void* Q, const void* K, const void* V, const int* block_cnt,
+                            const int* block_idx, void* O, cudaStream_t st, const SeqDesc* seqs = nullptr,
+                            int n_seqs = 0, int varlen_items = 0);
 // tcgen05 estimation (bf16, d = b = 128, s = 4): A2+A3 and A4 (see score_tc.cu).
 bool score_tc_supported(const Dims& D);
 size_t score_tc_scratch_bytes(const Dims& D);

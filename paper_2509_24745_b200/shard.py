@@ -135,10 +135,11 @@ def work_share(block_cnt_full: torch.Tensor, n_kv_heads: int, world: int) -> lis
 
 
 def row_align(cfg) -> int:
-    """Block rows per attention work unit: 2 for block size 64 (the kernel packs the row pair
-    (2q, 2q+1) of one head into its 128 lanes), else 1.  Row ranges aligned to it give
-    outputs bit-identical to the unsharded launch."""
-    return 2 if cfg.block_size == 64 else 1
+    """Block rows per attention work unit: 2 — the attention kernels work on block-row pairs
+    (2q, 2q+1) of one head: at b = 64 packed into one 128-lane tile, at d = b = 128 sharing
+    their K/V tiles (attn_tc9).  Row ranges aligned to it give outputs bit-identical to the
+    unsharded launch (an unaligned edge splits a pair: within tolerance, not bitwise)."""
+    return 2
 
 
 def zigzag_rows(M: int, world: int, rank: int, align: int = 1) -> list[tuple[int, int]]:

@@ -394,12 +394,20 @@ def test_row_range_prefill_matches_full_bitwise():
     for world in (2, 3):
         O = torch.zeros_like(full)
         for rank in range(world):
-            shard.prefill_rows(cfg, Qd, Kd, Vd, cnt, idx, O, shard.zigzag_rows(cfg.M, world, rank))
+            shard.prefill_rows(cfg, Qd, Kd, Vd, cnt, idx, O,
+                               shard.zigzag_rows(cfg.M, world, rank, shard.row_align(cfg)))
         assert torch.equal(O, full)
-    part = torch.zeros_like(full)
-    pa.prefill(cfg.replace(row_begin=5, row_end=12), Qd, Kd, Vd, cnt, idx, part)
-    assert torch.equal(part[:, 5 * 128:12 * 128], full[:, 5 * 128:12 * 128])
-    assert torch.all(part[:, :5 * 128] == 0) and torch.all(part[:, 12 * 128:] == 0)
+    # a range aligned to the kernel's block-row pairs: bit for bit; an unaligned one splits a
+    # pair (row 5 alone: its own two first blocks set its reference) -> within tolerance
+    for b, e, exact in ((4, 12, True), (5, 12, False)):
+        part = torch.zeros_like(full)
+        pa.prefill(cfg.replace(row_begin=b, row_end=e), Qd, Kd, Vd, cnt, idx, part)
+        if exact:
+            assert torch.equal(part[:, b * 128:e * 128], full[:, b * 128:e * 128])
+        else:
+            d = (part[:, b * 128:e * 128].float() - full[:, b * 128:e * 128].float()).abs()
+            assert d.max().item() <= 2e-2 and d.mean().item() <= 2e-3
+        assert torch.all(part[:, :b * 128] == 0) and torch.all(part[:, e * 128:] == 0)
 
 
 def test_score_spikes_wide_dynamic_range():
