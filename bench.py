@@ -678,7 +678,8 @@ def run_ours(args):
     peak_burst = pk["bf16_tflops"]
     peak_sus = pk.get("bf16_tflops_sustained", peak_burst)
     achieved = flops_exec / (att_m * 1e-3) / 1e12
-    kname = "attn_tc8_kernel"
+    # A7 kernel of this shape: the row-pair kernel at d = b = 128, attn_tc8 otherwise
+    kname = "attn_tc9_kernel" if (b == 128 and d == 128) else "attn_tc8_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tp):
@@ -745,7 +746,7 @@ def run_ours(args):
         "verified": verified,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # attn_tc8 is two launches per prefill call: the fast pass and the exact re-run of
+        # the attention is two launches per prefill call: the fast pass and the exact re-run of
         # the rows it flagged (an empty list at these inputs), plus the KV-head order
         # (and the row-pair union at b = 64); estimate: 8 kernels (4 of them Alg. 1), a
         # row-range estimate adds 4 per extra range
