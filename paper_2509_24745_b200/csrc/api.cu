@@ -21,6 +21,11 @@
 #ifndef PA_ATTN_V9
 #define PA_ATTN_V9 1
 #endif
+// ... and at d = 64, b = 128 as well
+#ifndef PA_ATTN_V9_D64
+#define PA_ATTN_V9_D64 0
+#endif
+static bool use_v9(int d, int b) { return PA_ATTN_V9 && b == 128 && (d == 128 || (PA_ATTN_V9_D64 && d == 64)); }
 
 #include "../../include/proxyattn.h"
 #include "common.cuh"
@@ -419,7 +424,7 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32)
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
 #if PA_ATTN_V9
-    else if (block_cnt && D.d == 128 && D.b == 128)   // A7 at d = b = 128: row-pair kernel
+    else if (block_cnt && use_v9(D.d, D.b))   // A7 at b = 128: the row-pair kernel
         PA_CUDA(pa::launch_attn_tc9(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc9");
 #endif
     else   // block-sparse (A7) or, with no lists, every causal block (A8): the same kernel
@@ -722,7 +727,7 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
             sd.N = static_cast<int>(cu[i + 1] - cu[i]);
             sd.M = static_cast<int>((sd.N + D0.b - 1) / D0.b);
             sd.item0 = static_cast<int>(item0);
-            item0 += (PA_ATTN_V9 && D0.d == 128) ? (long long)pa::attn_tc9_units(D0.Hl, sd.M)
+            item0 += use_v9(D0.d, D0.b) ? (long long)pa::attn_tc9_units(D0.Hl, sd.M)
                                                  : (long long)D0.Hl * sd.M;
             descs.push_back(sd);
         }
@@ -801,7 +806,7 @@ int proxyattn_forward_varlen(const proxyattn_cfg* cfg, int32_t n_seqs, const int
         c.seq_len = cu[n_seqs];   // the packed tensors: TMA maps over every token
         pa::Dims D;               // (each sequence's M was checked by varlen_layout; the packed
         if ((rc = derive(&c, D, false))) return rc;   // total may exceed one sequence's limit)
-        const bool v9 = PA_ATTN_V9 && D.d == 128;
+        const bool v9 = use_v9(D.d, D.b);
         const int n_items = descs.back().item0 + (v9 ? static_cast<int>(pa::attn_tc9_units(D.Hl, descs.back().M))
                                                       : D.Hl * descs.back().M);
         if (v9)

@@ -15,17 +15,18 @@ import paper_2509_24745_b200 as pa  # noqa: E402
 import workloads  # noqa: E402
 
 dev = torch.device("cuda:0")
+D = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 cases = [(2, 1, 256), (2, 1, 384), (8, 2, 1024), (8, 2, 3000)]
 for Hq, Hkv, N in cases:
-    cfg = pa.Config(Hq, Hkv, 128, N, 128, 4, 1, 0.9)
-    Q, K, V, _ = workloads.structured(Hq, Hkv, N, 128, seed=0, device="cpu")
+    cfg = pa.Config(Hq, Hkv, D, N, 128, 4, 1, 0.9)
+    Q, K, V, _ = workloads.structured(Hq, Hkv, N, D, seed=0, device="cpu")
     Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
     kstar, budget, cnt, idx = pa.estimate(cfg, Qd, Kd)
     torch.cuda.synchronize()
-    print("case", Hq, Hkv, N, "cnt sum", int(cnt.sum()), flush=True)
+    print("case d", D, Hq, Hkv, N, "cnt sum", int(cnt.sum()), flush=True)
     O = pa.prefill(cfg, Qd, Kd, Vd, cnt, idx)
     torch.cuda.synchronize()
-    oc = oracle.Cfg(Hq, Hkv, 128, N, 128, 4, 1, 0.9, round_bf16=True)
+    oc = oracle.Cfg(Hq, Hkv, D, N, 128, 4, 1, 0.9, round_bf16=True)
     Oref = oracle.attention(oc, Q.float().numpy(), K.float().numpy(), V.float().numpy(),
                             cnt.cpu().numpy(), idx.cpu().numpy())
     err = np.abs(O.float().cpu().numpy() - Oref)
