@@ -16,20 +16,12 @@
 
 #include <nvtx3/nvToolsExt.h>
 
-// A7 at d = b = 128 runs the row-pair kernel (attn_tc9.cu); 0 selects attn_tc8 everywhere
-// (a build define for A/B timing, not a runtime switch)
-#ifndef PA_ATTN_V9
-#define PA_ATTN_V9 1
-#endif
-// ... and at d = 64, b = 128 as well
-#ifndef PA_ATTN_V9_D64
-#define PA_ATTN_V9_D64 0
-#endif
-static bool use_v9(int d, int b) { return PA_ATTN_V9 && b == 128 && (d == 128 || (PA_ATTN_V9_D64 && d == 64)); }
-
 #include "../../include/proxyattn.h"
 #include "common.cuh"
 #include "kernels.h"
+
+// A7 kernel choice: the row-pair attn_tc9 at d = b = 128 (PA_ATTN_V9, common.cuh), else attn_tc8
+static bool use_v9(int d, int b) { return PA_ATTN_V9 && b == 128 && d == 128; }
 
 namespace {
 

@@ -973,8 +973,13 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
     // vs 13.4-13.6 at 3/8 and 13.8 at 4/8); b = 64 all-MUFU.
     AttnKernel kern = nullptr;
     constexpr int e128 = PA_EMU_D128, e64 = PA_EMU_D64, eb64 = PA_EMU_B64;
-    if (n_seqs > 0)            // varlen instantiations (b = 128)
+    if (n_seqs > 0) {          // varlen instantiations (b = 128; d = 128 is attn_tc9's)
+#if PA_ATTN_V9
+        kern = D.d == 128 ? nullptr : kernel_with_attr<64, 128, e64, true>();
+#else
         kern = D.d == 128 ? kernel_with_attr<128, 128, e128, true>() : kernel_with_attr<64, 128, e64, true>();
+#endif
+    }
     else if (D.d == 128)
         kern = D.b == 128 ? kernel_with_attr<128, 128, e128>() : kernel_with_attr<128, 64, eb64>();
     else

@@ -1,5 +1,11 @@
 // common.cuh — derived configuration shared by the host API and the kernels of libproxyattn.
 #pragma once
+
+// A7 at d = b = 128 runs the row-pair kernel (attn_tc9.cu); 0 selects attn_tc8 everywhere
+// (a build define for A/B timing, not a runtime switch)
+#ifndef PA_ATTN_V9
+#define PA_ATTN_V9 1
+#endif
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
