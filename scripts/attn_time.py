@@ -36,7 +36,8 @@ def main():
     w = bench.WORKLOADS[a.workload]
     dev = torch.device("cuda:0")
     cfg = pa.Config(w["n_q_heads"], w["n_kv_heads"], w["head_dim"], w["seq_len"], w["block_size"],
-                    w["stride"], w["n_groups"], w["gamma"], w["min_budget_tokens"])
+                    w["stride"], w["n_groups"], w["gamma"], w["min_budget_tokens"],
+                    static_kstar=w.get("static_kstar", 0))
     Q, K, V, _ = workloads.structured(cfg.n_q_heads, cfg.n_kv_heads, cfg.seq_len, cfg.head_dim, seed=0,
                                       params=workloads.PRESETS[w["preset"]], device=dev)
     kstar, budget, cnt, idx = pa.estimate(cfg, Q, K)
