@@ -324,3 +324,59 @@ def test_forward_host_many_chunks_ragged(token_major, d, b):
     assert torch.equal(ks, kstar.cpu())
     ref = O.cpu()
     assert torch.equal(Oh.transpose(0, 1) if token_major else Oh, ref)
+
+
+@pytest.mark.parametrize("pattern", ["identical", "disjoint", "diag_only_partner", "shifted_first",
+                                     "spike_in_partner"])
+def test_row_pair_kernel_list_patterns(pattern):
+    # attn_tc9 (d = b = 128) walks the MERGED lists of block rows (2q+1, 2q) and shares a K/V
+    # tile between consecutive tasks on the same block; each row's reference is the max of its
+    # own first block.  Lists built to stress that walk: identical pair lists (every tile
+    # shared), disjoint ones (none shared), a partner with only its diagonal, first blocks that
+    # differ between the rows, and a score spike (+40 log2 units) seen by one row only of each
+    # pair after its first block (+50 log2 units on every odd row: exact re-run of the pair).  M = 17: a lone last row.
+    N, H, Hkv = 17 * 128, 4, 1
+    cfg = cfg_of(128, 128, N, heads=(H, Hkv))
+    M = cfg.M
+    Q, K, V, _ = workloads.structured(H, Hkv, N, 128, seed=40)
+    if pattern == "spike_in_partner":
+        Q = Q.clone()
+        K = K.clone()
+        # key block 5 strongly aligned with the queries of the odd rows (2q+1) only
+        d = torch.randn(128, generator=torch.Generator().manual_seed(41))
+        d = d / d.norm()
+        for m in range(1, M, 2):
+            Q[:, m * 128:(m + 1) * 128] += 24.0 * d
+        K[:, 5 * 128:6 * 128] += 24.0 * d
+        Q, K = Q.bfloat16(), K.bfloat16()
+        # the spike overflows the fast reference (2^32 headroom) on odd rows: exact re-run
+        q, k = Q[0, 7 * 128:8 * 128].float(), K[0].float()
+        x = (q @ k.T) / (128 ** 0.5) * 1.4426950408889634
+        assert (x[:, 5 * 128:6 * 128].max(1).values - x[:, :128].max(1).values).max() > 32
+    rng = np.random.default_rng(42)
+    cnt = np.zeros((H, M), np.int32)
+    idx = np.zeros((H, M, M), np.int32)
+    for h in range(H):
+        for m in range(M):
+            q, odd = m // 2, m % 2
+            if pattern == "identical":        # both rows of a pair: the same blocks below 2q
+                base = [n for n in range(2 * q) if (n * 7 + h + q) % 3 == 0]
+            elif pattern == "disjoint":       # even rows: even blocks, odd rows: odd blocks
+                base = [n for n in range(m) if n % 2 == odd]
+            elif pattern == "diag_only_partner":
+                base = list(range(0, m, 2)) if odd else []
+            elif pattern == "shifted_first":  # odd rows start at block 1, even rows at block 0
+                base = sorted({odd} | {int(x) for x in rng.choice(max(m, 1), size=min(m, 3), replace=False)}) if m > 1 else []
+                base = [n for n in base if n < m]
+            else:                             # spike: every row sees block 0 first, then block 5
+                base = [n for n in (0, 5) if n < m]
+            lst = sorted(set(base) | {m})
+            cnt[h, m] = len(lst)
+            idx[h, m, :len(lst)] = lst
+    Qd, Kd, Vd = to_dev(Q, K, V)
+    O = pa.prefill(cfg, Qd, Kd, Vd, torch.from_numpy(cnt).to(DEV), torch.from_numpy(idx).to(DEV))
+    ref = oracle.attention(ocfg_of(cfg), np32(Q), np32(K), np32(V), cnt, idx)
+    check_out(O, ref, fp32=False)
+    # deterministic across calls (dynamic schedule, unit-local task parity)
+    O2 = pa.prefill(cfg, Qd, Kd, Vd, torch.from_numpy(cnt).to(DEV), torch.from_numpy(idx).to(DEV))
+    assert torch.equal(O, O2)
