@@ -62,7 +62,7 @@ alg1_ws = pa.alloc_workspace(cfg, dev)
 aux = torch.cuda.Stream()
 graphs = "--graph" in sys.argv     # replay the row estimate and the attention from CUDA graphs, as bench.py
 for r in range(P):
-    rows = shard.zigzag_rows(M, P, r)
+    rows = shard.zigzag_rows(M, P, r, shard.row_align(cfg))
 
     def alg1(r=r):
         shard.budgets_sharded(cfg, Q, K, P, r, alg1_ws, all_gather=lambda d, s: d.copy_(kfull), out=(kstar, budget))
