@@ -146,9 +146,10 @@ int proxyattn_estimate(const proxyattn_cfg* cfg, const void* Q, const void* K,
  * Q[h][t]·K[kv(h)][k]/sqrt(d), times V.  Accepts ANY valid lists (non-empty, ascending,
  * in range, n <= m), so oracle masks can be injected.  With PROXYATTN_FLAG_CHECK the
  * lists are validated on the device first and E_SHAPE is returned on a violation
- * (this flag synchronises the stream).  b = 64 works on row PAIRS (2q, 2q+1) of a head: a
- * [row_begin, row_end) range aligned to even rows gives outputs bit-identical to the full
- * launch; an unaligned one splits a pair (results within the bf16 tolerance, not bitwise). */
+ * (this flag synchronises the stream).  b = 64 and d = b = 128 work on row PAIRS (2q, 2q+1)
+ * of a head (b = 64: one 128-lane tile; d = b = 128: shared K/V tiles): a [row_begin,
+ * row_end) range aligned to even rows gives outputs bit-identical to the full launch; an
+ * unaligned one splits a pair (results within the bf16 tolerance, not bitwise). */
 int proxyattn_prefill(const proxyattn_cfg* cfg, const void* Q, const void* K, const void* V,
                       const int32_t* block_cnt, const int32_t* block_idx, void* O,
                       void* stream);
