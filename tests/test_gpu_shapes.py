@@ -327,30 +327,36 @@ def test_forward_host_many_chunks_ragged(token_major, d, b):
 
 
 @pytest.mark.parametrize("pattern", ["identical", "disjoint", "diag_only_partner", "shifted_first",
-                                     "spike_in_partner"])
+                                     "spike_in_partner", "spike_in_even", "spike_in_both"])
 def test_row_pair_kernel_list_patterns(pattern):
     # attn_tc9 (d = b = 128) walks the MERGED lists of block rows (2q+1, 2q) and shares a K/V
     # tile between consecutive tasks on the same block; each row's reference is the max of its
     # own first block.  Lists built to stress that walk: identical pair lists (every tile
     # shared), disjoint ones (none shared), a partner with only its diagonal, first blocks that
-    # differ between the rows, and a score spike (+40 log2 units) seen by one row only of each
-    # pair after its first block (+50 log2 units on every odd row: exact re-run of the pair).  M = 17: a lone last row.
+    # differ between the rows, and score spikes (+50 log2 units over the first block) in the
+    # second block of the odd rows, the even rows or all rows: the exact launch re-runs row 0,
+    # row 1 or both rows of the pairs (the per-row mask).  M = 17: a lone last row.
     N, H, Hkv = 17 * 128, 4, 1
     cfg = cfg_of(128, 128, N, heads=(H, Hkv))
     M = cfg.M
     Q, K, V, _ = workloads.structured(H, Hkv, N, 128, seed=40)
-    if pattern == "spike_in_partner":
+    spike = pattern.startswith("spike")
+    if spike:
         Q = Q.clone()
         K = K.clone()
-        # key block 5 strongly aligned with the queries of the odd rows (2q+1) only
+        # key block 5 strongly aligned with the queries of the odd rows (2q+1: the exact launch
+        # re-runs row 0 of each pair), the even rows (row 1) or all rows (both)
         d = torch.randn(128, generator=torch.Generator().manual_seed(41))
         d = d / d.norm()
-        for m in range(1, M, 2):
+        first = {"spike_in_partner": 1, "spike_in_even": 0}.get(pattern, 0)
+        step = 1 if pattern == "spike_in_both" else 2
+        for m in range(first, M, step):
             Q[:, m * 128:(m + 1) * 128] += 24.0 * d
         K[:, 5 * 128:6 * 128] += 24.0 * d
         Q, K = Q.bfloat16(), K.bfloat16()
-        # the spike overflows the fast reference (2^32 headroom) on odd rows: exact re-run
-        q, k = Q[0, 7 * 128:8 * 128].float(), K[0].float()
+        # the spike overflows the fast reference (2^32 headroom) on those rows: exact re-run
+        r = 6 if pattern == "spike_in_even" else 7          # a spiked row with block 5 in its list
+        q, k = Q[0, r * 128:(r + 1) * 128].float(), K[0].float()
         x = (q @ k.T) / (128 ** 0.5) * 1.4426950408889634
         assert (x[:, 5 * 128:6 * 128].max(1).values - x[:, :128].max(1).values).max() > 32
     rng = np.random.default_rng(42)
@@ -368,7 +374,7 @@ def test_row_pair_kernel_list_patterns(pattern):
             elif pattern == "shifted_first":  # odd rows start at block 1, even rows at block 0
                 base = sorted({odd} | {int(x) for x in rng.choice(max(m, 1), size=min(m, 3), replace=False)}) if m > 1 else []
                 base = [n for n in base if n < m]
-            else:                             # spike: every row sees block 0 first, then block 5
+            else:                             # spikes: every row sees block 0 first, then block 5
                 base = [n for n in (0, 5) if n < m]
             lst = sorted(set(base) | {m})
             cnt[h, m] = len(lst)
