@@ -22,6 +22,10 @@
 
 // A7 kernel choice: the row-pair attn_tc9 at d = b = 128 (PA_ATTN_V9, common.cuh), else attn_tc8
 static bool use_v9(int d, int b) { return PA_ATTN_V9 && b == 128 && d == 128; }
+// ... and for the dense A8 (diagonal-first walk over both rows of a pair; build define for A/B)
+#ifndef PA_ATTN_V9_DENSE
+#define PA_ATTN_V9_DENSE 0
+#endif
 
 namespace {
 
@@ -416,7 +420,7 @@ static int attention(const proxyattn_cfg* cfg, const void* Q, const void* K, con
     if (D.fp32)
         PA_CUDA(pa::launch_attn_simt(D, Q, K, V, block_cnt, block_idx, O, st), "attn_simt");
 #if PA_ATTN_V9
-    else if (block_cnt && use_v9(D.d, D.b))   // A7 at b = 128: the row-pair kernel
+    else if ((block_cnt || PA_ATTN_V9_DENSE) && use_v9(D.d, D.b))   // the row-pair kernel
         PA_CUDA(pa::launch_attn_tc9(D, Q, K, V, block_cnt, block_idx, O, st), "attn_tc9");
 #endif
     else   // block-sparse (A7) or, with no lists, every causal block (A8): the same kernel
