@@ -22,10 +22,7 @@
 
 // A7 kernel choice: the row-pair attn_tc9 at d = b = 128 (PA_ATTN_V9, common.cuh), else attn_tc8
 static bool use_v9(int d, int b) { return PA_ATTN_V9 && b == 128 && d == 128; }
-// ... and for the dense A8 (diagonal-first walk over both rows of a pair; build define for A/B)
-#ifndef PA_ATTN_V9_DENSE
-#define PA_ATTN_V9_DENSE 0
-#endif
+
 
 namespace {
 

@@ -981,7 +981,11 @@ cudaError_t launch_tc8(const Dims& D, const void* Q, const void* K, const void* 
 #endif
     }
     else if (D.d == 128)
+#if PA_ATTN_V9 && PA_ATTN_V9_DENSE
+        kern = D.b == 128 ? nullptr : kernel_with_attr<128, 64, eb64>();   // d = b = 128: attn_tc9
+#else
         kern = D.b == 128 ? kernel_with_attr<128, 128, e128>() : kernel_with_attr<128, 64, eb64>();
+#endif
     else
         kern = D.b == 128 ? kernel_with_attr<64, 128, e64>() : kernel_with_attr<64, 64, e64>();
     if (!kern) return cudaErrorInvalidValue;

@@ -6,6 +6,11 @@
 #ifndef PA_ATTN_V9
 #define PA_ATTN_V9 1
 #endif
+// ... and for the dense A8 (diagonal-first walk over both rows of a pair): 109.4-110.7 vs
+// 111.4-111.5 ms for attn_tc8 at 128K, no exact re-runs (profiles/r03_dense_v9_ab.jsonl)
+#ifndef PA_ATTN_V9_DENSE
+#define PA_ATTN_V9_DENSE 1
+#endif
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
